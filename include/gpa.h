@@ -1,0 +1,243 @@
+/*
+ * gpa.h — C ABI of the B200-native GPU PC-sample attribution library (libgpa).
+ *
+ * Method: Zhou et al., "Measurement and Analysis of GPU-accelerated Applications
+ * with HPCToolkit", Parallel Computing 2021 (arXiv 2109.06931).  Citations below
+ * are "P:<line>" into /root/reference/PAPER.md (read-only copy of the paper's LaTeX)
+ * plus the section they fall in; "Rn" refers to the numbered readings in DESIGN.md
+ * §3 where the paper is silent or ambiguous.
+ *
+ * The library implements the data-parallel analysis path the paper describes:
+ *   a-1..a-3  PC-sample decode, pc -> instruction range lookup, per-instruction x
+ *             stall-reason histogram                        (§4.2, §4.5 P:475-479,
+ *                                                           §5)
+ *   a-4       cross-GPU combine (caller: NCCL reduce of the histogram; §5.1)
+ *   a-5       roll-up to lines / loops / inlined code / functions  (§5.1)
+ *   a-6..a-9  approximate GPU calling-context tree (§5.3, Steps 1-4)
+ *   a-10      PC-sample-derived metrics, e.g. Warp Issue Rate W=(S-S_stall)/S (§6.1)
+ *
+ * Conventions shared by every entry point:
+ *  - "d_" pointers are DEVICE pointers on the structure's device; "h_" pointers are host.
+ *  - Every call that takes a cudaStream_t only ENQUEUES work on that stream unless its
+ *    comment says it synchronizes.  Completion/ordering of caller buffers is the caller's job.
+ *  - Errors are status codes; nothing aborts.  gpa_last_error() returns a thread-local
+ *    message describing the most recent non-OK status on the calling thread.
+ *  - Asynchronous device faults surface as GPA_ERR_CUDA at the next synchronizing call.
+ *  - Handles are immutable after creation and may be used concurrently from several
+ *    host threads / streams.
+ */
+#ifndef GPA_H
+#define GPA_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without pulling in cuda_runtime.h (identical ABI: an opaque pointer). */
+typedef struct CUstream_st *gpa_stream_t;
+
+/* ---- constants (readings R2/R3/R5) -------------------------------------- */
+#define GPA_SLOTS        16          /* histogram slots per instruction row                  */
+#define GPA_VALID_SLOTS  12          /* slots 0..11 = stall reasons (R2); 12..14 always 0     */
+#define GPA_SLOT_INVALID 15          /* a record whose stall field is >= 12 lands here (R2)   */
+#define GPA_CLASSES      16          /* instruction classes (R5)                       */
+#define GPA_NUM_DERIVED  33          /* derived columns per row (R3-R5, DESIGN.md §3 table)    */
+#define GPA_NONE         0xFFFFFFFFu /* "no index" in every u32 index array                    */
+
+/* Stall slots, modeled on CUPTI's PC-sampling stall enumeration (R2; the paper only says
+ * "a stall reason").  Slot 0 = the warp issued (not stalled); W uses it. */
+enum {
+  GPA_STALL_NONE = 0, GPA_STALL_INST_FETCH = 1, GPA_STALL_EXEC_DEPENDENCY = 2,
+  GPA_STALL_MEMORY_DEPENDENCY = 3, GPA_STALL_TEXTURE = 4, GPA_STALL_SYNC = 5,
+  GPA_STALL_CONSTANT_MEMORY_DEPENDENCY = 6, GPA_STALL_PIPE_BUSY = 7,
+  GPA_STALL_MEMORY_THROTTLE = 8, GPA_STALL_NOT_SELECTED = 9, GPA_STALL_OTHER = 10,
+  GPA_STALL_SLEEPING = 11
+};
+
+typedef enum {
+  GPA_OK = 0,
+  GPA_ERR_INVALID_ARG = 1,   /* NULL pointer with n>0, misaligned sample buffer, bad enum,
+                                pointer not on the handle's device                         */
+  GPA_ERR_STRUCTURE = 2,     /* gpa_load_structure / gpa_validate_structure: malformed desc */
+  GPA_ERR_CAPACITY = 3,      /* gpa_reconstruct_cct: more contexts than max_contexts        */
+  GPA_ERR_OUT_OF_MEMORY = 4, /* device or host allocation failed                             */
+  GPA_ERR_CUDA = 5,          /* a CUDA runtime call or kernel launch failed                  */
+  GPA_ERR_INTERNAL = 6,      /* invariant violated inside the library (a bug)                */
+  GPA_ERR_UNSUPPORTED = 7    /* feature not built (e.g. GPA_WEIGHTS_EXACT)                   */
+} gpa_status;
+
+/* Scope kinds of the program-structure tree ("procedures, inlined functions,
+ * loop nests, and source lines").  FUNCTION scopes are roots; LINE scopes are
+ * leaves and every instruction's innermost scope (R7, R8). */
+typedef enum { GPA_KIND_FUNCTION = 0, GPA_KIND_INLINE = 1, GPA_KIND_LOOP = 2,
+               GPA_KIND_LINE = 3 } gpa_scope_kind;
+
+/* Row sets gpa_derive_metrics can produce. */
+typedef enum {
+  GPA_SCOPE_INST = 0,     /* one row per instruction (rows = n_inst)                           */
+  GPA_SCOPE_LINE = 1,     /* one row per LINE scope, ascending scope id (leaf rows, R8)          */
+  GPA_SCOPE_LOOP = 2,     /* one row per LOOP scope, ascending scope id (inclusive, R8)          */
+  GPA_SCOPE_INLINE = 3,   /* one row per INLINE scope, ascending scope id (inclusive, R8)        */
+  GPA_SCOPE_FUNC = 4,     /* one row per function f (row f = func_scope[f]; inclusive; flat view
+                             P:936-937)                                                          */
+  GPA_SCOPE_CCT_EXCL = 5, /* one row per CCT context: exclusive apportioned samples  */
+  GPA_SCOPE_CCT_INCL = 6  /* one row per CCT context: inclusive (context + descendants)          */
+} gpa_scope;
+
+/* CCT context kinds (R14). */
+typedef enum { GPA_CTX_FUNC = 0, GPA_CTX_SCC = 1, GPA_CTX_SCC_MEMBER = 2 } gpa_ctx_kind;
+
+/* Step-1 edge weights: call-instruction sample counts, or exact call counts. */
+typedef enum { GPA_WEIGHTS_SAMPLES = 0, GPA_WEIGHTS_EXACT = 1 } gpa_weight_mode;
+
+/* One PC sample as a sampler delivers it ("an instruction address, a stall
+ * reason, and a count").  16 bytes, little-endian, 16-byte aligned (one 128-bit load).
+ * pc: relocated module offset (R1).  stall: reason code; >= 12 is invalid data (R2).
+ * stream: profile slot (GPU stream / rank); read but not used by the histogram. */
+typedef struct {
+  uint64_t pc;
+  uint32_t count;
+  uint16_t stall;
+  uint16_t stream;
+} gpa_sample;
+
+/* Program structure of ONE load module (R1).  HOST arrays, copied by
+ * gpa_load_structure; the caller keeps ownership and may free them after the call.
+ * Validation (GPA_ERR_STRUCTURE) rejects: inst_addr not strictly ascending; inst_len == 0;
+ * overlapping ranges ([addr,addr+len) must be disjoint, R6) or addr+len overflowing u64;
+ * inst_scope not a LINE scope; scope_parent out of range / cyclic; a FUNCTION scope with a
+ * parent or a non-FUNCTION scope without one; a LINE scope that is some scope's parent;
+ * func_scope not a bijection onto the FUNCTION scopes; call_inst / call_callee out of range;
+ * two call sites on the same instruction (direct calls only, R22); inst_class > 15;
+ * scope_kind > 3. */
+typedef struct {
+  uint32_t n_inst;
+  const uint64_t *inst_addr;    /* [n_inst] strictly ascending relocated start addresses    */
+  const uint16_t *inst_len;     /* [n_inst] length in bytes (> 0)                            */
+  const uint8_t  *inst_class;   /* [n_inst] class 0..15 (R5)                          */
+  const uint32_t *inst_scope;   /* [n_inst] innermost scope, a LINE scope                    */
+  uint32_t n_scope;
+  const uint32_t *scope_parent; /* [n_scope] parent scope, GPA_NONE for FUNCTION scopes      */
+  const uint8_t  *scope_kind;   /* [n_scope] gpa_scope_kind                                  */
+  uint32_t n_func;
+  const uint32_t *func_scope;   /* [n_func] the FUNCTION scope of function f                 */
+  uint32_t n_call;
+  const uint32_t *call_inst;    /* [n_call] instruction index of call site e          */
+  const uint32_t *call_callee;  /* [n_call] callee function of call site e (direct calls)    */
+} gpa_structure_desc;
+
+typedef struct gpa_structure_s *gpa_structure;  /* device-resident, immutable after load */
+typedef struct gpa_cct_s *gpa_cct;              /* library-owned CCT result               */
+
+typedef struct {
+  uint32_t n_inst, n_scope, n_line, n_loop, n_inline, n_func, n_call;
+  uint32_t n_dag;          /* nodes of the SCC-condensed call graph (Step 3)       */
+  uint32_t n_scc;          /* non-trivial SCCs (>= 2 members, or a self-call; R14)            */
+  uint32_t dag_levels;     /* longest root->node chain in the condensed DAG (+1)              */
+  uint64_t cct_path_bound; /* contexts if every call site had weight > 0 (saturating)         */
+  uint32_t lookup_mode;    /* 0 = direct granule map, 1 = sorted-range binary search          */
+  uint32_t granule_shift;  /* log2 of the granule size of the direct map                      */
+  uint64_t lookup_entries; /* entries of the direct map (0 in mode 1)                         */
+  uint64_t device_bytes;   /* device memory held by the handle                                */
+} gpa_structure_info;
+
+/* Read-only DEVICE views of a CCT (valid until gpa_free_cct).  Contexts are numbered in
+ * breadth-first order (R17): roots first (ascending DAG id), then level by level; the
+ * children of a context are contiguous, ordered by ascending call instruction (for call
+ * children) or ascending member function id (for SCC members). */
+typedef struct {
+  uint64_t n;                  /* contexts                                                    */
+  const uint32_t *parent;      /* [n] parent context or GPA_NONE for roots                   */
+  const uint32_t *site;        /* [n] call site e that created it, GPA_NONE for roots/members */
+  const uint32_t *node;        /* [n] DAG node id (FUNC/SCC) or function id (SCC_MEMBER)     */
+  const uint8_t  *kind;        /* [n] gpa_ctx_kind                                            */
+  const uint32_t *first_child; /* [n] index of first child (valid when n_children > 0)        */
+  const uint32_t *n_children;  /* [n]                                                         */
+  const double   *frac;        /* [n] apportioning fraction f (product form, R13)             */
+  const double   *excl;        /* [n*16] f * S_function (0 for SCC contexts)                  */
+  const double   *incl;        /* [n*16] excl + sum of children's incl, in child order        */
+  /* Step-1..3 intermediates, exposed for verification: */
+  uint32_t n_call, n_func, n_dag;
+  const uint64_t *call_weight; /* [n_call] w_e after Step 2 and the DAG guard (R11, R12)      */
+  const uint64_t *dag_weight;  /* [n_dag] W_X = sum of external in-edge weights              */
+  const uint8_t  *dag_active;  /* [n_dag]                                                     */
+  const uint8_t  *func_active; /* [n_func] after Step 2                                       */
+  const uint64_t *func_hist;   /* [n_func*16] S_f                                             */
+} gpa_cct_view;
+
+/* ---- version / host-only queries ------------------------------------------------------ */
+const char *gpa_version(void);
+/* Message for the most recent non-OK status on this thread ("" if none). */
+const char *gpa_last_error(void);
+/* Validate a structure description on the host only (no device touched).  Same checks and
+ * status as gpa_load_structure. */
+gpa_status gpa_validate_structure(const gpa_structure_desc *desc);
+
+/* ---- structure ------------------------------------------------------------------------ */
+/* Validate desc, derive the load-time tables (pc->instruction map, roll-up CSR, call-graph
+ * CSR, Tarjan SCC condensation of the STATIC call graph (Step 3: weights do not
+ * change the SCCs), DAG levels) and upload them to `device`.  Synchronous. */
+gpa_status gpa_load_structure(const gpa_structure_desc *desc, int device, gpa_structure *out);
+gpa_status gpa_get_structure_info(gpa_structure s, gpa_structure_info *out);
+/* Rows produced for `scope` and, if h_ids != NULL, the id behind each row: instruction
+ * index (INST), scope id (LINE/LOOP/INLINE) or function id (FUNC).  Host only. */
+gpa_status gpa_scope_rows(gpa_structure s, gpa_scope scope, uint64_t *rows, uint32_t *h_ids);
+/* h_scc_of[f] = DAG node of function f (DAG ids ascend with their smallest member). */
+gpa_status gpa_get_scc(gpa_structure s, uint32_t *h_scc_of);
+void gpa_free_structure(gpa_structure s);
+
+/* ---- a-1..a-3: attribution -------------------------------------------------------------
+ * For every record k in d_samples[0..n):  slot = stall < 12 ? stall : 15;
+ *   i = the instruction with inst_addr[i] <= pc < inst_addr[i] + inst_len[i] (R6)
+ *   found:  d_inst_hist[i*16 + slot] += count       (raw metric = sum)
+ *   else:   d_unattributed[slot]     += count
+ *   d_rec_inst[k] = i or GPA_NONE (only if d_rec_inst != NULL).
+ * Outputs ACCUMULATE (+=, u64): the caller zeroes them; calling again on further chunks
+ * or from several streams is how streams are chunked/resumed.  d_samples must be 16-byte
+ * aligned.  n == 0 is a no-op.  Enqueue-only on `stream`. */
+gpa_status gpa_attribute_samples(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+                                 uint64_t *d_inst_hist, uint64_t *d_unattributed,
+                                 uint32_t *d_rec_inst, gpa_stream_t stream);
+/* Same result from HOST records: the library streams h_samples to the device in chunks
+ * (pipelined host->device copy overlapped with the attribution kernel) using internal
+ * staging buffers.  h_samples may be pageable or pinned (pinned is copied directly).
+ * Synchronizes `stream` before returning. */
+gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_samples, uint64_t n,
+                                      uint64_t *d_inst_hist, uint64_t *d_unattributed,
+                                      gpa_stream_t stream);
+
+/* ---- a-6..a-9: approximate GPU calling-context tree (§5.3) -----------------
+ * From a per-instruction histogram: Step 1 edge weights w_e = sum_{r<12} H[call_inst[e]][r]
+ * (R10); Step 2 zero-weight propagation to the least fixpoint (R11) and the
+ * DAG guard (R12); Step 3 uses the load-time SCC condensation; Step 4 splits
+ * the DAG into a tree, apportioning by f(child) = f(parent) * w_e / W_callee (P:880-881,
+ * R13-R16).  max_contexts == 0: count only (*out untouched, *n_contexts = required).
+ * More contexts than max_contexts -> GPA_ERR_CAPACITY with *n_contexts = required.
+ * Synchronizes `stream` (the context count decides the allocation). */
+gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist,
+                               gpa_weight_mode mode, uint64_t max_contexts,
+                               gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream);
+gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *out);
+void gpa_free_cct(gpa_cct c);
+
+/* ---- a-5 + a-10: roll-up and derived metrics -------------------------------------------
+ * INST..FUNC: rows of `scope` (see gpa_scope_rows).  Row histogram (u64[16]) =
+ *   sum of H over the instructions whose scope chain contains the row's scope (R8);
+ *   mix (u64[16]) = per instruction class k, sum of S(i) = sum_{r<12} H[i][r] (R5).
+ * CCT_EXCL / CCT_INCL: rows = contexts of `cct` (excl / incl vectors; no mix, no u64 out).
+ * d_metrics[row*33 + c] (DESIGN.md §3 table; NaN = 0x7FF8000000000000 when S == 0, R18):
+ *   0 S  1 W=v0/S  2 (v0+v9)/S  3 sum_{LAT} v/S  4..15 v[r]/S  16 v[15]
+ *   17..32 mix[k]/S (NaN for CCT rows).
+ * Any of d_scope_hist, d_scope_mix, d_metrics may be NULL.  For INST rows d_scope_hist
+ * receives a copy of d_inst_hist.  Enqueue-only on `stream`. */
+gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist,
+                              gpa_cct cct, uint64_t *d_scope_hist, uint64_t *d_scope_mix,
+                              double *d_metrics, gpa_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPA_H */

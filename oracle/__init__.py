@@ -1,0 +1,210 @@
+"""CPU oracle for the PC-sample attribution path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference` legs
+may import this package.  The product (paper_2109_06931_b200) never does, and the two
+share no code: this is a ctypes wrapper over oracle/gpa_oracle.c, a plain C transcription
+of the paper's definitions (D1-D7, see that file's header and DESIGN.md §3).
+
+Structures are dicts of numpy arrays with the keys of gpa_structure_desc
+(inst_addr, inst_len, inst_class, inst_scope, scope_parent, scope_kind, func_scope,
+call_inst, call_callee); records are 16-byte (pc u64, count u32, stall u16, stream u16).
+"""
+from __future__ import annotations
+
+import ctypes
+import functools
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+SRC = os.path.join(HERE, "gpa_oracle.c")
+NONE = 0xFFFFFFFF
+SLOTS, VALID, NCOLS = 16, 12, 33
+KIND_FUNCTION, KIND_INLINE, KIND_LOOP, KIND_LINE = 0, 1, 2, 3
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+
+class _CctResult(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64), ("cap", ctypes.c_uint64),
+        ("parent", _u32p), ("site", _u32p), ("node", _u32p), ("first_child", _u32p),
+        ("n_children", _u32p), ("kind", _u8p), ("frac", _f64p), ("excl", _f64p), ("incl", _f64p),
+        ("n_func", ctypes.c_uint32), ("n_call", ctypes.c_uint32), ("n_dag", ctypes.c_uint32),
+        ("w_step1", _u64p), ("w", _u64p), ("func_active", _u8p), ("S_f", _u64p),
+        ("scc_of", _u32p), ("dag_nontrivial", _u8p), ("dag_active", _u8p), ("W", _u64p),
+        ("status", ctypes.c_int),
+    ]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2 -ffp-contract=off: one IEEE op per written operation)."""
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(SRC) > os.path.getmtime(LIB_PATH):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-shared", "-fPIC",
+                               "-o", LIB_PATH, SRC, "-lpthread"])
+    return LIB_PATH
+
+
+@functools.lru_cache(None)
+def _lib():
+    build()
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, u32, u64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64
+    lib.oracle_attribute.argtypes = [u32, vp, vp, vp, u64, vp, vp, vp]
+    lib.oracle_attribute.restype = None
+    lib.oracle_attribute_mt.argtypes = [u32, vp, vp, vp, u64, vp, vp, ctypes.c_int]
+    lib.oracle_attribute_mt.restype = ctypes.c_int
+    lib.oracle_rollup.argtypes = [u32, vp, vp, u32, vp, vp, vp, vp]
+    lib.oracle_rollup.restype = None
+    lib.oracle_inst_func.argtypes = [u32, vp, u32, vp, u32, vp, vp]
+    lib.oracle_inst_func.restype = None
+    lib.oracle_cct.argtypes = [u32, vp, u32, vp, u32, vp, u32, vp, vp, vp, u64]
+    lib.oracle_cct.restype = ctypes.POINTER(_CctResult)
+    lib.oracle_cct_free.argtypes = [ctypes.POINTER(_CctResult)]
+    lib.oracle_cct_free.restype = None
+    lib.oracle_derive_u64.argtypes = [u64, vp, vp, vp]
+    lib.oracle_derive_u64.restype = None
+    lib.oracle_derive_f64.argtypes = [u64, vp, vp]
+    lib.oracle_derive_f64.restype = None
+    return lib
+
+
+def _c(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, (a.ctypes.data if a.size else None)
+
+
+def _records(rec) -> np.ndarray:
+    rec = np.ascontiguousarray(rec)
+    if rec.dtype.itemsize != 16:
+        raise ValueError("records must be 16-byte items")
+    return rec
+
+
+# ---- D1 ---------------------------------------------------------------------------------
+def attribute(st: dict, rec, rec_inst: bool = False, threads: int = 1):
+    """D1: returns (H [n_inst,16] u64, U [16] u64, rec_inst [n] u32 or None)."""
+    rec = _records(rec)
+    n_inst = len(st["inst_addr"])
+    addr, pa = _c(st["inst_addr"], np.uint64)
+    ln, pl = _c(st["inst_len"], np.uint16)
+    H = np.zeros((n_inst, SLOTS), np.uint64)
+    U = np.zeros(SLOTS, np.uint64)
+    ri = np.empty(len(rec), np.uint32) if rec_inst else None
+    if threads > 1 and not rec_inst:
+        _lib().oracle_attribute_mt(n_inst, pa, pl, rec.ctypes.data if len(rec) else None, len(rec),
+                                   H.ctypes.data, U.ctypes.data, threads)
+    else:
+        _lib().oracle_attribute(n_inst, pa, pl, rec.ctypes.data if len(rec) else None, len(rec),
+                                H.ctypes.data, U.ctypes.data, ri.ctypes.data if ri is not None and len(rec) else None)
+    return H, U, ri
+
+
+# ---- D2 ---------------------------------------------------------------------------------
+def rollup(st: dict, H):
+    """D2: per-scope inclusive histograms and sample-weighted class mix, by scope id."""
+    n_inst, n_scope = len(st["inst_addr"]), len(st["scope_parent"])
+    Hc, ph = _c(H, np.uint64)
+    Hs = np.zeros((n_scope, SLOTS), np.uint64)
+    MIX = np.zeros((n_scope, SLOTS), np.uint64)
+    a_s, ps = _c(st["inst_scope"], np.uint32)
+    a_c, pc = _c(st["inst_class"], np.uint8)
+    a_p, pp = _c(st["scope_parent"], np.uint32)
+    _lib().oracle_rollup(n_inst, ps, pc, n_scope, pp, ph, Hs.ctypes.data if n_scope else None,
+                         MIX.ctypes.data if n_scope else None)
+    return Hs, MIX
+
+
+def inst_func(st: dict) -> np.ndarray:
+    n_inst = len(st["inst_addr"])
+    out = np.empty(n_inst, np.uint32)
+    a = [_c(st[k], np.uint32) for k in ("inst_scope", "scope_parent", "func_scope")]
+    _lib().oracle_inst_func(n_inst, a[0][1], len(st["scope_parent"]), a[1][1], len(st["func_scope"]),
+                            a[2][1], out.ctypes.data if n_inst else None)
+    return out
+
+
+def scope_rows(st: dict, scope: str) -> np.ndarray:
+    """Row ids of a scope set: 'INST' instruction ids, 'LINE'/'LOOP'/'INLINE' ascending scope
+    ids of that kind, 'FUNC' function ids (the row order gpa_derive_metrics documents)."""
+    kinds = {"LINE": KIND_LINE, "LOOP": KIND_LOOP, "INLINE": KIND_INLINE}
+    if scope == "INST":
+        return np.arange(len(st["inst_addr"]), dtype=np.uint32)
+    if scope == "FUNC":
+        return np.arange(len(st["func_scope"]), dtype=np.uint32)
+    return np.nonzero(np.asarray(st["scope_kind"]) == kinds[scope])[0].astype(np.uint32)
+
+
+def scope_hist(st: dict, H, scope: str):
+    """(hist [rows,16], mix [rows,16]) of a scope set, from D2 (INST rows: H itself and the
+    per-instruction class mix)."""
+    H = np.asarray(H, np.uint64)
+    if scope == "INST":
+        S = H[:, :VALID].sum(1, dtype=np.uint64)
+        mix = np.zeros_like(H)
+        mix[np.arange(len(H)), np.asarray(st["inst_class"], np.int64)] = S
+        return H.copy(), mix
+    Hs, MIX = rollup(st, H)
+    ids = scope_rows(st, scope)
+    if scope == "FUNC":
+        ids = np.asarray(st["func_scope"], np.int64)
+    return Hs[ids], MIX[ids]
+
+
+# ---- D3-D6 ------------------------------------------------------------------------------
+def cct(st: dict, H, max_contexts: int = (1 << 63)) -> dict:
+    """D3-D6: the approximate GPU CCT (BFS numbering) and the Step 1-3 intermediates."""
+    n_inst, n_scope = len(st["inst_addr"]), len(st["scope_parent"])
+    n_func, n_call = len(st["func_scope"]), len(st["call_inst"])
+    a = {k: _c(st[k], np.uint32) for k in ("inst_scope", "scope_parent", "func_scope", "call_inst", "call_callee")}
+    Hc, ph = _c(H, np.uint64)
+    r = _lib().oracle_cct(n_inst, a["inst_scope"][1], n_scope, a["scope_parent"][1], n_func,
+                          a["func_scope"][1], n_call, a["call_inst"][1], a["call_callee"][1], ph, max_contexts)
+    try:
+        R = r.contents
+        n, nd = int(R.n), int(R.n_dag)
+
+        def arr(p, cnt, dt):
+            if cnt == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(p, shape=(cnt,)).astype(dt, copy=True)
+
+        out = dict(
+            n=n, status=int(R.status), n_dag=nd,
+            parent=arr(R.parent, n, np.uint32), site=arr(R.site, n, np.uint32), node=arr(R.node, n, np.uint32),
+            kind=arr(R.kind, n, np.uint8), first_child=arr(R.first_child, n, np.uint32),
+            n_children=arr(R.n_children, n, np.uint32), frac=arr(R.frac, n, np.float64),
+            excl=arr(R.excl, n * SLOTS, np.float64).reshape(n, SLOTS),
+            incl=arr(R.incl, n * SLOTS, np.float64).reshape(n, SLOTS),
+            w_step1=arr(R.w_step1, n_call, np.uint64), w=arr(R.w, n_call, np.uint64),
+            func_active=arr(R.func_active, n_func, np.uint8),
+            S_f=arr(R.S_f, n_func * SLOTS, np.uint64).reshape(n_func, SLOTS),
+            scc_of=arr(R.scc_of, n_func, np.uint32), dag_nontrivial=arr(R.dag_nontrivial, nd, np.uint8),
+            dag_active=arr(R.dag_active, nd, np.uint8), W=arr(R.W, nd, np.uint64))
+    finally:
+        _lib().oracle_cct_free(r)
+    return out
+
+
+# ---- D7 ---------------------------------------------------------------------------------
+def derive_u64(V, MIX=None) -> np.ndarray:
+    V = np.ascontiguousarray(V, np.uint64).reshape(-1, SLOTS)
+    out = np.empty((len(V), NCOLS), np.float64)
+    M = None if MIX is None else np.ascontiguousarray(MIX, np.uint64).reshape(-1, SLOTS)
+    if len(V):
+        _lib().oracle_derive_u64(len(V), V.ctypes.data, None if M is None else M.ctypes.data, out.ctypes.data)
+    return out
+
+
+def derive_f64(V) -> np.ndarray:
+    V = np.ascontiguousarray(V, np.float64).reshape(-1, SLOTS)
+    out = np.empty((len(V), NCOLS), np.float64)
+    if len(V):
+        _lib().oracle_derive_f64(len(V), V.ctypes.data, out.ctypes.data)
+    return out
