@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the PC-sample attribution path (BASELINE.json metric: PC samples
+attributed/sec and % of HBM roofline, vs the CPU oracle).
+
+One step = one pass of the whole hot path over one batch (DESIGN.md §1 rows a-1..a-10):
+zero H||U, attribute this rank's shard of the record stream (K_attr), NCCL-reduce H||U to
+rank 0 (N > 1), then on rank 0 roll up + derive metrics for INST/LINE/LOOP/INLINE/FUNC,
+reconstruct the CCT and derive its EXCL/INCL metrics.  Inputs are generated on the device
+(untimed) and are 64 GB at C5, far larger than the 126 MB L2, so no L2 flush is needed.
+
+    python bench.py [--gpus N --steps K --warmup W --config C5]        (torchrun for N > 1)
+    python bench.py --impl reference ...                              (the CPU oracle arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PC samples attributed/sec"
+UNIT = "samples/s"
+SCOPES = ["INST", "LINE", "LOOP", "INLINE", "FUNC"]
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [l.split(", ") for l in open(self.path).read().strip().splitlines() if l.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if len(r) > 5 + j and "Active" in r[5 + j]
+                          and "Not" not in r[5 + j]})
+        loaded = [x for x in sm if x >= 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def _dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------------------
+def oracle_pass(w, n_sample: int, k0: int, threads: int):
+    """Time the oracle on records [k0, k0+n_sample): D1 attribution on `threads` cores
+    (thread-private histograms, serial merge) + D2 roll-up + D3-D6 CCT + D7 metrics
+    (single-threaded, the oracle as it stands).  Host generation is untimed."""
+    import numpy as np
+    import oracle
+    rec = w.records_host(k0, n_sample)
+    st = w.structure
+    t0 = time.perf_counter()
+    H, U, _ = oracle.attribute(st, rec, threads=threads)
+    t1 = time.perf_counter()
+    for sc in SCOPES:
+        h, m = oracle.scope_hist(st, H, sc)
+        oracle.derive_u64(h, m)
+    R = oracle.cct(st, H)
+    oracle.derive_f64(R["excl"])
+    oracle.derive_f64(R["incl"])
+    t2 = time.perf_counter()
+    del rec
+    return t2 - t0, t1 - t0, t2 - t1, int(np.asarray(H).sum() + np.asarray(U).sum())
+
+
+def cpu_baseline(w, target_s: float = 12.0):
+    cores = len(os.sched_getaffinity(0))
+    # calibrate attribution speed on 2^21 records, then size the sample for ~target_s
+    t, ta, tr, _ = oracle_pass(w, 1 << 21, 0, cores)
+    per_rec = ta / (1 << 21)
+    n = int(min(w.cfg.records, max(1 << 21, (target_s - tr) / max(per_rec, 1e-12))))
+    n = min(n, 1 << 28)
+    t, ta, tr, _ = oracle_pass(w, n, 0, cores)
+    return {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {n} records of {w.cfg.name} ({w.cfg.records} total); whole path: D1 attribution "
+                      f"({cores} threads, {ta:.2f} s) + roll-up/derive/CCT ({tr:.2f} s, 1 thread)",
+            "seconds": t, "attr_seconds": ta, "rest_seconds": tr}
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    import gen
+    w = gen.workload(args.config)
+    cores = len(os.sched_getaffinity(0))
+    n = args.ref_sample
+    times = []
+    for i in range(args.warmup + args.steps):
+        k0 = (i * n) % max(1, w.cfg.records - n)
+        t, ta, tr, _ = oracle_pass(w, n, k0, cores)
+        if i >= args.warmup:
+            times.append(t)
+    t = sum(times) / len(times)
+    val = n / t
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+            "config": {"workload": w.cfg.name, "records": w.cfg.records, "sample_per_step": n,
+                       "n_inst": w.meta["n_inst"], "n_func": w.meta["n_func"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} records per step of {w.cfg.name}, whole path"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+def run_gpa(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    from paper_2109_06931_b200 import gpa
+    from paper_2109_06931_b200.parallel import reduce_histogram, shard_range
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = gen.workload(args.config, records=args.records)
+    n_all = w.cfg.records
+    a, b = shard_range(n_all, rank, world)
+    n = b - a
+    s = gpa.load_structure(w.structure, local)
+    ni = s.info["n_inst"]
+    stream = torch.cuda.current_stream(dev)
+
+    rec = torch.empty((max(n, 1), 2), dtype=torch.int64, device=dev)
+    CH = 1 << 28
+    for k in range(0, n, CH):
+        w.records_device(rec[k:k + CH], a + k, min(CH, n - k))
+    torch.cuda.synchronize()
+    HU = torch.zeros(ni * 16 + 16, dtype=torch.int64, device=dev)   # H_inst || U, one buffer
+    H, U = HU[:ni * 16].view(ni, 16), HU[ni * 16:]
+    rows = {sc: max(1, gpa.scope_row_count(s, sc)) for sc in SCOPES}
+    met = {sc: torch.empty((rows[sc], gpa.NUM_DERIVED), dtype=torch.float64, device=dev) for sc in SCOPES}
+    ev_a0, ev_a1 = [], []
+
+    def step(timed: bool):
+        HU.zero_()
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        gpa.attribute_samples(s, rec, H, U, n=n, stream=stream)
+        if timed:
+            e1.record(stream)
+            ev_a0.append(e0)
+            ev_a1.append(e1)
+        reduce_histogram(HU, dst=0)
+        if rank == 0:
+            for sc in SCOPES:
+                gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=stream)
+            cct = gpa.reconstruct_cct(s, H, stream=stream)
+            cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+            gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
+            gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+            stream.synchronize()
+            nctx = cct.n
+            cct.free()
+            return nctx
+        return 0
+
+    for _ in range(args.warmup):
+        nctx = step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = gpa._lib.gpa_kernel_launches()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            nctx = step(True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = gpa._lib.gpa_kernel_launches() - l0
+    ms = t0.elapsed_time(t1) / args.steps
+    attr_ms = sum(x.elapsed_time(y) for x, y in zip(ev_a0, ev_a1)) / len(ev_a0)
+    if world > 1:
+        t = torch.tensor([ms, attr_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, attr_ms = t.tolist()
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    clocks = clk.summary()
+
+    # e2e: the same step through the C ABI with HOST records (pinned), H2D inside the timed
+    # region (gpa_attribute_samples_host pipelines the copies), D2H of the step's results.
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((n, 2), dtype=torch.int64, pin_memory=True)
+        w.records_host(a, n, out=host.numpy().view(gen.RECORD_DTYPE).reshape(-1))
+        res_h = torch.empty(HU.numel(), dtype=torch.int64, pin_memory=True)
+        fm_h = torch.empty(met["FUNC"].shape, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            HU.zero_()
+            gpa.attribute_samples_host(s, host, H, U, stream=stream)
+            reduce_histogram(HU, dst=0)
+            if rank == 0:
+                for sc in SCOPES:
+                    gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=stream)
+                cct = gpa.reconstruct_cct(s, H, stream=stream)
+                cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+                gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+                res_h.copy_(HU, non_blocking=True)
+                fm_h.copy_(met["FUNC"], non_blocking=True)
+                stream.synchronize()
+                cct.free()
+
+        e_w = min(args.warmup, 1) if args.e2e_steps else args.warmup
+        e_k = args.e2e_steps or args.steps
+        for _ in range(e_w):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(e_k):
+            e2e_step()
+        q1.record(stream)
+        torch.cuda.synchronize()
+        ems = q0.elapsed_time(q1) / e_k
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": n_all / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * n_all,
+               "d2h_bytes_per_step": (res_h.numel() * 8 + fm_h.numel() * 8) if rank == 0 else 0,
+               "ms_per_step": ems, "steps": e_k}
+        del host
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = _peaks()
+    algo_bytes = 16 * n                              # per K_attr launch
+    achieved = algo_bytes / (attr_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"k_attr_traffic_{w.cfg.name}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {"metric": METRIC, "value": n_all / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+            "config": {"workload": w.cfg.name, "records": n_all, "records_per_gpu": n, "n_inst": ni,
+                       "n_func": s.info["n_func"], "n_call": s.info["n_call"], "cct_contexts": int(nctx),
+                       "parallelism": f"record shards x{world}, NCCL reduce of H||U",
+                       "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_attribute",
+                         "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
+            "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--records", type=int, default=None, help="override the config's record count")
+    ap.add_argument("--impl", default="gpa", choices=["gpa", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-sample", type=int, default=1 << 26)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "gpa":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpa(args)
+
+
+if __name__ == "__main__":
+    main()

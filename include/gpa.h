@@ -36,6 +36,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define GPA_API __attribute__((visibility("default")))
+#else
+#define GPA_API
+#endif
+
 /* cudaStream_t without pulling in cuda_runtime.h (identical ABI: an opaque pointer). */
 typedef struct CUstream_st *gpa_stream_t;
 
@@ -112,7 +118,7 @@ typedef struct {
  * parent or a non-FUNCTION scope without one; a LINE scope that is some scope's parent;
  * func_scope not a bijection onto the FUNCTION scopes; call_inst / call_callee out of range;
  * two call sites on the same instruction (direct calls only, R22); inst_class > 15;
- * scope_kind > 3. */
+ * scope_kind > 3; n_inst > 2^28 - 16. */
 typedef struct {
   uint32_t n_inst;
   const uint64_t *inst_addr;    /* [n_inst] strictly ascending relocated start addresses    */
@@ -169,25 +175,28 @@ typedef struct {
 } gpa_cct_view;
 
 /* ---- version / host-only queries ------------------------------------------------------ */
-const char *gpa_version(void);
+GPA_API const char *gpa_version(void);
 /* Message for the most recent non-OK status on this thread ("" if none). */
-const char *gpa_last_error(void);
+GPA_API const char *gpa_last_error(void);
+/* Kernels this process has launched through the library so far (all devices; a
+ * diagnostic counter for benchmarks: launches inside a timed region = difference). */
+GPA_API uint64_t gpa_kernel_launches(void);
 /* Validate a structure description on the host only (no device touched).  Same checks and
  * status as gpa_load_structure. */
-gpa_status gpa_validate_structure(const gpa_structure_desc *desc);
+GPA_API gpa_status gpa_validate_structure(const gpa_structure_desc *desc);
 
 /* ---- structure ------------------------------------------------------------------------ */
 /* Validate desc, derive the load-time tables (pc->instruction map, roll-up CSR, call-graph
  * CSR, Tarjan SCC condensation of the STATIC call graph (Step 3: weights do not
  * change the SCCs), DAG levels) and upload them to `device`.  Synchronous. */
-gpa_status gpa_load_structure(const gpa_structure_desc *desc, int device, gpa_structure *out);
-gpa_status gpa_get_structure_info(gpa_structure s, gpa_structure_info *out);
+GPA_API gpa_status gpa_load_structure(const gpa_structure_desc *desc, int device, gpa_structure *out);
+GPA_API gpa_status gpa_get_structure_info(gpa_structure s, gpa_structure_info *out);
 /* Rows produced for `scope` and, if h_ids != NULL, the id behind each row: instruction
  * index (INST), scope id (LINE/LOOP/INLINE) or function id (FUNC).  Host only. */
-gpa_status gpa_scope_rows(gpa_structure s, gpa_scope scope, uint64_t *rows, uint32_t *h_ids);
+GPA_API gpa_status gpa_scope_rows(gpa_structure s, gpa_scope scope, uint64_t *rows, uint32_t *h_ids);
 /* h_scc_of[f] = DAG node of function f (DAG ids ascend with their smallest member). */
-gpa_status gpa_get_scc(gpa_structure s, uint32_t *h_scc_of);
-void gpa_free_structure(gpa_structure s);
+GPA_API gpa_status gpa_get_scc(gpa_structure s, uint32_t *h_scc_of);
+GPA_API void gpa_free_structure(gpa_structure s);
 
 /* ---- a-1..a-3: attribution -------------------------------------------------------------
  * For every record k in d_samples[0..n):  slot = stall < 12 ? stall : 15;
@@ -198,14 +207,14 @@ void gpa_free_structure(gpa_structure s);
  * Outputs ACCUMULATE (+=, u64): the caller zeroes them; calling again on further chunks
  * or from several streams is how streams are chunked/resumed.  d_samples must be 16-byte
  * aligned.  n == 0 is a no-op.  Enqueue-only on `stream`. */
-gpa_status gpa_attribute_samples(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+GPA_API gpa_status gpa_attribute_samples(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
                                  uint64_t *d_inst_hist, uint64_t *d_unattributed,
                                  uint32_t *d_rec_inst, gpa_stream_t stream);
 /* Same result from HOST records: the library streams h_samples to the device in chunks
  * (pipelined host->device copy overlapped with the attribution kernel) using internal
  * staging buffers.  h_samples may be pageable or pinned (pinned is copied directly).
  * Synchronizes `stream` before returning. */
-gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_samples, uint64_t n,
+GPA_API gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_samples, uint64_t n,
                                       uint64_t *d_inst_hist, uint64_t *d_unattributed,
                                       gpa_stream_t stream);
 
@@ -217,11 +226,11 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
  * R13-R16).  max_contexts == 0: count only (*out untouched, *n_contexts = required).
  * More contexts than max_contexts -> GPA_ERR_CAPACITY with *n_contexts = required.
  * Synchronizes `stream` (the context count decides the allocation). */
-gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist,
+GPA_API gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist,
                                gpa_weight_mode mode, uint64_t max_contexts,
                                gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream);
-gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *out);
-void gpa_free_cct(gpa_cct c);
+GPA_API gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *out);
+GPA_API void gpa_free_cct(gpa_cct c);
 
 /* ---- a-5 + a-10: roll-up and derived metrics -------------------------------------------
  * INST..FUNC: rows of `scope` (see gpa_scope_rows).  Row histogram (u64[16]) =
@@ -233,7 +242,7 @@ void gpa_free_cct(gpa_cct c);
  *   17..32 mix[k]/S (NaN for CCT rows).
  * Any of d_scope_hist, d_scope_mix, d_metrics may be NULL.  For INST rows d_scope_hist
  * receives a copy of d_inst_hist.  Enqueue-only on `stream`. */
-gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist,
+GPA_API gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist,
                               gpa_cct cct, uint64_t *d_scope_hist, uint64_t *d_scope_mix,
                               double *d_metrics, gpa_stream_t stream);
 

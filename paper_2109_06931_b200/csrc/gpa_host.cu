@@ -1,0 +1,754 @@
+// gpa_host.cu — the C ABI of libgpa (include/gpa.h): argument checking, structure
+// validation and load-time table construction (pc->instruction granule map, roll-up CSR,
+// call-graph CSR, Tarjan SCC condensation, DAG levels), and the host orchestration of the
+// kernels in k_attr.cu / k_rollup.cu / k_cct.cu.
+//
+// Paper: Zhou et al., arXiv 2109.06931.  Citations: P:<line>.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "gpa.h"
+#include "gpa_internal.cuh"
+
+using namespace gpa;
+
+static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};
+
+void gpa::count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+static gpa_status fail(gpa_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      if (e_ == cudaErrorMemoryAllocation) {                                             \
+        cudaGetLastError();                                                              \
+        return fail(GPA_ERR_OUT_OF_MEMORY, "%s: %s", #call, cudaGetErrorString(e_));     \
+      }                                                                                  \
+      return fail(GPA_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));                \
+    }                                                                                    \
+  } while (0)
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Everything validation derives on the way (needed again by the loader).
+struct Derived {
+  std::vector<uint32_t> inst_func;     // function of each instruction
+  std::vector<uint32_t> func_of_scope; // function owning each FUNCTION scope
+  std::vector<uint32_t> call_caller;   // caller function of each call site
+};
+
+gpa_status validate(const gpa_structure_desc *d, Derived *out) {
+  if (!d) return fail(GPA_ERR_INVALID_ARG, "desc is NULL");
+  const uint32_t ni = d->n_inst, ns = d->n_scope, nf = d->n_func, nc = d->n_call;
+  if (ni && (!d->inst_addr || !d->inst_len || !d->inst_class || !d->inst_scope))
+    return fail(GPA_ERR_INVALID_ARG, "instruction arrays are NULL with n_inst=%u", ni);
+  if (ns && (!d->scope_parent || !d->scope_kind))
+    return fail(GPA_ERR_INVALID_ARG, "scope arrays are NULL with n_scope=%u", ns);
+  if (nf && !d->func_scope) return fail(GPA_ERR_INVALID_ARG, "func_scope is NULL with n_func=%u", nf);
+  if (nc && (!d->call_inst || !d->call_callee))
+    return fail(GPA_ERR_INVALID_ARG, "call arrays are NULL with n_call=%u", nc);
+  if (ni > (1u << 28) - 16) return fail(GPA_ERR_STRUCTURE, "n_inst=%u exceeds 2^28-16", ni);
+  // instructions: disjoint ranges in ascending order (reading R6)
+  for (uint32_t i = 0; i < ni; i++) {
+    if (d->inst_len[i] == 0) return fail(GPA_ERR_STRUCTURE, "inst_len[%u] == 0", i);
+    if (d->inst_addr[i] > UINT64_MAX - d->inst_len[i])
+      return fail(GPA_ERR_STRUCTURE, "instruction %u range overflows 2^64", i);
+    if (i && d->inst_addr[i - 1] + d->inst_len[i - 1] > d->inst_addr[i])
+      return fail(GPA_ERR_STRUCTURE, "instruction %u overlaps or precedes instruction %u", i, i - 1);
+    if (d->inst_class[i] >= GPA_CLASSES) return fail(GPA_ERR_STRUCTURE, "inst_class[%u] > 15", i);
+  }
+  // scope tree: FUNCTION roots, LINE leaves, no cycles
+  for (uint32_t s = 0; s < ns; s++) {
+    uint8_t k = d->scope_kind[s];
+    uint32_t p = d->scope_parent[s];
+    if (k > GPA_KIND_LINE) return fail(GPA_ERR_STRUCTURE, "scope_kind[%u]=%u", s, k);
+    if ((k == GPA_KIND_FUNCTION) != (p == NONE))
+      return fail(GPA_ERR_STRUCTURE, "scope %u: FUNCTION scopes (only) must be roots", s);
+    if (p != NONE) {
+      if (p >= ns) return fail(GPA_ERR_STRUCTURE, "scope_parent[%u]=%u out of range", s, p);
+      if (d->scope_kind[p] == GPA_KIND_LINE) return fail(GPA_ERR_STRUCTURE, "scope %u has a LINE parent", s);
+    }
+  }
+  std::vector<uint8_t> state(ns, 0);  // 0 new, 1 on the current walk, 2 reaches a root
+  std::vector<uint32_t> walk;
+  for (uint32_t s = 0; s < ns; s++) {
+    walk.clear();
+    uint32_t x = s;
+    while (x != NONE && state[x] == 0) {
+      state[x] = 1;
+      walk.push_back(x);
+      x = d->scope_parent[x];
+    }
+    if (x != NONE && state[x] == 1) return fail(GPA_ERR_STRUCTURE, "scope tree has a cycle through %u", x);
+    for (uint32_t y : walk) state[y] = 2;
+  }
+  out->func_of_scope.assign(ns, NONE);
+  for (uint32_t f = 0; f < nf; f++) {
+    uint32_t s = d->func_scope[f];
+    if (s >= ns || d->scope_kind[s] != GPA_KIND_FUNCTION)
+      return fail(GPA_ERR_STRUCTURE, "func_scope[%u]=%u is not a FUNCTION scope", f, s);
+    if (out->func_of_scope[s] != NONE) return fail(GPA_ERR_STRUCTURE, "FUNCTION scope %u claimed twice", s);
+    out->func_of_scope[s] = f;
+  }
+  for (uint32_t s = 0; s < ns; s++)
+    if (d->scope_kind[s] == GPA_KIND_FUNCTION && out->func_of_scope[s] == NONE)
+      return fail(GPA_ERR_STRUCTURE, "FUNCTION scope %u is not claimed by any function", s);
+  // instruction -> LINE scope -> ... -> FUNCTION root -> function
+  out->inst_func.resize(ni);
+  std::vector<uint32_t> root(ns, NONE);
+  for (uint32_t i = 0; i < ni; i++) {
+    uint32_t s = d->inst_scope[i];
+    if (s >= ns || d->scope_kind[s] != GPA_KIND_LINE)
+      return fail(GPA_ERR_STRUCTURE, "inst_scope[%u]=%u is not a LINE scope", i, s);
+    if (root[s] == NONE) {
+      uint32_t x = s;
+      while (d->scope_parent[x] != NONE) x = d->scope_parent[x];
+      root[s] = x;
+    }
+    out->inst_func[i] = out->func_of_scope[root[s]];
+  }
+  // call sites: direct calls, one per call instruction (reading R22)
+  out->call_caller.resize(nc);
+  std::vector<uint8_t> is_call(ni, 0);
+  for (uint32_t e = 0; e < nc; e++) {
+    if (d->call_inst[e] >= ni) return fail(GPA_ERR_STRUCTURE, "call_inst[%u] out of range", e);
+    if (d->call_callee[e] >= nf) return fail(GPA_ERR_STRUCTURE, "call_callee[%u] out of range", e);
+    if (is_call[d->call_inst[e]]++) return fail(GPA_ERR_STRUCTURE, "two call sites on instruction %u", d->call_inst[e]);
+    out->call_caller[e] = out->inst_func[d->call_inst[e]];
+  }
+  return GPA_OK;
+}
+
+// Tarjan's SCC algorithm, iterative form.  comp[v] = component id in completion order.
+uint32_t tarjan(uint32_t n, const std::vector<uint32_t> &ptr, const std::vector<uint32_t> &dst,
+                std::vector<uint32_t> &comp) {
+  std::vector<uint32_t> index(n, NONE), low(n, 0), stack, it(n, 0);
+  std::vector<uint8_t> on(n, 0);
+  std::vector<uint32_t> call;
+  uint32_t next = 0, ncomp = 0;
+  comp.assign(n, NONE);
+  for (uint32_t r = 0; r < n; r++) {
+    if (index[r] != NONE) continue;
+    call.push_back(r);
+    index[r] = low[r] = next++;
+    stack.push_back(r);
+    on[r] = 1;
+    it[r] = ptr[r];
+    while (!call.empty()) {
+      uint32_t v = call.back();
+      if (it[v] < ptr[v + 1]) {
+        uint32_t u = dst[it[v]++];
+        if (index[u] == NONE) {
+          index[u] = low[u] = next++;
+          stack.push_back(u);
+          on[u] = 1;
+          it[u] = ptr[u];
+          call.push_back(u);
+        } else if (on[u]) {
+          low[v] = std::min(low[v], index[u]);
+        }
+      } else {
+        call.pop_back();
+        if (!call.empty()) low[call.back()] = std::min(low[call.back()], low[v]);
+        if (low[v] == index[v]) {
+          uint32_t u;
+          do {
+            u = stack.back();
+            stack.pop_back();
+            on[u] = 0;
+            comp[u] = ncomp;
+          } while (u != v);
+          ncomp++;
+        }
+      }
+    }
+  }
+  return ncomp;
+}
+
+template <class T>
+gpa_status upload(gpa_structure_s *s, T **dptr, const T *h, size_t n) {
+  *dptr = nullptr;
+  size_t bytes = sizeof(T) * (n ? n : 1);
+  CU(cudaMalloc((void **)dptr, bytes));
+  s->allocs.push_back(*dptr);
+  s->info.device_bytes += bytes;
+  if (n) CU(cudaMemcpy(*dptr, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return GPA_OK;
+}
+
+#define UP(dst, vec)                                                   \
+  do {                                                                 \
+    gpa_status st_ = upload(s, &(dst), (vec).data(), (vec).size());    \
+    if (st_ != GPA_OK) return st_;                                     \
+  } while (0)
+
+void free_structure(gpa_structure_s *s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  for (void *p : s->allocs) cudaFree(p);
+  delete s;
+}
+
+gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s *s) {
+  const uint32_t ni = d->n_inst, ns = d->n_scope, nf = d->n_func, nc = d->n_call;
+  gpa_structure_info &info = s->info;
+  info.n_inst = ni; info.n_scope = ns; info.n_func = nf; info.n_call = nc;
+  for (uint32_t x = 0; x < ns; x++) {
+    if (d->scope_kind[x] == GPA_KIND_LINE) info.n_line++;
+    if (d->scope_kind[x] == GPA_KIND_LOOP) info.n_loop++;
+    if (d->scope_kind[x] == GPA_KIND_INLINE) info.n_inline++;
+  }
+
+  // ---- a-2: pc -> instruction map.  Granule 2^g = largest power of two that
+  // divides every start offset and every length; each granule is then wholly inside one
+  // instruction or wholly inside a gap, so the map reproduces [addr, addr+len) exactly.
+  std::vector<uint64_t> addr(d->inst_addr, d->inst_addr + ni);
+  std::vector<uint16_t> len(d->inst_len, d->inst_len + ni);
+  std::vector<uint8_t> cls(d->inst_class, d->inst_class + ni);
+  UP(s->d_inst_addr, addr);
+  UP(s->d_inst_len, len);
+  UP(s->d_inst_class, cls);
+  AttrTables &T = s->attr;
+  T.n_inst = ni;
+  T.inst_addr = s->d_inst_addr;
+  T.inst_len = s->d_inst_len;
+  T.mode = 1;
+  if (ni) {
+    T.base = addr[0];
+    T.end = addr[ni - 1] + len[ni - 1];
+    uint64_t bits = 0;
+    for (uint32_t i = 0; i < ni; i++) bits |= (addr[i] - T.base) | len[i];
+    T.gshift = (uint32_t)__builtin_ctzll(bits);
+    T.n_gran = (T.end - T.base) >> T.gshift;
+    if (T.n_gran <= (1ull << 28)) {
+      std::vector<uint32_t> gmap(T.n_gran, NONE);
+      for (uint32_t i = 0; i < ni; i++) {
+        uint64_t g0 = (addr[i] - T.base) >> T.gshift, g1 = (addr[i] + len[i] - T.base) >> T.gshift;
+        for (uint64_t g = g0; g < g1; g++) gmap[g] = i;
+      }
+      UP(s->d_gmap, gmap);
+      T.gmap = s->d_gmap;
+      T.mode = 0;
+    }
+  } else {
+    T.base = 1;
+    T.end = 0;  // empty range: every pc is unattributed
+  }
+  info.lookup_mode = T.mode;
+  info.granule_shift = T.gshift;
+  info.lookup_entries = T.mode == 0 ? T.n_gran : 0;
+
+  // ---- a-5: roll-up CSR: row -> instructions whose scope chain
+  // contains the row's scope.  LINE/LOOP/INLINE rows = scopes of that kind in ascending id;
+  // FUNC rows = functions.
+  std::vector<uint32_t> row_of(ns, NONE);
+  RollSet *R = s->roll;
+  for (uint32_t x = 0; x < ns; x++) {
+    uint8_t k = d->scope_kind[x];
+    int set = k == GPA_KIND_LINE ? ROLL_LINE : k == GPA_KIND_LOOP ? ROLL_LOOP : k == GPA_KIND_INLINE ? ROLL_INLINE : -1;
+    if (set >= 0) {
+      row_of[x] = (uint32_t)R[set].ids.size();
+      R[set].ids.push_back(x);
+    } else {
+      row_of[x] = dv.func_of_scope[x];
+    }
+  }
+  R[ROLL_FUNC].ids.resize(nf);
+  std::iota(R[ROLL_FUNC].ids.begin(), R[ROLL_FUNC].ids.end(), 0u);
+  auto set_of = [&](uint32_t x) -> int {
+    uint8_t k = d->scope_kind[x];
+    return k == GPA_KIND_LINE ? ROLL_LINE : k == GPA_KIND_LOOP ? ROLL_LOOP : k == GPA_KIND_INLINE ? ROLL_INLINE : ROLL_FUNC;
+  };
+  std::vector<std::vector<uint32_t>> ptr(ROLL_KINDS), lst(ROLL_KINDS);
+  for (int k = 0; k < ROLL_KINDS; k++) {
+    R[k].rows = (uint32_t)R[k].ids.size();
+    ptr[k].assign(R[k].rows + 1, 0);
+  }
+  for (uint32_t i = 0; i < ni; i++)
+    for (uint32_t x = d->inst_scope[i]; x != NONE; x = d->scope_parent[x]) ptr[set_of(x)][row_of[x] + 1]++;
+  for (int k = 0; k < ROLL_KINDS; k++) {
+    for (uint32_t r = 0; r < R[k].rows; r++) ptr[k][r + 1] += ptr[k][r];
+    lst[k].resize(ptr[k][R[k].rows]);
+  }
+  {
+    std::vector<std::vector<uint32_t>> fill(ptr);
+    for (uint32_t i = 0; i < ni; i++)
+      for (uint32_t x = d->inst_scope[i]; x != NONE; x = d->scope_parent[x]) {
+        int k = set_of(x);
+        lst[k][fill[k][row_of[x]]++] = i;
+      }
+  }
+  for (int k = 0; k < ROLL_KINDS; k++) {
+    UP(R[k].d_ptr, ptr[k]);
+    UP(R[k].d_inst, lst[k]);
+  }
+
+  // ---- Step 1 structure: call graph from call instructions ---------------------
+  std::vector<uint32_t> ci(d->call_inst, d->call_inst + nc), cc(d->call_callee, d->call_callee + nc);
+  UP(s->d_call_inst, ci);
+  UP(s->d_call_callee, cc);
+  UP(s->d_call_caller, dv.call_caller);
+  std::vector<uint32_t> order(nc);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ci[a] < ci[b]; });
+  std::vector<uint32_t> aptr(nf + 1, 0), adst(nc);  // adjacency for Tarjan
+  std::vector<uint32_t> fin_ptr(nf + 1, 0), fin_e(nc);
+  for (uint32_t e = 0; e < nc; e++) { aptr[dv.call_caller[e] + 1]++; fin_ptr[cc[e] + 1]++; }
+  for (uint32_t f = 0; f < nf; f++) { aptr[f + 1] += aptr[f]; fin_ptr[f + 1] += fin_ptr[f]; }
+  {
+    std::vector<uint32_t> fa(aptr), fi(fin_ptr);
+    for (uint32_t e : order) { adst[fa[dv.call_caller[e]]++] = cc[e]; fin_e[fi[cc[e]]++] = e; }
+  }
+  UP(s->d_fin_ptr, fin_ptr);
+  UP(s->d_fin_e, fin_e);
+
+  // ---- Step 3: Tarjan SCCs of the static call graph; DAG ids by ascending
+  // smallest member (reading R17); non-trivial = >= 2 members or a self-call (R14).
+  std::vector<uint32_t> comp;
+  uint32_t ncomp = tarjan(nf, aptr, adst, comp);
+  std::vector<uint32_t> cmin(ncomp, NONE), c2d(ncomp, NONE);
+  for (uint32_t f = 0; f < nf; f++) cmin[comp[f]] = std::min(cmin[comp[f]], f);
+  uint32_t nd = 0;
+  for (uint32_t f = 0; f < nf; f++)
+    if (cmin[comp[f]] == f) c2d[comp[f]] = nd++;
+  s->h_scc_of.resize(nf);
+  for (uint32_t f = 0; f < nf; f++) s->h_scc_of[f] = c2d[comp[f]];
+  const std::vector<uint32_t> &scc = s->h_scc_of;
+  info.n_dag = nd;
+  std::vector<uint32_t> dmem_ptr(nd + 1, 0), dmem(nf);
+  for (uint32_t f = 0; f < nf; f++) dmem_ptr[scc[f] + 1]++;
+  for (uint32_t X = 0; X < nd; X++) dmem_ptr[X + 1] += dmem_ptr[X];
+  {
+    std::vector<uint32_t> fm(dmem_ptr);
+    for (uint32_t f = 0; f < nf; f++) dmem[fm[scc[f]]++] = f;  // ascending function id
+  }
+  std::vector<uint8_t> nontriv(nd, 0);
+  for (uint32_t X = 0; X < nd; X++) nontriv[X] = dmem_ptr[X + 1] - dmem_ptr[X] >= 2;
+  for (uint32_t e = 0; e < nc; e++)
+    if (dv.call_caller[e] == cc[e]) nontriv[scc[cc[e]]] = 1;
+  for (uint32_t X = 0; X < nd; X++) info.n_scc += nontriv[X];
+  // external edges: out-edges per function in call-instruction order; in-edges per DAG node
+  std::vector<uint32_t> fout_ptr(nf + 1, 0), fout_e, din_ptr(nd + 1, 0), din_e;
+  for (uint32_t e : order)
+    if (scc[dv.call_caller[e]] != scc[cc[e]]) { fout_ptr[dv.call_caller[e] + 1]++; din_ptr[scc[cc[e]] + 1]++; }
+  for (uint32_t f = 0; f < nf; f++) fout_ptr[f + 1] += fout_ptr[f];
+  for (uint32_t X = 0; X < nd; X++) din_ptr[X + 1] += din_ptr[X];
+  fout_e.resize(fout_ptr[nf]);
+  din_e.resize(din_ptr[nd]);
+  {
+    std::vector<uint32_t> fo(fout_ptr), di(din_ptr);
+    for (uint32_t e : order)
+      if (scc[dv.call_caller[e]] != scc[cc[e]]) { fout_e[fo[dv.call_caller[e]]++] = e; din_e[di[scc[cc[e]]]++] = e; }
+  }
+  // static DAG levels (longest path from a source) and the all-edges context bound
+  std::vector<uint32_t> indeg(nd, 0), level(nd, 0);
+  std::vector<std::vector<uint32_t>> dsucc(nd);
+  for (uint32_t e : din_e) { indeg[scc[cc[e]]]++; dsucc[scc[dv.call_caller[e]]].push_back(scc[cc[e]]); }
+  std::vector<uint32_t> topo;
+  for (uint32_t X = 0; X < nd; X++)
+    if (!indeg[X]) topo.push_back(X);
+  for (size_t q = 0; q < topo.size(); q++)
+    for (uint32_t Y : dsucc[topo[q]]) {
+      level[Y] = std::max(level[Y], level[topo[q]] + 1);
+      if (--indeg[Y] == 0) topo.push_back(Y);
+    }
+  if (topo.size() != nd) return fail(GPA_ERR_INTERNAL, "condensed call graph is not a DAG");
+  uint32_t nlev = 0;
+  for (uint32_t X = 0; X < nd; X++) nlev = std::max(nlev, level[X] + 1);
+  info.dag_levels = nlev;
+  std::vector<uint32_t> dlev_ptr(nlev + 1, 0), dlev_node(nd);
+  for (uint32_t X = 0; X < nd; X++) dlev_ptr[level[X] + 1]++;
+  for (uint32_t L = 0; L < nlev; L++) dlev_ptr[L + 1] += dlev_ptr[L];
+  {
+    std::vector<uint32_t> fl(dlev_ptr);
+    for (uint32_t X = 0; X < nd; X++) dlev_node[fl[level[X]]++] = X;
+  }
+  const uint64_t SAT = 1ull << 62;
+  std::vector<uint64_t> paths(nd, 0);
+  uint64_t bound = 0;
+  for (uint32_t X : topo) {
+    uint64_t p = din_ptr[X + 1] == din_ptr[X] ? 1 : 0;
+    for (uint32_t k = din_ptr[X]; k < din_ptr[X + 1]; k++) p = std::min(SAT, p + paths[scc[dv.call_caller[din_e[k]]]]);
+    paths[X] = p;
+    uint64_t per = nontriv[X] ? 1 + (dmem_ptr[X + 1] - dmem_ptr[X]) : 1;
+    bound = std::min(SAT, bound + (p > SAT / per ? SAT : p * per));
+  }
+  info.cct_path_bound = bound;
+  UP(s->d_scc_of, s->h_scc_of);
+  UP(s->d_fout_ptr, fout_ptr);
+  UP(s->d_fout_e, fout_e);
+  UP(s->d_din_ptr, din_ptr);
+  UP(s->d_din_e, din_e);
+  UP(s->d_dmem_ptr, dmem_ptr);
+  UP(s->d_dmem, dmem);
+  UP(s->d_dag_nontrivial, nontriv);
+  UP(s->d_dlev_ptr, dlev_ptr);
+  UP(s->d_dlev_node, dlev_node);
+  CU(cudaDeviceSynchronize());
+  return GPA_OK;
+}
+
+gpa_status check_dev_ptr(const void *p, int dev, const char *name) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GPA_ERR_INVALID_ARG, "%s: not a CUDA pointer (%s)", name, cudaGetErrorString(e));
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(GPA_ERR_INVALID_ARG, "%s is not device memory", name);
+  if (a.type == cudaMemoryTypeDevice && a.device != dev)
+    return fail(GPA_ERR_INVALID_ARG, "%s is on device %d, structure on %d", name, a.device, dev);
+  return GPA_OK;
+}
+
+int sm_count(int dev) {
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = v;
+  return v;
+}
+
+}  // namespace
+
+#define CHECK(x)                         \
+  do {                                   \
+    gpa_status st_ = (x);                \
+    if (st_ != GPA_OK) return st_;       \
+  } while (0)
+
+// ---- a-6..a-9 ---------------------------------------------------------------------------
+static void free_cct(gpa_cct_s *c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  for (void *p : c->allocs) cudaFree(p);
+  delete c;
+}
+
+template <class T>
+static cudaError_t calloc_dev(gpa_cct_s *c, T **p, size_t n) {
+  *p = nullptr;
+  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (n ? n : 1));
+  if (e == cudaSuccess) c->allocs.push_back(*p);
+  return e;
+}
+
+extern "C" {
+
+const char *gpa_version(void) { return "libgpa 0.1 (sm_100a)"; }
+const char *gpa_last_error(void) { return g_err.c_str(); }
+uint64_t gpa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+gpa_status gpa_validate_structure(const gpa_structure_desc *desc) {
+  Derived dv;
+  return validate(desc, &dv);
+}
+
+gpa_status gpa_load_structure(const gpa_structure_desc *desc, int device, gpa_structure *out) {
+  if (!out) return fail(GPA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  Derived dv;
+  CHECK(validate(desc, &dv));
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(GPA_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+  DeviceGuard g(device);
+  CU(g.err);
+  gpa_structure_s *s = new gpa_structure_s();
+  s->device = device;
+  gpa_status st = build(desc, dv, s);
+  if (st != GPA_OK) {
+    std::string msg = g_err;
+    free_structure(s);
+    g_err = msg;
+    return st;
+  }
+  *out = s;
+  return GPA_OK;
+}
+
+gpa_status gpa_get_structure_info(gpa_structure s, gpa_structure_info *out) {
+  if (!s || !out) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  *out = s->info;
+  return GPA_OK;
+}
+
+gpa_status gpa_scope_rows(gpa_structure s, gpa_scope scope, uint64_t *rows, uint32_t *h_ids) {
+  if (!s || !rows) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if (scope == GPA_SCOPE_INST) {
+    *rows = s->info.n_inst;
+    if (h_ids)
+      for (uint32_t i = 0; i < s->info.n_inst; i++) h_ids[i] = i;
+    return GPA_OK;
+  }
+  int k = scope == GPA_SCOPE_LINE ? ROLL_LINE : scope == GPA_SCOPE_LOOP ? ROLL_LOOP
+        : scope == GPA_SCOPE_INLINE ? ROLL_INLINE : scope == GPA_SCOPE_FUNC ? ROLL_FUNC : -1;
+  if (k < 0) return fail(GPA_ERR_INVALID_ARG, "scope %d has no static rows", (int)scope);
+  *rows = s->roll[k].rows;
+  if (h_ids && s->roll[k].rows) memcpy(h_ids, s->roll[k].ids.data(), sizeof(uint32_t) * s->roll[k].rows);
+  return GPA_OK;
+}
+
+gpa_status gpa_get_scc(gpa_structure s, uint32_t *h_scc_of) {
+  if (!s || (!h_scc_of && s->info.n_func)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if (s->info.n_func) memcpy(h_scc_of, s->h_scc_of.data(), sizeof(uint32_t) * s->info.n_func);
+  return GPA_OK;
+}
+
+void gpa_free_structure(gpa_structure s) { free_structure(s); }
+
+// ---- a-1..a-3 -------------------------------------------------------------------------
+gpa_status gpa_attribute_samples(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+                                 uint64_t *d_inst_hist, uint64_t *d_unattributed, uint32_t *d_rec_inst,
+                                 gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (n == 0) return GPA_OK;
+  if (!d_samples || !d_unattributed || (!d_inst_hist && s->info.n_inst))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer with n=%llu", (unsigned long long)n);
+  if ((uintptr_t)d_samples & 15) return fail(GPA_ERR_INVALID_ARG, "d_samples is not 16-byte aligned");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
+  CHECK(check_dev_ptr(d_unattributed, s->device, "d_unattributed"));
+  if (d_inst_hist) CHECK(check_dev_ptr(d_inst_hist, s->device, "d_inst_hist"));
+  if (d_rec_inst) CHECK(check_dev_ptr(d_rec_inst, s->device, "d_rec_inst"));
+  CU(launch_attribute(s->attr, d_samples, n, (unsigned long long *)d_inst_hist,
+                      (unsigned long long *)d_unattributed, d_rec_inst, sm_count(s->device),
+                      (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_samples, uint64_t n,
+                                      uint64_t *d_inst_hist, uint64_t *d_unattributed, gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (n == 0) return GPA_OK;
+  if (!h_samples || !d_unattributed || (!d_inst_hist && s->info.n_inst))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer with n=%llu", (unsigned long long)n);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CHECK(check_dev_ptr(d_unattributed, s->device, "d_unattributed"));
+  cudaStream_t st = (cudaStream_t)stream;
+  // Pipeline: NBUF device staging buffers; H2D copy of chunk j on `cp` overlaps the
+  // attribution kernel of chunk j-1 on `st`.
+  const int NBUF = 3;
+  const uint64_t CHUNK = 1ull << 22;  // records (64 MiB)
+  uint64_t per = std::min<uint64_t>(CHUNK, n);
+  cudaStream_t cp = nullptr;
+  cudaEvent_t copied[NBUF] = {}, consumed[NBUF] = {};
+  gpa_sample *buf[NBUF] = {};
+  gpa_status ret = GPA_OK;
+  auto cleanup = [&]() {
+    if (cp) cudaStreamSynchronize(cp);
+    cudaStreamSynchronize(st);
+    for (int b = 0; b < NBUF; b++) {
+      if (buf[b]) cudaFree(buf[b]);
+      if (copied[b]) cudaEventDestroy(copied[b]);
+      if (consumed[b]) cudaEventDestroy(consumed[b]);
+    }
+    if (cp) cudaStreamDestroy(cp);
+  };
+#define HC(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      ret = fail(e_ == cudaErrorMemoryAllocation ? GPA_ERR_OUT_OF_MEMORY : GPA_ERR_CUDA,  \
+                 "%s: %s", #call, cudaGetErrorString(e_));                                \
+      cudaGetLastError();                                                                 \
+      cleanup();                                                                          \
+      return ret;                                                                         \
+    }                                                                                     \
+  } while (0)
+  HC(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  for (int b = 0; b < NBUF; b++) {
+    HC(cudaMalloc((void **)&buf[b], per * sizeof(gpa_sample)));
+    HC(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    HC(cudaEventCreateWithFlags(&consumed[b], cudaEventDisableTiming));
+  }
+  for (uint64_t off = 0, j = 0; off < n; off += per, j++) {
+    int b = (int)(j % NBUF);
+    uint64_t m = std::min(per, n - off);
+    if (j >= NBUF) HC(cudaStreamWaitEvent(cp, consumed[b], 0));
+    HC(cudaMemcpyAsync(buf[b], h_samples + off, m * sizeof(gpa_sample), cudaMemcpyHostToDevice, cp));
+    HC(cudaEventRecord(copied[b], cp));
+    HC(cudaStreamWaitEvent(st, copied[b], 0));
+    HC(launch_attribute(s->attr, buf[b], m, (unsigned long long *)d_inst_hist,
+                        (unsigned long long *)d_unattributed, nullptr, sm_count(s->device), st));
+    HC(cudaEventRecord(consumed[b], st));
+  }
+#undef HC
+  cleanup();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GPA_ERR_CUDA, "attribute_samples_host: %s", cudaGetErrorString(e));
+  return GPA_OK;
+}
+
+gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa_weight_mode mode,
+                               uint64_t max_contexts, gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream) {
+  if (!s || !n_contexts || (max_contexts && !out)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if (mode != GPA_WEIGHTS_SAMPLES) return fail(GPA_ERR_UNSUPPORTED, "only GPA_WEIGHTS_SAMPLES is built");
+  if (!d_inst_hist && s->info.n_inst) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  if (out) *out = nullptr;
+  DeviceGuard g(s->device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  const gpa_structure_info &I = s->info;
+  gpa_cct_s *c = new gpa_cct_s();
+  c->device = s->device;
+  c->n_call = I.n_call; c->n_func = I.n_func; c->n_dag = I.n_dag;
+  unsigned long long *d_cnt = nullptr;  // [0] total contexts, [1] next-level size
+  gpa_status ret = GPA_OK;
+#define CC(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      ret = fail(e_ == cudaErrorMemoryAllocation ? GPA_ERR_OUT_OF_MEMORY : GPA_ERR_CUDA,  \
+                 "%s: %s", #call, cudaGetErrorString(e_));                                \
+      cudaGetLastError();                                                                 \
+      free_cct(c);                                                                        \
+      return ret;                                                                         \
+    }                                                                                     \
+  } while (0)
+  CC(calloc_dev(c, &c->w, I.n_call));
+  CC(calloc_dev(c, &c->S_f, (size_t)I.n_func * SLOTS));
+  CC(calloc_dev(c, &c->func_active, I.n_func));
+  CC(calloc_dev(c, &c->dag_active, I.n_dag));
+  CC(calloc_dev(c, &c->W, I.n_dag));
+  CC(calloc_dev(c, &d_cnt, 4));
+  // Step 1: edge weights and per-function samples S_f (the FUNC roll-up)
+  CC(launch_cct_weights(s, d_inst_hist, c->w, st));
+  CC(launch_rollup(s->roll[ROLL_FUNC].d_ptr, s->roll[ROLL_FUNC].d_inst, s->roll[ROLL_FUNC].rows, false,
+                   d_inst_hist, s->d_inst_class, c->S_f, nullptr, nullptr, sm_count(s->device), st));
+  // Step 2 + guard (R12) + W + context count (path DP over the DAG)
+  CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, st));
+  unsigned long long h_cnt[2] = {0, 0};
+  CC(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+  CC(cudaStreamSynchronize(st));
+  *n_contexts = h_cnt[0];
+  if (max_contexts == 0 || h_cnt[0] > max_contexts) {
+    free_cct(c);
+    if (max_contexts == 0) return GPA_OK;
+    return fail(GPA_ERR_CAPACITY, "%llu contexts > max_contexts %llu", h_cnt[0], (unsigned long long)max_contexts);
+  }
+  const uint64_t n = h_cnt[0];
+  if (n >= (1ull << 32) - 1) {
+    free_cct(c);
+    return fail(GPA_ERR_CAPACITY, "%llu contexts exceed the u32 context index", (unsigned long long)n);
+  }
+  c->n = n;
+  CC(calloc_dev(c, &c->parent, n));
+  CC(calloc_dev(c, &c->site, n));
+  CC(calloc_dev(c, &c->node, n));
+  CC(calloc_dev(c, &c->first_child, n));
+  CC(calloc_dev(c, &c->n_children, n));
+  CC(calloc_dev(c, &c->kind, n));
+  CC(calloc_dev(c, &c->frac, n));
+  CC(calloc_dev(c, &c->excl, n * SLOTS));
+  CC(calloc_dev(c, &c->incl, n * SLOTS));
+  uint32_t *d_tmp = nullptr, *d_bs = nullptr;
+  CC(calloc_dev(c, &d_tmp, n + 1));
+  CC(calloc_dev(c, &d_bs, 65536));
+  // Step 4: breadth-first split of the DAG into the tree, level by level
+  CC(launch_cct_roots(s, c->dag_active, c, d_cnt + 1, st));
+  CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CC(cudaStreamSynchronize(st));
+  uint64_t a = 0, b = h_cnt[1];
+  c->level_start.push_back(0);
+  while (b > a) {
+    c->level_start.push_back(b);
+    if (b > n) { free_cct(c); return fail(GPA_ERR_INTERNAL, "BFS overran the counted contexts"); }
+    CC(launch_cct_level(s, c, a, b, d_tmp, d_bs, d_cnt + 1, st));
+    CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CC(cudaStreamSynchronize(st));
+    a = b;
+    b += h_cnt[1];
+  }
+  if (b != n) {
+    free_cct(c);
+    return fail(GPA_ERR_INTERNAL, "BFS built %llu contexts, path count said %llu", (unsigned long long)b,
+                (unsigned long long)n);
+  }
+  CC(launch_cct_excl(s, c, st));
+  for (size_t L = c->level_start.size() - 1; L-- > 0;)
+    CC(launch_cct_incl_level(c, c->level_start[L], c->level_start[L + 1], st));
+#undef CC
+  *out = c;
+  return GPA_OK;
+}
+
+gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *v) {
+  if (!c || !v) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  v->n = c->n;
+  v->parent = c->parent; v->site = c->site; v->node = c->node; v->kind = c->kind;
+  v->first_child = c->first_child; v->n_children = c->n_children;
+  v->frac = c->frac; v->excl = c->excl; v->incl = c->incl;
+  v->n_call = c->n_call; v->n_func = c->n_func; v->n_dag = c->n_dag;
+  v->call_weight = c->w; v->dag_weight = c->W; v->dag_active = c->dag_active;
+  v->func_active = c->func_active; v->func_hist = c->S_f;
+  return GPA_OK;
+}
+
+void gpa_free_cct(gpa_cct c) { free_cct(c); }
+
+// ---- a-5 + a-10 -------------------------------------------------------------------------
+gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist, gpa_cct cct,
+                              uint64_t *d_scope_hist, uint64_t *d_scope_mix, double *d_metrics,
+                              gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (scope == GPA_SCOPE_CCT_EXCL || scope == GPA_SCOPE_CCT_INCL) {
+    if (!cct) return fail(GPA_ERR_INVALID_ARG, "CCT scope without a cct");
+    if (d_scope_hist || d_scope_mix) return fail(GPA_ERR_INVALID_ARG, "CCT rows have no u64 histogram or mix");
+    if (!d_metrics || cct->n == 0) return GPA_OK;
+    CU(launch_derive_f64(scope == GPA_SCOPE_CCT_EXCL ? cct->excl : cct->incl, cct->n, d_metrics, st));
+    return GPA_OK;
+  }
+  int k = scope == GPA_SCOPE_LINE ? ROLL_LINE : scope == GPA_SCOPE_LOOP ? ROLL_LOOP
+        : scope == GPA_SCOPE_INLINE ? ROLL_INLINE : scope == GPA_SCOPE_FUNC ? ROLL_FUNC
+        : scope == GPA_SCOPE_INST ? -1 : -2;
+  if (k == -2) return fail(GPA_ERR_INVALID_ARG, "unknown scope %d", (int)scope);
+  uint32_t rows = k < 0 ? s->info.n_inst : s->roll[k].rows;
+  if (rows == 0 || (!d_scope_hist && !d_scope_mix && !d_metrics)) return GPA_OK;
+  if (!d_inst_hist) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  CU(launch_rollup(k < 0 ? nullptr : s->roll[k].d_ptr, k < 0 ? nullptr : s->roll[k].d_inst, rows, k < 0,
+                   d_inst_hist, s->d_inst_class, d_scope_hist, d_scope_mix, d_metrics, sm_count(s->device), st));
+  return GPA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// gpa_internal.cuh — internal types shared by the libgpa translation units.
+// Public contract: include/gpa.h.  Nothing here is visible across the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "gpa.h"
+
+namespace gpa {
+
+constexpr uint32_t NONE = GPA_NONE;
+constexpr int SLOTS = GPA_SLOTS;
+constexpr int VALID = GPA_VALID_SLOTS;
+constexpr int NCOLS = GPA_NUM_DERIVED;
+
+// roll-up row sets (index into gpa_structure_s::roll)
+enum { ROLL_LINE = 0, ROLL_LOOP = 1, ROLL_INLINE = 2, ROLL_FUNC = 3, ROLL_KINDS = 4 };
+
+// Tables the attribution kernel reads (passed by value as a kernel parameter).
+struct AttrTables {
+  uint64_t base;          // first instruction start
+  uint64_t end;           // last instruction end (exclusive)
+  uint32_t gshift;        // granule = 1 << gshift bytes
+  uint32_t mode;          // 0 = granule map, 1 = binary search
+  uint64_t n_gran;
+  const uint32_t *gmap;   // [n_gran] instruction covering each granule, or NONE
+  const uint64_t *inst_addr;
+  const uint16_t *inst_len;
+  uint32_t n_inst;
+};
+
+struct RollSet {
+  uint32_t rows = 0;
+  uint32_t *d_ptr = nullptr;    // [rows+1]
+  uint32_t *d_inst = nullptr;   // [ptr[rows]]
+  std::vector<uint32_t> ids;    // host: scope id (or function id) behind each row
+};
+
+}  // namespace gpa
+
+struct gpa_structure_s {
+  int device = 0;
+  gpa_structure_info info{};
+  gpa::AttrTables attr{};
+  // device tables
+  uint64_t *d_inst_addr = nullptr;
+  uint16_t *d_inst_len = nullptr;
+  uint8_t *d_inst_class = nullptr;
+  uint32_t *d_gmap = nullptr;
+  gpa::RollSet roll[gpa::ROLL_KINDS];
+  // call graph (function level)
+  uint32_t *d_call_inst = nullptr, *d_call_callee = nullptr, *d_call_caller = nullptr;
+  uint32_t *d_fin_ptr = nullptr, *d_fin_e = nullptr;    // in-edges per function
+  uint32_t *d_fout_ptr = nullptr, *d_fout_e = nullptr;  // external out-edges per function,
+                                                        // ascending call instruction
+  // condensed DAG
+  uint32_t *d_scc_of = nullptr;                         // [n_func]
+  uint32_t *d_din_ptr = nullptr, *d_din_e = nullptr;    // external in-edges per DAG node
+  uint32_t *d_dmem_ptr = nullptr, *d_dmem = nullptr;    // members per DAG node (ascending)
+  uint8_t *d_dag_nontrivial = nullptr;
+  uint32_t *d_dlev_ptr = nullptr, *d_dlev_node = nullptr;  // DAG nodes grouped by level
+  std::vector<uint32_t> h_scc_of;
+  std::vector<void *> allocs;
+};
+
+struct gpa_cct_s {
+  int device = 0;
+  uint64_t n = 0;
+  uint32_t n_call = 0, n_func = 0, n_dag = 0;
+  uint32_t *parent = nullptr, *site = nullptr, *node = nullptr, *first_child = nullptr,
+           *n_children = nullptr;
+  uint8_t *kind = nullptr;
+  double *frac = nullptr, *excl = nullptr, *incl = nullptr;
+  uint64_t *w = nullptr, *W = nullptr, *S_f = nullptr;
+  uint8_t *dag_active = nullptr, *func_active = nullptr;
+  std::vector<uint64_t> level_start;  // contexts of BFS level L: [level_start[L], level_start[L+1])
+  std::vector<void *> allocs;
+};
+
+// ---- kernel launch accounting (gpa_kernel_launches) ------------------------------------------
+namespace gpa {
+void count_launches(uint64_t k);
+}
+
+// ---- kernels launchers (k_*.cu) -----------------------------------------------------------
+namespace gpa {
+cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
+                             unsigned long long *d_hist, unsigned long long *d_unattr,
+                             uint32_t *d_rec_inst, int sm_count, cudaStream_t st);
+// Row-wise roll-up with the fused derived-metric epilogue.  identity: row r = instruction r.
+cudaError_t launch_rollup(const uint32_t *d_ptr, const uint32_t *d_inst, uint32_t rows, bool identity,
+                          const uint64_t *d_hist, const uint8_t *d_class, uint64_t *d_out_hist,
+                          uint64_t *d_out_mix, double *d_metrics, int sm_count, cudaStream_t st);
+cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st);
+
+// CCT pieces (k_cct.cu)
+cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist, uint64_t *d_w,
+                               cudaStream_t st);
+cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
+                                 uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
+                                 unsigned long long *d_count, cudaStream_t st);
+cudaError_t launch_cct_roots(const gpa_structure_s *s, const uint8_t *d_dag_active, gpa_cct_s *c,
+                             unsigned long long *d_n, cudaStream_t st);
+cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a, uint64_t b,
+                             uint32_t *d_tmp, uint32_t *d_blocksum, unsigned long long *d_next,
+                             cudaStream_t st);
+cudaError_t launch_cct_excl(const gpa_structure_s *s, gpa_cct_s *c, cudaStream_t st);
+cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStream_t st);
+}  // namespace gpa

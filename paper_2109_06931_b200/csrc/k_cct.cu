@@ -1,0 +1,424 @@
+// k_cct.cu — a-6..a-9: approximate GPU calling-context tree (§5.3).
+//
+//  Step 1  k_weights      w_e = valid samples on call instruction e (R10)
+//  Step 2  k_propagate    zero-weight propagation to the least fixpoint (R11), the
+//                                 same rule on the condensed DAG (guard, R12), W_X, and the
+//                                 exact context count by a path DP over the static DAG levels
+//  Step 3  load time      Tarjan condensation (gpa_host.cu)
+//  Step 4  k_roots, k_level_count / scan / k_level_write: breadth-first split of
+//                                 the DAG into the tree, one level at a time (count children,
+//                                 exclusive scan = BFS numbering R17, write children with
+//                                 f(child) = f(parent) * w_e / W_callee, R13);
+//                  k_excl         excl = f * S_function (0 for SCC contexts, R14);
+//                  k_incl_level   incl = excl + children's incl in child order, deepest
+//                                 level first.
+// Every fp64 operation is one correctly rounded __d*_rn call in the oracle's order.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gpa_internal.cuh"
+
+namespace gpa {
+namespace {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 2;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long SAT = 1ull << 62;
+
+__global__ void k_weights(const uint32_t *__restrict__ call_inst, uint32_t n_call, const uint64_t *__restrict__ H,
+                          uint64_t *__restrict__ w) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n_call; e += gridDim.x * blockDim.x) {
+    const uint64_t *h = H + ((uint64_t)call_inst[e] << 4);
+    uint64_t s = 0;
+#pragma unroll
+    for (int r = 0; r < GPA_VALID_SLOTS; r++) s += h[r];
+    w[e] = s;
+  }
+}
+
+struct PropArgs {
+  uint32_t n_func, n_dag, n_lev;
+  const uint64_t *S_f;
+  const uint32_t *fin_ptr, *fin_e, *caller, *scc_of, *din_ptr, *din_e, *dmem_ptr, *dmem, *dlev_ptr, *dlev_node;
+  const uint8_t *nontriv;
+  uint64_t *w, *W, *paths;
+  uint8_t *fact, *dact;
+  unsigned long long *count;
+};
+
+// Single CTA: the call graph is small (<= a few thousand functions); rounds are separated
+// by __syncthreads, which also orders the global-memory updates inside the CTA.
+__global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
+  __shared__ int changed;
+  __shared__ unsigned long long red[32];
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  volatile uint8_t *fact = A.fact;
+  volatile uint8_t *dact = A.dact;
+  volatile uint64_t *w = A.w;
+  for (uint32_t f = t; f < A.n_func; f += nt) {
+    uint64_t s = 0;
+    for (int r = 0; r < GPA_VALID_SLOTS; r++) s += A.S_f[(uint64_t)f * GPA_SLOTS + r];
+    fact[f] = s > 0;
+  }
+  // Step 2: "if a function has samples and none of its incoming call edges has a non-zero
+  // weight, we assign each of its incoming call edges a weight of one; we repeat this
+  // propagation through callers".  Each function's in-edges are written only by
+  // the thread that owns the function, so a round's result is race-free.
+  for (;;) {
+    __syncthreads();
+    if (t == 0) changed = 0;
+    __syncthreads();
+    for (uint32_t f = t; f < A.n_func; f += nt) {
+      uint32_t a = A.fin_ptr[f], b = A.fin_ptr[f + 1];
+      if (!fact[f] || a == b) continue;
+      bool zero = true;
+      for (uint32_t k = a; k < b; k++) zero &= w[A.fin_e[k]] == 0;
+      if (!zero) continue;
+      for (uint32_t k = a; k < b; k++) {
+        uint32_t e = A.fin_e[k];
+        w[e] = 1;
+        fact[A.caller[e]] = 1;
+      }
+      changed = 1;
+    }
+    __syncthreads();
+    if (!changed) break;
+  }
+  // DAG activity, then the guard (R12): the same rule on external in-edges of DAG nodes
+  for (uint32_t X = t; X < A.n_dag; X += nt) {
+    uint8_t act = 0;
+    for (uint32_t k = A.dmem_ptr[X]; k < A.dmem_ptr[X + 1]; k++) act |= fact[A.dmem[k]];
+    dact[X] = act;
+  }
+  for (;;) {
+    __syncthreads();
+    if (t == 0) changed = 0;
+    __syncthreads();
+    for (uint32_t X = t; X < A.n_dag; X += nt) {
+      uint32_t a = A.din_ptr[X], b = A.din_ptr[X + 1];
+      if (!dact[X] || a == b) continue;
+      bool zero = true;
+      for (uint32_t k = a; k < b; k++) zero &= w[A.din_e[k]] == 0;
+      if (!zero) continue;
+      for (uint32_t k = a; k < b; k++) {
+        uint32_t e = A.din_e[k];
+        w[e] = 1;
+        dact[A.scc_of[A.caller[e]]] = 1;
+      }
+      changed = 1;
+    }
+    __syncthreads();
+    if (!changed) break;
+  }
+  // W_X = total weight of the external calls into X
+  for (uint32_t X = t; X < A.n_dag; X += nt) {
+    uint64_t s = 0;
+    for (uint32_t k = A.din_ptr[X]; k < A.din_ptr[X + 1]; k++) s += w[A.din_e[k]];
+    A.W[X] = s;
+  }
+  // exact context count: paths from active roots through edges with w > 0, level by level
+  volatile uint64_t *paths = A.paths;
+  for (uint32_t L = 0; L < A.n_lev; L++) {
+    __syncthreads();
+    for (uint32_t q = A.dlev_ptr[L] + t; q < A.dlev_ptr[L + 1]; q += nt) {
+      uint32_t X = A.dlev_node[q];
+      uint32_t a = A.din_ptr[X], b = A.din_ptr[X + 1];
+      unsigned long long p = 0;
+      if (a == b) {
+        p = dact[X] ? 1 : 0;
+      } else {
+        for (uint32_t k = a; k < b; k++) {
+          uint32_t e = A.din_e[k];
+          if (w[e]) p = min(SAT, p + paths[A.scc_of[A.caller[e]]]);
+        }
+      }
+      paths[X] = p;
+    }
+  }
+  __syncthreads();
+  unsigned long long tot = 0;
+  for (uint32_t X = t; X < A.n_dag; X += nt) {
+    unsigned long long per = A.nontriv[X] ? 1ull + (A.dmem_ptr[X + 1] - A.dmem_ptr[X]) : 1ull;
+    unsigned long long p = paths[X];
+    tot = min(SAT, tot + (p > SAT / per ? SAT : p * per));
+  }
+  for (int o = 16; o; o >>= 1) tot = min(SAT, tot + __shfl_xor_sync(FULL, tot, o));
+  if ((t & 31) == 0) red[t >> 5] = tot;
+  __syncthreads();
+  if (t < 32) {
+    tot = t < (nt >> 5) ? red[t] : 0;
+    for (int o = 16; o; o >>= 1) tot = min(SAT, tot + __shfl_xor_sync(FULL, tot, o));
+    if (t == 0) A.count[0] = tot;
+  }
+}
+
+// block-wide exclusive scan of one u32 per thread; returns the block total in *total
+__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t *total) {
+  __shared__ uint32_t wsum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s;  // inclusive warp-prefix
+  }
+  __syncthreads();
+  *total = wsum[nw - 1];
+  return x - v + (wid ? wsum[wid - 1] : 0);
+}
+
+// roots: active DAG nodes without external in-edges, in DAG order (R15)
+__global__ void __launch_bounds__(1024) k_roots(uint32_t n_dag, const uint32_t *din_ptr, const uint8_t *dact,
+                                                const uint8_t *nontriv, uint32_t *parent, uint32_t *site,
+                                                uint32_t *node, uint8_t *kind, double *frac,
+                                                unsigned long long *n_out) {
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < n_dag; base += blockDim.x) {
+    uint32_t X = base + threadIdx.x;
+    uint32_t flag = X < n_dag && din_ptr[X] == din_ptr[X + 1] && dact[X];
+    uint32_t tot;
+    uint32_t pos = running + block_exscan(flag, &tot);
+    if (flag) {
+      parent[pos] = NONE;
+      site[pos] = NONE;
+      node[pos] = X;
+      kind[pos] = nontriv[X] ? GPA_CTX_SCC : GPA_CTX_FUNC;
+      frac[pos] = 1.0;
+    }
+    running += tot;
+  }
+  if (threadIdx.x == 0) n_out[0] = running;
+}
+
+struct LevelArgs {
+  const uint32_t *fout_ptr, *fout_e, *callee, *scc_of, *dmem_ptr, *dmem;
+  const uint8_t *nontriv;
+  const uint64_t *w, *W;
+  uint32_t *parent, *site, *node, *first_child, *n_children;
+  uint8_t *kind;
+  double *frac;
+};
+
+__device__ __forceinline__ uint32_t func_of_ctx(const LevelArgs &A, uint8_t k, uint32_t nd) {
+  return k == GPA_CTX_SCC_MEMBER ? nd : A.dmem[A.dmem_ptr[nd]];
+}
+
+__device__ __forceinline__ uint32_t child_count(const LevelArgs &A, uint64_t c) {
+  uint8_t k = A.kind[c];
+  uint32_t nd = A.node[c];
+  if (k == GPA_CTX_SCC) return A.dmem_ptr[nd + 1] - A.dmem_ptr[nd];
+  uint32_t g = func_of_ctx(A, k, nd), cnt = 0;
+  for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) cnt += A.w[A.fout_e[q]] != 0;
+  return cnt;
+}
+
+__global__ void k_level_count(LevelArgs A, uint64_t a, uint64_t b, uint32_t *tmp) {
+  for (uint64_t c = a + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < b; c += (uint64_t)gridDim.x * blockDim.x)
+    tmp[c - a] = child_count(A, c);
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *v, uint64_t m, uint32_t *bs) {
+  uint64_t i0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) s += i0 + q < m ? v[i0 + q] : 0;
+  uint32_t tot;
+  block_exscan(s, &tot);
+  if (threadIdx.x == 0) bs[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(uint32_t *bs, uint32_t nb, unsigned long long *total) {
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < nb; base += blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t v = i < nb ? bs[i] : 0, tot;
+    uint32_t ex = block_exscan(v, &tot);
+    if (i < nb) bs[i] = running + ex;
+    running += tot;
+  }
+  if (threadIdx.x == 0) total[0] = running;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t *v, uint64_t m, const uint32_t *bs) {
+  uint64_t i0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t x[kScanItems], s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    x[q] = i0 + q < m ? v[i0 + q] : 0;
+    s += x[q];
+  }
+  uint32_t tot;
+  uint32_t ex = block_exscan(s, &tot) + bs[blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    if (i0 + q < m) v[i0 + q] = ex;
+    ex += x[q];
+  }
+}
+
+__global__ void k_level_write(LevelArgs A, uint64_t a, uint64_t b, const uint32_t *off) {
+  for (uint64_t c = a + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < b; c += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t o = b + off[c - a];
+    uint8_t k = A.kind[c];
+    uint32_t nd = A.node[c];
+    double f = A.frac[c];
+    uint32_t cnt = 0;
+    if (k == GPA_CTX_SCC) {  // members in ascending function id (R14)
+      for (uint32_t q = A.dmem_ptr[nd]; q < A.dmem_ptr[nd + 1]; q++, cnt++) {
+        uint64_t d = o + cnt;
+        A.parent[d] = (uint32_t)c;
+        A.site[d] = NONE;
+        A.node[d] = A.dmem[q];
+        A.kind[d] = GPA_CTX_SCC_MEMBER;
+        A.frac[d] = f;
+      }
+    } else {  // external calls with w > 0, ascending call instruction (R15, R17)
+      uint32_t g = func_of_ctx(A, k, nd);
+      for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) {
+        uint32_t e = A.fout_e[q];
+        uint64_t we = A.w[e];
+        if (!we) continue;
+        uint32_t Y = A.scc_of[A.callee[e]];
+        uint64_t d = o + cnt++;
+        A.parent[d] = (uint32_t)c;
+        A.site[d] = e;
+        A.node[d] = Y;
+        A.kind[d] = A.nontriv[Y] ? GPA_CTX_SCC : GPA_CTX_FUNC;
+        A.frac[d] = __dmul_rn(f, __ddiv_rn(__ull2double_rn(we), __ull2double_rn(A.W[Y])));  // R13
+      }
+    }
+    A.first_child[c] = (uint32_t)o;
+    A.n_children[c] = cnt;
+  }
+}
+
+__global__ void k_excl(uint64_t n, const uint8_t *kind, const uint32_t *node, const double *frac,
+                       const uint32_t *dmem_ptr, const uint32_t *dmem, const uint64_t *S_f, double *excl) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n * GPA_SLOTS;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = x >> 4;
+    int r = (int)(x & 15);
+    uint8_t k = kind[c];
+    double v = 0.0;
+    if (k != GPA_CTX_SCC) {
+      uint32_t g = k == GPA_CTX_SCC_MEMBER ? node[c] : dmem[dmem_ptr[node[c]]];
+      v = __dmul_rn(frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
+    }
+    excl[x] = v;
+  }
+}
+
+__global__ void k_incl_level(uint64_t a, uint64_t b, const uint32_t *first_child, const uint32_t *n_children,
+                             const double *excl, double *incl) {
+  for (uint64_t x = a * GPA_SLOTS + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < b * GPA_SLOTS;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = x >> 4;
+    int r = (int)(x & 15);
+    double v = excl[x];
+    uint32_t d0 = first_child[c], nc = n_children[c];
+    for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, incl[(uint64_t)d * GPA_SLOTS + r]);
+    incl[x] = v;
+  }
+}
+
+unsigned grid_for(uint64_t work, unsigned threads) {
+  uint64_t b = (work + threads - 1) / threads;
+  if (b > 148 * 16) b = 148 * 16;
+  return (unsigned)(b ? b : 1);
+}
+
+LevelArgs level_args(const gpa_structure_s *s, gpa_cct_s *c) {
+  LevelArgs A;
+  A.fout_ptr = s->d_fout_ptr; A.fout_e = s->d_fout_e; A.callee = s->d_call_callee; A.scc_of = s->d_scc_of;
+  A.dmem_ptr = s->d_dmem_ptr; A.dmem = s->d_dmem; A.nontriv = s->d_dag_nontrivial;
+  A.w = c->w; A.W = c->W;
+  A.parent = c->parent; A.site = c->site; A.node = c->node; A.first_child = c->first_child;
+  A.n_children = c->n_children; A.kind = c->kind; A.frac = c->frac;
+  return A;
+}
+
+}  // namespace
+
+cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist, uint64_t *d_w, cudaStream_t st) {
+  uint32_t n = s->info.n_call;
+  if (!n) return cudaSuccess;
+  k_weights<<<grid_for(n, 256), 256, 0, st>>>(s->d_call_inst, n, d_hist, d_w);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
+                                 uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
+                                 unsigned long long *d_count, cudaStream_t st) {
+  // paths[] scratch lives behind W in the caller's allocation? keep it separate and simple:
+  static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
+  uint64_t *paths = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1), st);
+  if (e != cudaSuccess) return e;
+  PropArgs A;
+  A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels;
+  A.S_f = d_S_f; A.fin_ptr = s->d_fin_ptr; A.fin_e = s->d_fin_e; A.caller = s->d_call_caller;
+  A.scc_of = s->d_scc_of; A.din_ptr = s->d_din_ptr; A.din_e = s->d_din_e; A.dmem_ptr = s->d_dmem_ptr;
+  A.dmem = s->d_dmem; A.dlev_ptr = s->d_dlev_ptr; A.dlev_node = s->d_dlev_node; A.nontriv = s->d_dag_nontrivial;
+  A.w = d_w; A.W = d_W; A.paths = paths; A.fact = d_func_active; A.dact = d_dag_active; A.count = d_count;
+  k_propagate<<<1, 1024, 0, st>>>(A);
+  count_launches(1);
+  e = cudaGetLastError();
+  cudaError_t e2 = cudaFreeAsync(paths, st);
+  return e != cudaSuccess ? e : e2;
+}
+
+cudaError_t launch_cct_roots(const gpa_structure_s *s, const uint8_t *d_dag_active, gpa_cct_s *c,
+                             unsigned long long *d_n, cudaStream_t st) {
+  k_roots<<<1, 1024, 0, st>>>(s->info.n_dag, s->d_din_ptr, d_dag_active, s->d_dag_nontrivial, c->parent, c->site,
+                              c->node, c->kind, c->frac, d_n);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a, uint64_t b, uint32_t *d_tmp,
+                             uint32_t *d_bs, unsigned long long *d_next, cudaStream_t st) {
+  LevelArgs A = level_args(s, c);
+  uint64_t m = b - a;
+  k_level_count<<<grid_for(m, 256), 256, 0, st>>>(A, a, b, d_tmp);
+  uint64_t nb = (m + kScanTile - 1) / kScanTile;
+  if (nb > 65536) return cudaErrorInvalidValue;
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(d_tmp, m, d_bs);
+  k_scan_top<<<1, kScanThreads, 0, st>>>(d_bs, (uint32_t)nb, d_next);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(d_tmp, m, d_bs);
+  k_level_write<<<grid_for(m, 256), 256, 0, st>>>(A, a, b, d_tmp);
+  count_launches(5);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cct_excl(const gpa_structure_s *s, gpa_cct_s *c, cudaStream_t st) {
+  if (!c->n) return cudaSuccess;
+  k_excl<<<grid_for(c->n * GPA_SLOTS, 256), 256, 0, st>>>(c->n, c->kind, c->node, c->frac, s->d_dmem_ptr, s->d_dmem,
+                                                        c->S_f, c->excl);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStream_t st) {
+  if (b <= a) return cudaSuccess;
+  k_incl_level<<<grid_for((b - a) * GPA_SLOTS, 256), 256, 0, st>>>(a, b, c->first_child, c->n_children, c->excl,
+                                                                  c->incl);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace gpa

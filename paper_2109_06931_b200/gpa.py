@@ -1,0 +1,310 @@
+"""Thin Python binding of libgpa (include/gpa.h).  Argument marshalling only.
+
+Every call goes through the C ABI in ``libgpa.so`` next to this file; every step of the
+path runs in the library's CUDA kernels.  There is no fallback: importing this module
+raises if the library is missing, and each call raises GpaError on a non-OK status.
+Device buffers are torch CUDA tensors (int64 views are reinterpreted as u64 by the
+library); streams are torch.cuda.Stream objects (default: the current stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgpa.so")
+
+SLOTS, VALID_SLOTS, SLOT_INVALID, CLASSES, NUM_DERIVED = 16, 12, 15, 16, 33
+NONE = 0xFFFFFFFF
+SCOPES = {"INST": 0, "LINE": 1, "LOOP": 2, "INLINE": 3, "FUNC": 4, "CCT_EXCL": 5, "CCT_INCL": 6}
+CTX_FUNC, CTX_SCC, CTX_SCC_MEMBER = 0, 1, 2
+WEIGHTS_SAMPLES, WEIGHTS_EXACT = 0, 1
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STRUCTURE", 3: "CAPACITY", 4: "OUT_OF_MEMORY", 5: "CUDA",
+          6: "INTERNAL", 7: "UNSUPPORTED"}
+
+
+class GpaError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: GPA_ERR_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_vp = ctypes.c_void_p
+_u32, _u64 = ctypes.c_uint32, ctypes.c_uint64
+
+
+class StructureDesc(ctypes.Structure):
+    _fields_ = [("n_inst", _u32), ("inst_addr", _vp), ("inst_len", _vp), ("inst_class", _vp), ("inst_scope", _vp),
+                ("n_scope", _u32), ("scope_parent", _vp), ("scope_kind", _vp),
+                ("n_func", _u32), ("func_scope", _vp),
+                ("n_call", _u32), ("call_inst", _vp), ("call_callee", _vp)]
+
+
+class StructureInfo(ctypes.Structure):
+    _fields_ = [(k, _u32) for k in ("n_inst", "n_scope", "n_line", "n_loop", "n_inline", "n_func", "n_call",
+                                    "n_dag", "n_scc", "dag_levels")] + \
+               [("cct_path_bound", _u64), ("lookup_mode", _u32), ("granule_shift", _u32),
+                ("lookup_entries", _u64), ("device_bytes", _u64)]
+
+
+class CctView(ctypes.Structure):
+    _fields_ = [("n", _u64), ("parent", _vp), ("site", _vp), ("node", _vp), ("kind", _vp),
+                ("first_child", _vp), ("n_children", _vp), ("frac", _vp), ("excl", _vp), ("incl", _vp),
+                ("n_call", _u32), ("n_func", _u32), ("n_dag", _u32),
+                ("call_weight", _vp), ("dag_weight", _vp), ("dag_active", _vp), ("func_active", _vp),
+                ("func_hist", _vp)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    S = ctypes.c_int
+    sig = {
+        "gpa_version": ([], ctypes.c_char_p), "gpa_last_error": ([], ctypes.c_char_p),
+        "gpa_validate_structure": ([ctypes.POINTER(StructureDesc)], S),
+        "gpa_load_structure": ([ctypes.POINTER(StructureDesc), ctypes.c_int, ctypes.POINTER(_vp)], S),
+        "gpa_get_structure_info": ([_vp, ctypes.POINTER(StructureInfo)], S),
+        "gpa_scope_rows": ([_vp, ctypes.c_int, ctypes.POINTER(_u64), _vp], S),
+        "gpa_get_scc": ([_vp, _vp], S),
+        "gpa_free_structure": ([_vp], None),
+        "gpa_attribute_samples": ([_vp, _vp, _u64, _vp, _vp, _vp, _vp], S),
+        "gpa_attribute_samples_host": ([_vp, _vp, _u64, _vp, _vp, _vp], S),
+        "gpa_reconstruct_cct": ([_vp, _vp, ctypes.c_int, _u64, ctypes.POINTER(_vp), ctypes.POINTER(_u64), _vp], S),
+        "gpa_get_cct_view": ([_vp, ctypes.POINTER(CctView)], S),
+        "gpa_free_cct": ([_vp], None),
+        "gpa_derive_metrics": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], S),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+_lib = _load()
+EXPORTED = tuple(n for n in dir(_lib) if n.startswith("gpa_"))
+
+
+def version() -> str:
+    return _lib.gpa_version().decode()
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise GpaError(status, where, _lib.gpa_last_error().decode())
+
+
+def _stream_ptr(stream, device):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def _ptr(t, name, nbytes_min=0):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise GpaError(1, name, "expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise GpaError(1, name, "expected a contiguous tensor")
+    if t.numel() * t.element_size() < nbytes_min:
+        raise GpaError(1, name, f"buffer holds {t.numel() * t.element_size()} bytes, needs {nbytes_min}")
+    return t.data_ptr()
+
+
+_DESC_TYPES = dict(inst_addr=np.uint64, inst_len=np.uint16, inst_class=np.uint8, inst_scope=np.uint32,
+                   scope_parent=np.uint32, scope_kind=np.uint8, func_scope=np.uint32, call_inst=np.uint32,
+                   call_callee=np.uint32)
+
+
+def _desc(d: dict):
+    arrs = {k: np.ascontiguousarray(d[k], dtype=t) for k, t in _DESC_TYPES.items()}
+    p = {k: (a.ctypes.data if a.size else None) for k, a in arrs.items()}
+    desc = StructureDesc(n_inst=len(arrs["inst_addr"]), n_scope=len(arrs["scope_parent"]),
+                         n_func=len(arrs["func_scope"]), n_call=len(arrs["call_inst"]), **p)
+    return desc, arrs
+
+
+def validate_structure(d: dict) -> None:
+    desc, keep = _desc(d)
+    _check(_lib.gpa_validate_structure(ctypes.byref(desc)), "gpa_validate_structure")
+
+
+class Structure:
+    """A loaded, device-resident, immutable program structure (gpa_structure)."""
+
+    def __init__(self, d: dict, device: int = 0):
+        desc, keep = _desc(d)
+        h = _vp()
+        _check(_lib.gpa_load_structure(ctypes.byref(desc), device, ctypes.byref(h)), "gpa_load_structure")
+        self._h = h
+        self.device = device
+        inf = StructureInfo()
+        _check(_lib.gpa_get_structure_info(self._h, ctypes.byref(inf)), "gpa_get_structure_info")
+        self.info = {k: getattr(inf, k) for k, _ in StructureInfo._fields_}
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise GpaError(1, "Structure", "freed")
+        return self._h
+
+    def rows(self, scope: str) -> np.ndarray:
+        n = _u64()
+        _check(_lib.gpa_scope_rows(self.handle, SCOPES[scope], ctypes.byref(n), None), "gpa_scope_rows")
+        ids = np.empty(n.value, np.uint32)
+        _check(_lib.gpa_scope_rows(self.handle, SCOPES[scope], ctypes.byref(n),
+                                   ids.ctypes.data if n.value else None), "gpa_scope_rows")
+        return ids
+
+    def scc_of(self) -> np.ndarray:
+        out = np.empty(self.info["n_func"], np.uint32)
+        _check(_lib.gpa_get_scc(self.handle, out.ctypes.data if len(out) else None), "gpa_get_scc")
+        return out
+
+    def free(self):
+        if self._h is not None:
+            _lib.gpa_free_structure(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def load_structure(d: dict, device: int = 0) -> Structure:
+    return Structure(d, device)
+
+
+def attribute_samples(s: Structure, samples, inst_hist, unattributed, rec_inst=None, n: int | None = None,
+                      stream=None) -> None:
+    """a-1..a-3 on device records (`samples`: CUDA tensor of 16-B records, any dtype)."""
+    nb = samples.numel() * samples.element_size()
+    n = nb // 16 if n is None else int(n)
+    _check(_lib.gpa_attribute_samples(
+        s.handle, _ptr(samples, "samples", 16 * n), n,
+        _ptr(inst_hist, "inst_hist", 128 * s.info["n_inst"]), _ptr(unattributed, "unattributed", 128),
+        _ptr(rec_inst, "rec_inst", 4 * n), _stream_ptr(stream, samples.device)), "gpa_attribute_samples")
+
+
+def attribute_samples_host(s: Structure, samples, inst_hist, unattributed, stream=None) -> None:
+    """Same result from HOST records (numpy array or CPU tensor, pinned or pageable)."""
+    if isinstance(samples, np.ndarray):
+        arr = np.ascontiguousarray(samples)
+        ptr, nb = arr.ctypes.data, arr.nbytes
+    else:
+        if samples.is_cuda or not samples.is_contiguous():
+            raise GpaError(1, "samples", "expected a contiguous host tensor")
+        ptr, nb = samples.data_ptr(), samples.numel() * samples.element_size()
+    _check(_lib.gpa_attribute_samples_host(
+        s.handle, ptr, nb // 16, _ptr(inst_hist, "inst_hist", 128 * s.info["n_inst"]),
+        _ptr(unattributed, "unattributed", 128), _stream_ptr(stream, inst_hist.device)),
+        "gpa_attribute_samples_host")
+
+
+class _DevArray:
+    """Zero-copy view of a library-owned device array (for torch.as_tensor)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr or 0, False), "version": 3}
+
+
+class Cct:
+    """A reconstructed GPU calling-context tree (gpa_cct), library-owned device arrays."""
+
+    _FIELDS = {"parent": ("<i4", 1), "site": ("<i4", 1), "node": ("<i4", 1), "kind": ("|u1", 1),
+               "first_child": ("<i4", 1), "n_children": ("<i4", 1), "frac": ("<f8", 1), "excl": ("<f8", 16),
+               "incl": ("<f8", 16)}
+
+    def __init__(self, h, device):
+        self._h = h
+        self.device = device
+        v = CctView()
+        _check(_lib.gpa_get_cct_view(h, ctypes.byref(v)), "gpa_get_cct_view")
+        self._v = v
+        self.n = v.n
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise GpaError(1, "Cct", "freed")
+        return self._h
+
+    def tensors(self) -> dict:
+        """Zero-copy torch views (valid until free())."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        v, n = self._v, self.n
+        out = {}
+        dt = {"<i4": torch.int32, "|u1": torch.uint8, "<f8": torch.float64, "<i8": torch.int64}
+        for k, (ts, w) in self._FIELDS.items():
+            shape = (n, w) if w > 1 else (n,)
+            out[k] = torch.as_tensor(_DevArray(getattr(v, k), shape, ts), device=dev) if n else \
+                torch.empty(shape, dtype=dt[ts], device=dev)
+        # u64 arrays are exposed as int64 views (torch has no general uint64 support)
+        extra = {"call_weight": ("<i8", v.n_call), "dag_weight": ("<i8", v.n_dag), "dag_active": ("|u1", v.n_dag),
+                 "func_active": ("|u1", v.n_func), "func_hist": ("<i8", v.n_func * 16)}
+        for k, (ts, m) in extra.items():
+            ptr = getattr(v, k)
+            out[k] = torch.as_tensor(_DevArray(ptr, (m,), ts), device=dev) if m and ptr else \
+                torch.empty(0, dtype=dt[ts], device=dev)
+        return out
+
+    def to_numpy(self) -> dict:
+        t = self.tensors()
+        out = {k: x.cpu().numpy() for k, x in t.items()}
+        for k in ("call_weight", "dag_weight", "func_hist"):
+            out[k] = out[k].astype(np.int64).view(np.uint64)
+        for k in ("parent", "site", "node", "first_child", "n_children"):
+            out[k] = out[k].astype(np.int32).view(np.uint32)
+        out["func_hist"] = out["func_hist"].reshape(-1, 16)
+        out["n"] = self.n
+        return out
+
+    def free(self):
+        if self._h is not None:
+            _lib.gpa_free_cct(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def reconstruct_cct(s: Structure, inst_hist, mode: int = WEIGHTS_SAMPLES, max_contexts: int = (1 << 63) - 1,
+                    stream=None):
+    """a-6..a-9.  Returns a Cct, or the context count when max_contexts == 0."""
+    h = _vp()
+    n = _u64()
+    _check(_lib.gpa_reconstruct_cct(s.handle, _ptr(inst_hist, "inst_hist", 128 * s.info["n_inst"]), mode,
+                                    max_contexts, ctypes.byref(h), ctypes.byref(n),
+                                    _stream_ptr(stream, inst_hist.device)), "gpa_reconstruct_cct")
+    if max_contexts == 0:
+        return n.value
+    return Cct(h, s.device)
+
+
+def derive_metrics(s: Structure, scope: str, inst_hist=None, cct: Cct | None = None, scope_hist=None,
+                   scope_mix=None, metrics=None, stream=None) -> None:
+    """a-5 + a-10 for one row set (see gpa.h)."""
+    dev = (inst_hist if inst_hist is not None else metrics).device
+    _check(_lib.gpa_derive_metrics(s.handle, SCOPES[scope], _ptr(inst_hist, "inst_hist"),
+                                   cct.handle if cct is not None else None, _ptr(scope_hist, "scope_hist"),
+                                   _ptr(scope_mix, "scope_mix"), _ptr(metrics, "metrics"),
+                                   _stream_ptr(stream, dev)), "gpa_derive_metrics")
+
+
+def scope_row_count(s: Structure, scope: str, cct: Cct | None = None) -> int:
+    if scope.startswith("CCT"):
+        return cct.n
+    n = _u64()
+    _check(_lib.gpa_scope_rows(s.handle, SCOPES[scope], ctypes.byref(n), None), "gpa_scope_rows")
+    return n.value
