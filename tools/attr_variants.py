@@ -42,5 +42,5 @@ if __name__ == "__main__":
         env = dict(os.environ, GPA_ATTR_VARIANT=v)
         out = subprocess.run([sys.executable, "-c", CHILD, name, str(records), "5"], env=env, capture_output=True,
                              text=True)
-        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-2000:]
+        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:].replace("\n", " | ")
         print(f"variant {v}: {line}", flush=True)
