@@ -222,7 +222,7 @@ def run_gpa(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    l0 = gpa._lib.gpa_kernel_launches()
+    l0 = gpa.kernel_launches()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -236,7 +236,7 @@ def run_gpa(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    launches = gpa._lib.gpa_kernel_launches() - l0
+    launches = gpa.kernel_launches() - l0
     ms = t0.elapsed_time(t1) / args.steps
     attr_ms = sum(x.elapsed_time(y) for x, y in zip(ev_a0, ev_a1)) / len(ev_a0)
     if world > 1:

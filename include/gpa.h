@@ -181,6 +181,12 @@ GPA_API const char *gpa_last_error(void);
 /* Kernels this process has launched through the library so far (all devices; a
  * diagnostic counter for benchmarks: launches inside a timed region = difference). */
 GPA_API uint64_t gpa_kernel_launches(void);
+/* Force the attribution kernel process-wide (testing / benchmarking; results are identical):
+ * 0 automatic (default), 1 register streaming, 2 TMA ring with L2 reductions, 3 TMA ring with
+ * shared-memory heavy-hitter rows (used only where applicable: granule map, >= 2^21 records,
+ * >= 1024 instructions; otherwise the automatic choice).  Also settable by the environment
+ * variable GPA_ATTR_VARIANT before the first call.  DESIGN.md §7 describes the kernels. */
+GPA_API gpa_status gpa_set_attr_kernel(int which);
 /* Validate a structure description on the host only (no device touched).  Same checks and
  * status as gpa_load_structure. */
 GPA_API gpa_status gpa_validate_structure(const gpa_structure_desc *desc);

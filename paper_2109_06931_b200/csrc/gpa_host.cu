@@ -474,6 +474,12 @@ const char *gpa_version(void) { return "libgpa 0.1 (sm_100a)"; }
 const char *gpa_last_error(void) { return g_err.c_str(); }
 uint64_t gpa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
+gpa_status gpa_set_attr_kernel(int which) {
+  if (which < 0 || which > 3) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-3)", which);
+  gpa::set_attr_kernel(which);
+  return GPA_OK;
+}
+
 gpa_status gpa_validate_structure(const gpa_structure_desc *desc) {
   Derived dv;
   return validate(desc, &dv);

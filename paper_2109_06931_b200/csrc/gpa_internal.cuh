@@ -82,6 +82,7 @@ struct gpa_cct_s {
 // ---- kernel launch accounting (gpa_kernel_launches) ------------------------------------------
 namespace gpa {
 void count_launches(uint64_t k);
+void set_attr_kernel(int which);
 }
 
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------

@@ -1,12 +1,28 @@
 // k_attr.cu — a-1..a-3: PC-sample decode, pc -> instruction lookup, per-instruction x
-// stall-reason histogram (§4.2; §4.5; §5).
+// stall-reason histogram (§4.2 P:365-374 "an instruction address, a stall reason,
+// and a count"; §4.5 P:475-479 raw metric = sum; §5 P:614-617 disjoint relocated ranges).
 //
-// One persistent, grid-stride kernel streams the 16-B records (one 128-bit non-allocating
-// load each, several in flight per thread), maps pc -> instruction through the load-time
-// granule map (L2/L1-resident; exact range semantics, reading R6), and adds `count` to
-// H[inst][slot] (or U[slot]) with a u64 reduction in L2.  Records of a warp that hit the
-// same bin are combined first (match.any + shuffles), so a hot bin costs one L2 atomic per
-// warp instead of one per record.
+// Three kernels, chosen by launch_attribute (DESIGN.md §7 has the measurements behind them):
+//
+//  K_attr_hot (default for large calls, granule map present)
+//     Measured on B200 (tools/microbench.cu): u64 reductions into L2 sustain ~1.9e11/s at
+//     spread addresses (each RED lane costs ~1.3 SM cycles of LSU issue), far below the
+//     ~4.3e11 records/s the HBM roofline allows; shared-memory u32 atomics sustain ~1.3e12/s.
+//     So the rows of the hottest instructions are privatised per CTA in shared memory:
+//       1. k_sample       instruction hits in 64 evenly spaced chunks (2^21 records)
+//       2. k_vhist/k_pick/k_assign   choose up to kHotRows instructions with the most hits
+//       3. k_codemap      per-call code map: cold instruction i -> i<<4, hot row r -> r<<4|1,
+//                         unmapped -> ~0 (one gather resolves a record, one OR forms the index)
+//       4. k_attr_hot     persistent CTA per SM.  A producer warp streams record tiles
+//                         HBM -> shared memory with 1-D bulk copies (cp.async.bulk = TMA engine,
+//                         L2 evict-first) into a 4-stage mbarrier ring; 16 consumer warps copy
+//                         their records to registers, free the stage, gather the codes of the
+//                         tile two ahead, and accumulate: hot valid-slot records -> u32 shared
+//                         atomics (a u32 wrap, old + cnt < old, is repaid as +2^32 in L2, so
+//                         any count is exact), others -> u64 L2 reductions.  Each CTA flushes
+//                         its rows once.  The hot set only moves where a count lands first.
+//  K_attr_tma (mid-size calls): the same TMA ring, warp-aggregated L2 reductions only.
+//  K_attr_stream (small calls, sparse address spaces via binary search): register streaming.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -16,10 +32,9 @@
 namespace gpa {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kUnroll = 4;  // records in flight per thread per iteration
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
+// ---- device helpers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -32,13 +47,51 @@ __device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long
   asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t atoms_add(uint32_t saddr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// pc -> instruction: granule map (MODE 0) or binary search over the sorted starts (MODE 1)
 template <int MODE>
 __device__ __forceinline__ uint32_t lookup(const AttrTables &T, uint64_t pc) {
-  if (!(pc >= T.base && pc < T.end)) return NONE;
   if (MODE == 0) {
-    return __ldg(T.gmap + ((pc - T.base) >> T.gshift));
+    uint64_t g = (pc - T.base) >> T.gshift;  // pc < base wraps to a huge g
+    return g < T.n_gran ? __ldg(T.gmap + g) : NONE;
   } else {
-    // largest start <= pc (binary search over the sorted starts), then the length check
+    if (!(pc >= T.base && pc < T.end)) return NONE;
     uint32_t lo = 0, hi = T.n_inst;
     while (lo < hi) {
       uint32_t mid = (lo + hi) >> 1;
@@ -70,205 +123,136 @@ __device__ __forceinline__ void warp_accumulate(uint32_t key, uint32_t cnt, unsi
   if (key != FULL && lane == __ffs(peers) - 1) red_add_u64(target, total);
 }
 
+__device__ __forceinline__ void accumulate_one(uint32_t i, uint4 v, bool live, unsigned long long *H,
+                                               unsigned long long *U) {
+  uint32_t cnt = v.z, stall = v.w & 0xFFFFu;
+  uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
+  uint32_t key = (!live || cnt == 0) ? FULL : (i == NONE ? (0xFFFFFFE0u | slot) : (i << 4 | slot));
+  warp_accumulate(key, cnt, i == NONE ? U + slot : H + ((uint64_t)i << 4 | slot));
+}
+
+// ---- K_attr_stream: register streaming ---------------------------------------------------------
+constexpr int kStreamThreads = 256, kStreamUnroll = 4;
+
 template <int MODE, bool REC>
-__global__ void __launch_bounds__(kThreads) k_attribute(AttrTables T, const uint4 *__restrict__ rec, uint64_t n,
-                                                        unsigned long long *__restrict__ H,
-                                                        unsigned long long *__restrict__ U,
-                                                        uint32_t *__restrict__ rec_inst) {
+__global__ void __launch_bounds__(kStreamThreads)
+    k_attr_stream(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
+                  unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst) {
   const int lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  const uint64_t step = nwarps * 32 * kUnroll;
-  // each warp owns 32*kUnroll consecutive records per iteration (coalesced 16-B loads)
-  for (uint64_t base = warp * 32 * kUnroll; base < n; base += step) {
-    uint4 v[kUnroll];
+  const uint64_t warp = ((uint64_t)blockIdx.x * kStreamThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kStreamThreads) >> 5;
+  for (uint64_t base = warp * 32 * kStreamUnroll; base < n; base += nwarps * 32 * kStreamUnroll) {
+    uint4 v[kStreamUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; u++) {
+    for (int u = 0; u < kStreamUnroll; u++) {
       uint64_t k = base + (uint64_t)u * 32 + lane;
       v[u] = k < n ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
     }
+    uint32_t inst[kStreamUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; u++) {
+    for (int u = 0; u < kStreamUnroll; u++) inst[u] = lookup<MODE>(T, ((uint64_t)v[u].y << 32) | v[u].x);
+#pragma unroll
+    for (int u = 0; u < kStreamUnroll; u++) {
       uint64_t k = base + (uint64_t)u * 32 + lane;
-      bool live = k < n;
-      uint64_t pc = ((uint64_t)v[u].y << 32) | v[u].x;
-      uint32_t cnt = v[u].z;
-      uint32_t stall = v[u].w & 0xFFFFu;
-      uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
-      uint32_t i = lookup<MODE>(T, pc);
-      if (REC && live) rec_inst[k] = i;
-      uint32_t key = !live ? FULL : (i == NONE ? (0xFFFFFFE0u | slot) : (i << 4 | slot));
-      unsigned long long *target = i == NONE ? U + slot : H + ((uint64_t)i << 4 | slot);
-      // live records with count 0 contribute nothing; keep them idle
-      if (cnt == 0) key = FULL;
-      warp_accumulate(key, cnt, target);
+      if (REC && k < n) rec_inst[k] = inst[u];
+      accumulate_one(inst[u], v[u], k < n, H, U);
     }
   }
 }
 
-
-// ---- v2: TMA-fed persistent kernel ----------------------------------------------------------
-// One CTA per SM.  A producer warp streams tiles of S records HBM -> shared memory with 1-D
-// bulk copies (cp.async.bulk, the TMA engine) into an NST-stage ring guarded by mbarriers,
-// with an L2 evict-first policy so the stream does not push the histogram and the granule
-// map out of L2.  NC consumer warps copy their R records per tile to registers, release the
-// stage at once (so the next bulk copy can land), issue all R granule-map gathers before
-// using any (R independent L2 round trips in flight per lane), then accumulate.
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity), "r"(0x989680u)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
+// ---- TMA ring geometry ----------------------------------------------------------------------------
 template <int NC, int R, int NST>
-struct TmaCfg {
-  static constexpr int kConsumers = NC;
-  static constexpr int kPerLane = R;
-  static constexpr int kStages = NST;
-  static constexpr int kTile = NC * 32 * R;                   // records per stage
+struct Ring {
+  static constexpr int kConsumers = NC, kPerLane = R, kStages = NST;
+  static constexpr int kTile = NC * 32 * R;  // records per stage
+  static constexpr size_t kBytes = (size_t)NST * kTile * 16;
   static constexpr int kThreads = (NC + 1) * 32;
-  static constexpr size_t kSmem = (size_t)NST * kTile * 16 + 2 * NST * sizeof(uint64_t);
+  static_assert((NST & (NST - 1)) == 0, "stages must be a power of two");
 };
 
-template <class C, int MODE, bool REC, bool AGG>
-__global__ void __launch_bounds__(C::kThreads, 1)
-    k_attribute_tma(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
-                    unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int S = C::kTile, NST = C::kStages, NC = C::kConsumers, R = C::kPerLane;
-  uint4 *ring = reinterpret_cast<uint4 *>(smem);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)NST * S * 16);
-  uint64_t *empty = full + NST;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// producer warp body: one elected lane drives the bulk-copy engine over this CTA's tiles
+template <class RG>
+__device__ __forceinline__ void ring_produce(uint4 *ring, uint64_t *full, uint64_t *empty, const uint4 *rec,
+                                             uint64_t n) {
+  constexpr int S = RG::kTile, NST = RG::kStages;
   const uint64_t ntiles = (n + S - 1) / S;
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  uint32_t it = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
+    uint64_t left = n - tile * S;
+    uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);
+    mbar_arrive_expect_tx(full + st, bytes);
+    bulk_g2s(ring + (size_t)st * S, rec + tile * S, bytes, full + st, policy);
+  }
+}
+
+__device__ __forceinline__ void ring_init(uint64_t *full, uint64_t *empty, int nst, uint32_t consumers) {
   if (threadIdx.x == 0) {
-    for (int q = 0; q < NST; q++) {
+    for (int q = 0; q < nst; q++) {
       mbar_init(full + q, 1);
-      mbar_init(empty + q, NC);
+      mbar_init(empty + q, consumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+}
+
+// ---- K_attr_tma: TMA ring + warp-aggregated L2 reductions ----------------------------------------
+using RingTma = Ring<16, 4, 4>;
+
+template <int MODE, bool REC>
+__global__ void __launch_bounds__(RingTma::kThreads, 1)
+    k_attr_tma(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
+               unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  using RG = RingTma;
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes);
+  uint64_t *empty = full + NST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ring_init(full, empty, NST, NC);
   __syncthreads();
-  if (warp == NC) {  // producer warp: one elected lane drives the bulk-copy engine
-    if (lane == 0) {
-      uint64_t policy;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      uint32_t it = 0;
-      for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        uint32_t st = it % NST, ph = (it / NST) & 1;
-        if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
-        uint64_t left = n - tile * S;
-        uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);
-        mbar_arrive_expect_tx(full + st, bytes);
-        bulk_g2s(ring + (size_t)st * S, rec + tile * S, bytes, full + st, policy);
-      }
-    }
+  if (warp == NC) {
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n);
     return;
   }
+  const uint64_t ntiles = (n + S - 1) / S;
   uint32_t it = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    uint32_t st = it % NST, ph = (it / NST) & 1;
+    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
     uint64_t left = n - tile * S;
     uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
     uint4 v[R];
 #pragma unroll
-    for (int u = 0; u < R; u++) {
-      uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
-      v[u] = j < m ? ring[(size_t)st * S + j] : make_uint4(0, 0, 0, 0);
-    }
+    for (int u = 0; u < R; u++) v[u] = ring[(size_t)st * S + (u * NC + warp) * 32 + lane];
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);   // registers hold the records: stage free
+    if (lane == 0) mbar_arrive(empty + st);
     uint32_t inst[R];
 #pragma unroll
     for (int u = 0; u < R; u++) inst[u] = lookup<MODE>(T, ((uint64_t)v[u].y << 32) | v[u].x);
 #pragma unroll
     for (int u = 0; u < R; u++) {
       uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
-      bool live = j < m;
-      uint32_t i = inst[u], cnt = v[u].z, stall = v[u].w & 0xFFFFu;
-      uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
-      if (REC && live) rec_inst[tile * S + j] = i;
-      unsigned long long *target = i == NONE ? U + slot : H + ((uint64_t)i << 4 | slot);
-      if (AGG) {
-        uint32_t key = (!live || cnt == 0) ? FULL : (i == NONE ? (0xFFFFFFE0u | slot) : (i << 4 | slot));
-        warp_accumulate(key, cnt, target);
-      } else if (live && cnt) {
-        red_add_u64(target, cnt);
-      }
+      if (REC && j < m) rec_inst[tile * S + j] = inst[u];
+      accumulate_one(inst[u], v[u], j < m, H, U);
     }
   }
 }
 
-using CfgA = TmaCfg<16, 4, 6>;
-
-template <class C, int MODE, bool REC, bool AGG>
-cudaError_t launch_tma(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
-                       unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
-  auto kern = k_attribute_tma<C, MODE, REC, AGG>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-  if (e != cudaSuccess) return e;
-  uint64_t ntiles = (n + C::kTile - 1) / C::kTile;
-  unsigned blocks = (unsigned)(ntiles < (uint64_t)sm_count ? ntiles : (uint64_t)sm_count);
-  kern<<<blocks, C::kThreads, C::kSmem, st>>>(T, rec, n, H, U, ri);
-  return cudaGetLastError();
-}
-
-int attr_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("GPA_ATTR_VARIANT");
-    v = e ? atoi(e) : 6;
-  }
-  return v;
-}
-
-// ---- v3: heavy-hitter rows privatised in shared memory ---------------------------------------
-// Measured on B200 (tools/microbench.cu): u64 reductions into L2 sustain ~1.9e11/s at spread
-// addresses and far less on hot addresses, while the HBM roofline needs ~4.3e11 records/s;
-// shared-memory u32 atomics sustain ~1.3e12/s.  So the histogram rows of the hottest
-// instructions are privatised per CTA in shared memory:
-//   1. k_sample    count instruction hits in 64 evenly spaced chunks of the stream (2^21 records)
-//   2. k_vhist / k_pick / k_assign   pick up to KROWS instructions with the largest counts
-//   3. k_codemap   per-call copy of the granule map: code = hot row | 0x80000000, or the
-//                  instruction index (one gather still resolves a record)
-//   4. k_attr_hot  stream records (registers, software-pipelined one iteration ahead); hot
-//                  valid-slot records -> u32 shared atomics, others -> u64 L2 reductions;
-//                  a u32 wrap (old + cnt < old) is repaid as +2^32 in L2, so the result is
-//                  exact for any counts; each CTA flushes its rows once at the end.
-// The hot set only changes where a count is added first, never the result (bit-exact).
-constexpr int kHotRows = 4608;                 // 4608 rows x 12 slots x 4 B = 216 KiB smem
+// ---- K_attr_hot: heavy-hitter rows in shared memory ---------------------------------------------
 constexpr int kHotSlots = GPA_VALID_SLOTS;
-constexpr size_t kHotSmem = (size_t)kHotRows * kHotSlots * 4;
+constexpr int kHotRows = 3328;                     // 3328 x 12 x 4 B = 156 KiB
+using RingHot = Ring<16, 2, 4>;                    // 4 x 16 KiB stages
+constexpr int kLook = 2;                           // tiles of records + codes in flight ahead
+constexpr size_t kHotTab = (size_t)kHotRows * kHotSlots * 4;
+constexpr size_t kHotSmem = RingHot::kBytes + kHotTab + 2 * RingHot::kStages * 8;
 constexpr int kSampleChunks = 64, kSampleChunk = 1 << 15;
+constexpr uint64_t kHotMinRecords = (uint64_t)kSampleChunks * kSampleChunk;
 constexpr int kVBins = 4096;
-constexpr int kHotThreads = 768;
-constexpr int kHotR = 4;
 
 __global__ void k_sample(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
   const uint64_t total = (uint64_t)kSampleChunks * kSampleChunk;
@@ -281,24 +265,68 @@ __global__ void k_sample(AttrTables T, const uint4 *__restrict__ rec, uint64_t n
   }
 }
 
-__global__ void k_vhist(const uint32_t *__restrict__ scnt, uint32_t n_inst, uint32_t *__restrict__ V) {
+// histogram of the per-instruction sample counts (capped at kVBins-1), block-privatised
+__global__ void __launch_bounds__(1024) k_vhist(const uint32_t *__restrict__ scnt, uint32_t n_inst,
+                                                uint32_t *__restrict__ V) {
+  __shared__ uint32_t h[kVBins];
+  for (int c = threadIdx.x; c < kVBins; c += blockDim.x) h[c] = 0;
+  __syncthreads();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += gridDim.x * blockDim.x) {
     uint32_t c = scnt[i];
-    if (c) atomicAdd(V + (c < kVBins - 1 ? c : kVBins - 1), 1u);
+    if (c) atomicAdd(h + (c < kVBins - 1 ? c : kVBins - 1), 1u);
   }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kVBins; c += blockDim.x)
+    if (h[c]) atomicAdd(V + c, h[c]);
 }
 
-// smallest threshold t >= 1 whose suffix count fits in kHotRows (or the top bucket)
-__global__ void k_pick(const uint32_t *__restrict__ V, uint32_t *__restrict__ thr, uint32_t rows) {
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0, t = kVBins - 1;
-    for (int c = kVBins - 1; c >= 1; c--) {
-      if (acc + V[c] > rows) break;
-      acc += V[c];
-      t = c;
+// thr[0] = smallest t >= 1 whose suffix count sum_{c >= t} V[c] fits in `rows` (or the top
+// bucket if even it does not fit; k_assign then caps the rows); thr[1] = 0 (rows assigned).
+// One CTA of 1024 threads; thread t owns the 4 bins c = 4095-4t .. 4092-4t.
+__global__ void __launch_bounds__(1024) k_pick(const uint32_t *__restrict__ V, uint32_t *__restrict__ thr,
+                                               uint32_t rows) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t n_over;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) n_over = 0;
+  uint32_t v[4], s = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    v[q] = V[kVBins - 1 - (4 * t + q)];
+    s += v[q];
+  }
+  uint32_t x = s;  // inclusive scan over threads = suffix sums over bins
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t z = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULL, z, o);
+      if (lane >= o) z += y;
     }
-    thr[0] = t;
-    thr[1] = 0;  // rows assigned so far
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  uint32_t run = x - s + (w ? wsum[w - 1] : 0);
+  uint32_t over = 0;  // bins c >= 1 whose suffix sum exceeds rows
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    run += v[q];
+    int c = kVBins - 1 - (4 * t + q);
+    over += (c >= 1 && run > rows);
+  }
+  if (over) atomicAdd(&n_over, over);
+  __syncthreads();
+  if (t == 0) {
+    uint32_t th = 1 + n_over;  // suffix sums are non-increasing in c
+    thr[0] = th > kVBins - 1 ? kVBins - 1 : th;
+    thr[1] = 0;
   }
 }
 
@@ -318,284 +346,101 @@ __global__ void k_assign(const uint32_t *__restrict__ scnt, uint32_t n_inst, uin
   }
 }
 
+// code: cold instruction i -> i << 4 (low nibble 0), hot row r -> r << 4 | 1, unmapped -> ~0
 __global__ void k_codemap(const uint32_t *__restrict__ gmap, uint64_t n_gran, const uint32_t *__restrict__ hot_row,
                           uint32_t *__restrict__ code) {
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_gran; g += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t m = gmap[g];
     uint32_t r = m == NONE ? NONE : hot_row[m];
-    code[g] = m == NONE ? NONE : (r != NONE ? (0x80000000u | r) : m);
+    code[g] = m == NONE ? 0xFFFFFFFFu : (r != NONE ? (r << 4 | 1u) : (m << 4));
   }
 }
 
 template <bool REC>
-__device__ __forceinline__ void hot_accumulate(uint32_t *tab, const uint32_t *__restrict__ row_inst, uint32_t c,
-                                               uint4 v, bool live, uint64_t k, unsigned long long *__restrict__ H,
-                                               unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst) {
-  uint32_t cnt = v.z, stall = v.w & 0xFFFFu;
-  uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
-  bool hot = c != NONE && (c & 0x80000000u);
-  if (REC && live) rec_inst[k] = c == NONE ? NONE : (hot ? __ldg(row_inst + (c & 0x7FFFFFFFu)) : c);
-  if (!live || cnt == 0) return;
-  if (c == NONE) {
-    red_add_u64(U + slot, cnt);
-  } else if (hot && slot < (uint32_t)kHotSlots) {
-    uint32_t r = c & 0x7FFFFFFFu;
-    uint32_t old = atomicAdd(tab + r * kHotSlots + slot, cnt);
-    if (old + cnt < old) red_add_u64(H + ((uint64_t)__ldg(row_inst + r) << 4 | slot), 1ull << 32);
-  } else {
-    uint32_t i = hot ? __ldg(row_inst + (c & 0x7FFFFFFFu)) : c;
-    red_add_u64(H + ((uint64_t)i << 4 | slot), cnt);
-  }
-}
-
-template <bool REC>
-__global__ void __launch_bounds__(kHotThreads, 1)
-    k_attr_hot(uint64_t base, uint64_t end, uint32_t gshift, const uint32_t *__restrict__ code,
+__global__ void __launch_bounds__(RingHot::kThreads, 1)
+    k_attr_hot(uint64_t base, uint64_t n_gran, uint32_t gshift, const uint32_t *__restrict__ code,
                const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
                unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
                const uint32_t *__restrict__ row_inst, const uint32_t *__restrict__ thr) {
-  extern __shared__ __align__(16) uint32_t tab[];
-  const uint32_t nhot = min(thr[1], (uint32_t)kHotRows);
-  for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += blockDim.x) tab[x] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t step = nwarps * 32 * kHotR;
-  uint4 nxt[kHotR];
-  uint64_t b = warp * 32 * kHotR;
-#pragma unroll
-  for (int u = 0; u < kHotR; u++) {
-    uint64_t k = b + (uint64_t)u * 32 + lane;
-    nxt[u] = k < n ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
-  }
-  for (; b < n; b += step) {
-    uint4 v[kHotR];
-#pragma unroll
-    for (int u = 0; u < kHotR; u++) v[u] = nxt[u];
-#pragma unroll
-    for (int u = 0; u < kHotR; u++) {          // prefetch the next iteration's records
-      uint64_t k = b + step + (uint64_t)u * 32 + lane;
-      nxt[u] = k < n ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
-    }
-    uint32_t c[kHotR];
-#pragma unroll
-    for (int u = 0; u < kHotR; u++) {
-      uint64_t pc = ((uint64_t)v[u].y << 32) | v[u].x;
-      c[u] = (pc >= base && pc < end) ? __ldg(code + ((pc - base) >> gshift)) : NONE;
-    }
-#pragma unroll
-    for (int u = 0; u < kHotR; u++) {
-      uint64_t k = b + (uint64_t)u * 32 + lane;
-      hot_accumulate<REC>(tab, row_inst, c[u], v[u], k < n, k, H, U, rec_inst);
-    }
-  }
-  __syncthreads();
-  for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += blockDim.x) {
-    uint32_t val = tab[x];
-    if (val) red_add_u64(H + ((uint64_t)__ldg(row_inst + x / kHotSlots) << 4 | (x % kHotSlots)), val);
-  }
-}
-
-// v3b: the same accumulation with a three-deep software pipeline per thread: records of
-// iteration i+2 are loaded from HBM while the granule codes of iteration i+1 are gathered from
-// L2 and iteration i is accumulated, so neither latency is exposed.  Shared atomics are issued
-// before any of their results are examined (wrap checks last).
-template <bool REC, int R>
-__global__ void __launch_bounds__(kHotThreads, 1)
-    k_attr_hot2(uint64_t base, uint64_t end, uint32_t gshift, const uint32_t *__restrict__ code,
-                const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
-                unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
-                const uint32_t *__restrict__ row_inst, const uint32_t *__restrict__ thr) {
-  extern __shared__ __align__(16) uint32_t tab[];
-  const uint32_t nhot = min(thr[1], (uint32_t)kHotRows);
-  for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += blockDim.x) tab[x] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t step = nwarps * 32 * R;
-  auto load = [&](uint64_t b, uint4 *dst) {
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      uint64_t k = b + (uint64_t)u * 32 + lane;
-      dst[u] = k < n ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
-    }
-  };
-  auto gather = [&](const uint4 *v, uint32_t *c) {
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      uint64_t pc = ((uint64_t)v[u].y << 32) | v[u].x;
-      c[u] = (pc >= base && pc < end) ? __ldg(code + ((pc - base) >> gshift)) : NONE;
-    }
-  };
-  uint64_t b = warp * 32 * R;
-  uint4 va[R], vb[R], vc[R];
-  uint32_t ca[R], cb[R];
-  load(b, va);
-  load(b + step, vb);
-  gather(va, ca);
-  for (; b < n; b += step) {
-    load(b + 2 * step, vc);
-    gather(vb, cb);
-    uint32_t old[R];
-    bool hot[R];
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      uint64_t k = b + (uint64_t)u * 32 + lane;
-      bool live = k < n;
-      uint32_t c = ca[u], cnt = va[u].z, stall = va[u].w & 0xFFFFu;
-      uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
-      bool h = c != NONE && (c & 0x80000000u);
-      if (REC && live) rec_inst[k] = c == NONE ? NONE : (h ? __ldg(row_inst + (c & 0x7FFFFFFFu)) : c);
-      hot[u] = live && cnt && h && slot < (uint32_t)kHotSlots;
-      old[u] = hot[u] ? atomicAdd(tab + (c & 0x7FFFFFFFu) * kHotSlots + slot, cnt) : 0u;
-      if (live && cnt && !hot[u]) {
-        uint32_t i = h ? __ldg(row_inst + (c & 0x7FFFFFFFu)) : c;
-        red_add_u64(c == NONE ? U + slot : H + ((uint64_t)i << 4 | slot), cnt);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      if (hot[u] && old[u] + va[u].z < old[u]) {
-        uint32_t stall = va[u].w & 0xFFFFu;
-        red_add_u64(H + ((uint64_t)__ldg(row_inst + (ca[u] & 0x7FFFFFFFu)) << 4 | stall), 1ull << 32);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      va[u] = vb[u];
-      vb[u] = vc[u];
-      ca[u] = cb[u];
-    }
-  }
-  __syncthreads();
-  for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += blockDim.x) {
-    uint32_t val = tab[x];
-    if (val) red_add_u64(H + ((uint64_t)__ldg(row_inst + x / kHotSlots) << 4 | (x % kHotSlots)), val);
-  }
-}
-
-// v3c: records fed by the TMA engine.  Measured (ncu, v3b): gathers issued behind
-// streaming loads complete in issue order from the L1TEX queue, so register prefetching
-// cannot hide the HBM latency from the granule-code gather.  Here a producer warp streams
-// record tiles into a shared-memory ring with cp.async.bulk (UBLKCP, outside the LSU queue);
-// consumer warps read their records from shared memory, release the stage, issue the code
-// gathers of tile i+1 and accumulate tile i meanwhile.  Ring (3 x 24 KiB) and the hot-row
-// table (3200 rows x 48 B) share the 227 KiB of shared memory.
-constexpr int kT3Warps = 24, kT3Rpl = 2, kT3Stages = 3;
-constexpr int kT3Tile = kT3Warps * 32 * kT3Rpl;                 // records per stage
-constexpr int kT3Rows = 3200;
-constexpr size_t kT3Ring = (size_t)kT3Stages * kT3Tile * 16;
-constexpr size_t kT3Smem = kT3Ring + (size_t)kT3Rows * kHotSlots * 4 + 2 * kT3Stages * 8;
-
-template <bool REC>
-__global__ void __launch_bounds__((kT3Warps + 1) * 32, 1)
-    k_attr_hot3(uint64_t base, uint64_t end, uint32_t gshift, const uint32_t *__restrict__ code,
-                const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
-                unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
-                const uint32_t *__restrict__ row_inst, const uint32_t *__restrict__ thr) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int S = kT3Tile, NST = kT3Stages, NC = kT3Warps, R = kT3Rpl;
+  using RG = RingHot;
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = kLook + 1;
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
-  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + kT3Ring);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kT3Ring + (size_t)kT3Rows * kHotSlots * 4);
+  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + kHotTab);
   uint64_t *empty = full + NST;
+  const uint32_t tab_s = smem_u32(tab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t ntiles = (n + S - 1) / S;
-  const uint32_t nhot = min(thr[1], (uint32_t)kT3Rows);
+  const uint32_t nhot = min(thr[1], (uint32_t)kHotRows);
   for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += blockDim.x) tab[x] = 0;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < NST; q++) {
-      mbar_init(full + q, 1);
-      mbar_init(empty + q, NC);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) {
-      uint64_t policy;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      uint32_t it = 0;
-      for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        uint32_t st = it % NST, ph = (it / NST) & 1;
-        if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
-        uint64_t left = n - tile * S;
-        uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);
-        mbar_arrive_expect_tx(full + st, bytes);
-        bulk_g2s(ring + (size_t)st * S, rec + tile * S, bytes, full + st, policy);
-      }
-    }
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n);
     return;
   }
-  // consumers: tile i+1's records and code gathers overlap tile i's accumulation
-  uint4 va[R], vb[R];
-  uint32_t ca[R], cb[R];
-  uint64_t ka = 0;
-  uint32_t ma = 0;
-  auto fetch = [&](uint32_t it, uint64_t tile, uint4 *v, uint32_t *c, uint32_t &m) {
-    uint32_t st = it % NST, ph = (it / NST) & 1;
+  uint4 v[D][R];
+  uint32_t c[D][R];
+  const uint64_t G = gridDim.x;
+  auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *cc) {
+    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
-    uint64_t left = n - tile * S;
-    m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
+    const uint4 *src = ring + (size_t)st * S + warp * 32 + lane;
 #pragma unroll
-    for (int u = 0; u < R; u++) {
-      uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
-      v[u] = j < m ? ring[(size_t)st * S + j] : make_uint4(0, 0, 0, 0);
-    }
+    for (int u = 0; u < R; u++) vv[u] = src[u * NC * 32];  // beyond the tile end: masked below
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
 #pragma unroll
     for (int u = 0; u < R; u++) {
-      uint64_t pc = ((uint64_t)v[u].y << 32) | v[u].x;
-      c[u] = (pc >= base && pc < end) ? __ldg(code + ((pc - base) >> gshift)) : NONE;
+      uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - base) >> gshift;
+      cc[u] = g < n_gran ? __ldg(code + g) : 0xFFFFFFFFu;
     }
   };
-  uint32_t it = 0;
-  uint64_t tile = blockIdx.x;
-  if (tile < ntiles) {
-    fetch(it, tile, va, ca, ma);
-    ka = tile * S;
-  }
-  while (tile < ntiles) {
-    uint64_t nt = tile + gridDim.x;
-    uint32_t mb = 0;
-    if (nt < ntiles) fetch(it + 1, nt, vb, cb, mb);
-    uint32_t old[R];
-    bool hot[R];
 #pragma unroll
-    for (int u = 0; u < R; u++) {
-      uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
-      bool live = j < ma;
-      uint32_t c = ca[u], cnt = va[u].z, stall = va[u].w & 0xFFFFu;
-      uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
-      bool h = c != NONE && (c & 0x80000000u);
-      if (REC && live) rec_inst[ka + j] = c == NONE ? NONE : (h ? __ldg(row_inst + (c & 0x7FFFFFFFu)) : c);
-      hot[u] = live && cnt && h && slot < (uint32_t)kHotSlots;
-      old[u] = hot[u] ? atomicAdd(tab + (c & 0x7FFFFFFFu) * kHotSlots + slot, cnt) : 0u;
-      if (live && cnt && !hot[u]) {
-        uint32_t i = h ? __ldg(row_inst + (c & 0x7FFFFFFFu)) : c;
-        red_add_u64(c == NONE ? U + slot : H + ((uint64_t)i << 4 | slot), cnt);
+  for (int q = 0; q < kLook; q++)
+    if (blockIdx.x + q * G < ntiles) fetch(q, v[q], c[q]);
+  for (uint32_t it0 = 0;; it0 += D) {
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      const uint32_t it = it0 + q;
+      const uint64_t tile = blockIdx.x + it * G;
+      if (tile >= ntiles) goto done;
+      if (tile + kLook * G < ntiles) fetch(it + kLook, v[(q + kLook) % D], c[(q + kLook) % D]);
+      const uint64_t left = n - tile * S;
+      const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
+      uint32_t old[R];
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+        const uint32_t cd = c[q][u], cnt = v[q][u].z, stall = v[q][u].w & 0xFFFFu;
+        const uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
+        const uint32_t nib = cd & 15u;
+        const bool live = j < m;
+        if (REC && live)
+          rec_inst[tile * S + j] = nib == 15u ? NONE : (nib == 1u ? __ldg(row_inst + (cd >> 4)) : (cd >> 4));
+        old[u] = 0xFFFFFFFFu;  // "no shared add"
+        if (live) {
+          if (nib == 1u && slot < (uint32_t)kHotSlots) {
+            old[u] = atoms_add(tab_s + ((cd >> 4) * kHotSlots + slot) * 4, cnt);
+          } else if (nib == 0u) {
+            red_add_u64(H + (cd | slot), cnt);
+          } else if (nib == 15u) {
+            red_add_u64(U + slot, cnt);
+          } else {  // hot instruction, invalid stall slot
+            red_add_u64(H + ((uint64_t)__ldg(row_inst + (cd >> 4)) << 4 | slot), cnt);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        // old + cnt wrapped the u32 shared counter: repay 2^32 in L2
+        if (old[u] != 0xFFFFFFFFu && old[u] + v[q][u].z < old[u])
+          red_add_u64(H + ((uint64_t)__ldg(row_inst + (c[q][u] >> 4)) << 4 | (v[q][u].w & 0xFFFFu)), 1ull << 32);
       }
     }
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      if (hot[u] && old[u] + va[u].z < old[u]) {
-        uint32_t stall = va[u].w & 0xFFFFu;
-        red_add_u64(H + ((uint64_t)__ldg(row_inst + (ca[u] & 0x7FFFFFFFu)) << 4 | stall), 1ull << 32);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < R; u++) {
-      va[u] = vb[u];
-      ca[u] = cb[u];
-    }
-    ma = mb;
-    ka = nt * S;
-    tile = nt;
-    ++it;
   }
+done:
   asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
   for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += NC * 32) {
     uint32_t val = tab[x];
@@ -603,9 +448,19 @@ __global__ void __launch_bounds__((kT3Warps + 1) * 32, 1)
   }
 }
 
+int g_attr_kernel = -1;  // gpa_set_attr_kernel; -1 = read GPA_ATTR_VARIANT once (0 if unset)
+
+int attr_variant() {  // 0 auto, 1 stream, 2 tma, 3 hot (when applicable)
+  if (g_attr_kernel < 0) {
+    const char *e = getenv("GPA_ATTR_VARIANT");
+    g_attr_kernel = e ? atoi(e) : 0;
+  }
+  return g_attr_kernel;
+}
+
 cudaError_t launch_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
                        unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
-  // scratch (stream-ordered): scnt[n_inst] | hot_row[n_inst] | row_inst[K] | V[4096] | thr[2] | code[n_gran]
+  // stream-ordered scratch: scnt[n_inst] | hot_row[n_inst] | row_inst[K] | V[4096] | thr[4] | code[n_gran]
   size_t ni = T.n_inst;
   size_t words = 2 * ni + kHotRows + kVBins + 4 + T.n_gran;
   uint32_t *w = nullptr;
@@ -616,72 +471,67 @@ cudaError_t launch_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsign
   cudaMemsetAsync(scnt, 0, ni * 4, st);
   cudaMemsetAsync(V, 0, kVBins * 4, st);
   k_sample<<<sm_count * 4, 256, 0, st>>>(T, rec, n, scnt);
-  k_vhist<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, V);
-  uint32_t rows = attr_variant() == 6 ? kT3Rows : kHotRows;
-  k_pick<<<1, 32, 0, st>>>(V, thr, rows);
-  k_assign<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_row, row_inst, rows);
+  k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)ni, V);
+  k_pick<<<1, 1024, 0, st>>>(V, thr, kHotRows);
+  k_assign<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_row, row_inst, kHotRows);
   k_codemap<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_row, code);
-  if (attr_variant() == 6) {
-    auto kern = ri ? k_attr_hot3<true> : k_attr_hot3<false>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT3Smem);
-    if (e == cudaSuccess) {
-      kern<<<sm_count, (kT3Warps + 1) * 32, kT3Smem, st>>>(T.base, T.end, T.gshift, code, rec, n, H, U, ri, row_inst,
-                                                            thr);
-      e = cudaGetLastError();
-    }
-  } else {
-    auto kern = attr_variant() == 5 ? (ri ? k_attr_hot2<true, 4> : k_attr_hot2<false, 4>)
-                                    : (ri ? k_attr_hot<true> : k_attr_hot<false>);
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHotSmem);
-    if (e == cudaSuccess) {
-      kern<<<sm_count, kHotThreads, kHotSmem, st>>>(T.base, T.end, T.gshift, code, rec, n, H, U, ri, row_inst, thr);
-      e = cudaGetLastError();
-    }
+  auto kern = ri ? k_attr_hot<true> : k_attr_hot<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHotSmem);
+  if (e == cudaSuccess) {
+    kern<<<sm_count, RingHot::kThreads, kHotSmem, st>>>(T.base, T.n_gran, T.gshift, code, rec, n, H, U, ri, row_inst,
+                                                       thr);
+    e = cudaGetLastError();
   }
   count_launches(6);
   cudaError_t e2 = cudaFreeAsync(w, st);
   return e != cudaSuccess ? e : e2;
 }
 
+template <int MODE>
+cudaError_t launch_tma(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
+                       unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  auto kern = ri ? k_attr_tma<MODE, true> : k_attr_tma<MODE, false>;
+  size_t smem = RingTma::kBytes + 2 * RingTma::kStages * 8;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  uint64_t ntiles = (n + RingTma::kTile - 1) / RingTma::kTile;
+  unsigned blocks = (unsigned)(ntiles < (uint64_t)sm_count ? ntiles : (uint64_t)sm_count);
+  kern<<<blocks, RingTma::kThreads, smem, st>>>(T, rec, n, H, U, ri);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_stream(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
+                          unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  uint64_t per_block = (uint64_t)kStreamThreads * kStreamUnroll;
+  uint64_t want = (n + per_block - 1) / per_block;
+  uint64_t cap = (uint64_t)sm_count * (2048 / kStreamThreads);  // one full wave of resident blocks
+  unsigned blocks = (unsigned)(want < cap ? want : cap);
+  if (ri) k_attr_stream<MODE, true><<<blocks, kStreamThreads, 0, st>>>(T, rec, n, H, U, ri);
+  else k_attr_stream<MODE, false><<<blocks, kStreamThreads, 0, st>>>(T, rec, n, H, U, nullptr);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 }  // namespace
+
+void set_attr_kernel(int which) { g_attr_kernel = which; }
 
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr, uint32_t *d_rec_inst,
                              int sm_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
-  int var = attr_variant();  // 1: register-streaming kernel; 2: TMA ring + warp aggregation;
-                             // 3: TMA ring, one reduction per record; 4: shared-memory
-                             // heavy-hitter rows (v3) for large calls
-  if (var >= 4 && T.mode == 0 && n >= (uint64_t)kSampleChunks * kSampleChunk && T.n_inst >= 1024)
-    return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
-  if (var >= 4) var = 2;
-  count_launches(1);
-  if (var >= 2 && n >= 4096) {
-    bool agg = var == 2;
-#define GPA_TMA(M, RI, A) return launch_tma<CfgA, M, RI, A>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
-    if (T.mode == 0) {
-      if (d_rec_inst) { if (agg) GPA_TMA(0, true, true); else GPA_TMA(0, true, false); }
-      else { if (agg) GPA_TMA(0, false, true); else GPA_TMA(0, false, false); }
-    } else {
-      if (d_rec_inst) { if (agg) GPA_TMA(1, true, true); else GPA_TMA(1, true, false); }
-      else { if (agg) GPA_TMA(1, false, true); else GPA_TMA(1, false, false); }
-    }
-#undef GPA_TMA
+  const int var = attr_variant();
+  const bool hot_ok = T.mode == 0 && n >= kHotMinRecords && T.n_inst >= 1024;
+  if ((var == 0 || var == 3) && hot_ok) return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+  if (var == 1 || n < 4096) {
+    return T.mode == 0 ? launch_stream<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
+                       : launch_stream<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
   }
-  uint64_t per_block = (uint64_t)kThreads * kUnroll;
-  uint64_t want = (n + per_block - 1) / per_block;
-  uint64_t cap = (uint64_t)sm_count * (2048 / kThreads);  // one full wave of resident blocks
-  unsigned blocks = (unsigned)(want < cap ? want : cap);
-  if (T.mode == 0) {
-    if (d_rec_inst) k_attribute<0, true><<<blocks, kThreads, 0, st>>>(T, rec, n, d_hist, d_unattr, d_rec_inst);
-    else k_attribute<0, false><<<blocks, kThreads, 0, st>>>(T, rec, n, d_hist, d_unattr, nullptr);
-  } else {
-    if (d_rec_inst) k_attribute<1, true><<<blocks, kThreads, 0, st>>>(T, rec, n, d_hist, d_unattr, d_rec_inst);
-    else k_attribute<1, false><<<blocks, kThreads, 0, st>>>(T, rec, n, d_hist, d_unattr, nullptr);
-  }
-  return cudaGetLastError();
+  return T.mode == 0 ? launch_tma<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
+                     : launch_tma<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
 }
 
 }  // namespace gpa

@@ -76,6 +76,8 @@ def _load():
         "gpa_get_cct_view": ([_vp, ctypes.POINTER(CctView)], S),
         "gpa_free_cct": ([_vp], None),
         "gpa_derive_metrics": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], S),
+        "gpa_kernel_launches": ([], ctypes.c_uint64),
+        "gpa_set_attr_kernel": ([ctypes.c_int], S),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -86,6 +88,16 @@ def _load():
 
 _lib = _load()
 EXPORTED = tuple(n for n in dir(_lib) if n.startswith("gpa_"))
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library in this process so far."""
+    return int(_lib.gpa_kernel_launches())
+
+
+def set_attr_kernel(which: int) -> None:
+    """0 automatic, 1 register streaming, 2 TMA + L2 reductions, 3 TMA + shared-memory rows."""
+    _check(_lib.gpa_set_attr_kernel(int(which)), "gpa_set_attr_kernel")
 
 
 def version() -> str:

@@ -290,3 +290,37 @@ def test_cct_capacity(gpa):
     with pytest.raises(gpa.GpaError) as ei:
         gpa.reconstruct_cct(s, Ht, mode=gpa.WEIGHTS_EXACT)
     assert ei.value.status == 7
+
+
+# ---- every attribution kernel, and the u32 wrap repayment of the shared-memory rows -------------
+@pytest.fixture
+def attr_kernel(gpa):
+    yield gpa.set_attr_kernel
+    gpa.set_attr_kernel(0)
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("name,records", [("C3", 4_000_003), ("C5", 3_000_001)])
+def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
+    attr_kernel(kernel)
+    w = gen.workload(name, records=records)
+    s = gpa.load_structure(w.structure, 0)
+    H, U, ri = _attribute(gpa, s, _device_records(w))
+    Ho, Uo, rio = oracle.attribute(w.structure, w.records_host(), rec_inst=True)
+    assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
+    assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3])
+def test_attribution_huge_counts_exact(gpa, attr_kernel, kernel):
+    """Counts near 2^32 make every shared u32 add wrap: the repaid 2^32 keeps H exact."""
+    attr_kernel(kernel)
+    w = gen.workload("C3", records=2_200_000)
+    rec = w.records_host()
+    rng = np.random.default_rng(5)
+    rec["count"] = np.where(rng.random(len(rec)) < 0.5, 0xFFFFFFF0, rng.integers(1, 1 << 31, len(rec)))
+    s = gpa.load_structure(w.structure, 0)
+    H, U, _ = _attribute(gpa, s, torch.from_numpy(rec.view(np.int64).reshape(-1, 2)).to(DEV), rec_inst=False)
+    Ho, Uo, _ = oracle.attribute(w.structure, rec)
+    assert Ho.max() > 2 ** 40
+    assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
