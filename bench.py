@@ -94,16 +94,26 @@ def _dist_env():
 # ---------------------------------------------------------------------------------------
 # CPU oracle legs (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------------------
-def oracle_pass(w, n_sample: int, k0: int, threads: int):
+def oracle_pass(w, n_sample: int, k0: int, threads: int, chunk: int = 1 << 27):
     """Time the oracle on records [k0, k0+n_sample): D1 attribution on `threads` cores
-    (thread-private histograms, serial merge) + D2 roll-up + D3-D6 CCT + D7 metrics
-    (single-threaded, the oracle as it stands).  Host generation is untimed."""
+    (thread-private histograms, serial merge), chunk by chunk (host generation of each chunk
+    is untimed), then D2 roll-up + D3-D6 CCT + D7 metrics once on the summed histogram
+    (single-threaded: the oracle as it stands)."""
     import numpy as np
     import oracle
-    rec = w.records_host(k0, n_sample)
     st = w.structure
-    t0 = time.perf_counter()
-    H, U, _ = oracle.attribute(st, rec, threads=threads)
+    H = np.zeros((w.meta["n_inst"], 16), np.uint64)
+    U = np.zeros(16, np.uint64)
+    buf = np.empty(min(chunk, n_sample), w.records_host(0, 1).dtype)
+    ta = 0.0
+    for c0 in range(0, n_sample, chunk):
+        m = min(chunk, n_sample - c0)
+        rec = w.records_host(k0 + c0, m, threads=threads, out=buf[:m])
+        t0 = time.perf_counter()
+        h, u, _ = oracle.attribute(st, rec, threads=threads)
+        H += h
+        U += u
+        ta += time.perf_counter() - t0
     t1 = time.perf_counter()
     for sc in SCOPES:
         h, m = oracle.scope_hist(st, H, sc)
@@ -111,18 +121,18 @@ def oracle_pass(w, n_sample: int, k0: int, threads: int):
     R = oracle.cct(st, H)
     oracle.derive_f64(R["excl"])
     oracle.derive_f64(R["incl"])
-    t2 = time.perf_counter()
-    del rec
-    return t2 - t0, t1 - t0, t2 - t1, int(np.asarray(H).sum() + np.asarray(U).sum())
+    tr = time.perf_counter() - t1
+    return ta + tr, ta, tr, int(H.sum() + U.sum())
 
 
 def cpu_baseline(w, target_s: float = 12.0):
+    """The oracle on the GPU box's host cores over a bounded prefix of the same workload,
+    sized (after a calibration pass) for about target_s seconds of timed CPU work."""
     cores = len(os.sched_getaffinity(0))
-    # calibrate attribution speed on 2^21 records, then size the sample for ~target_s
-    t, ta, tr, _ = oracle_pass(w, 1 << 21, 0, cores)
-    per_rec = ta / (1 << 21)
-    n = int(min(w.cfg.records, max(1 << 21, (target_s - tr) / max(per_rec, 1e-12))))
-    n = min(n, 1 << 28)
+    n = 1 << 24
+    t, ta, tr, _ = oracle_pass(w, n, 0, cores)
+    per_rec = ta / n
+    n = int(min(w.cfg.records, max(n, (target_s - tr) / max(per_rec, 1e-12))))
     t, ta, tr, _ = oracle_pass(w, n, 0, cores)
     return {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {n} records of {w.cfg.name} ({w.cfg.records} total); whole path: D1 attribution "
@@ -318,7 +328,7 @@ def run_gpa(args):
                        "parallelism": f"record shards x{world}, NCCL reduce of H||U",
                        "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_attribute",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_attr_hot",
                          "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
             "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:
@@ -340,7 +350,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-sample", type=int, default=1 << 26)
+    ap.add_argument("--ref-sample", type=int, default=1 << 28)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "gpa":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

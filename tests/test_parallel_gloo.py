@@ -1,0 +1,64 @@
+"""The N > 1 path on CPU: world_size-2 gloo process groups shard the record stream with
+parallel.shard_range and combine per-rank histograms with parallel.reduce_histogram (the
+same call bench.py makes over NCCL).  Per-rank partials come from the oracle here (no
+GPU); the reduced H||U must equal the single-process oracle bit for bit (integer sums are
+associative, "aggregated by a second reduction")."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import gen
+import oracle
+from paper_2109_06931_b200.parallel import reduce_histogram, shard_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, records, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = gen.workload(name, records=records)
+        a, b = shard_range(w.cfg.records, rank, world)
+        rec = w.records_host(a, b - a)
+        H, U, _ = oracle.attribute(w.structure, rec)
+        HU = torch.from_numpy(np.concatenate([H.reshape(-1), U]).view(np.int64).copy())
+        reduce_histogram(HU, dst=0)
+        if rank == 0:
+            np.save(out_path, HU.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,records,world", [("C2", 100_003, 2), ("C4", 60_001, 2), ("C1", 1, 2), ("C1", 0, 2)])
+def test_sharded_reduce_equals_single_process(tmp_path, name, records, world):
+    out = str(tmp_path / "hu.npy")
+    mp.start_processes(_worker, args=(world, _free_port(), name, records, out), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(out).view(np.uint64)
+    w = gen.workload(name, records=records)
+    H, U, _ = oracle.attribute(w.structure, w.records_host(0, w.cfg.records))
+    assert np.array_equal(got, np.concatenate([H.reshape(-1), U]))
+
+
+def test_shard_range_partitions():
+    for n in [0, 1, 7, 1000, 4_000_000_000]:
+        for world in [1, 2, 3, 8]:
+            parts = [shard_range(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
