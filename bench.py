@@ -158,7 +158,7 @@ def run_reference(args):
     val = n / t
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
             "config": {"workload": w.cfg.name, "records": w.cfg.records, "sample_per_step": n,
                        "n_inst": w.meta["n_inst"], "n_func": w.meta["n_func"]},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",

@@ -231,11 +231,15 @@ GPA_API gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample 
  * the DAG into a tree, apportioning by f(child) = f(parent) * w_e / W_callee (P:880-881,
  * R13-R16).  max_contexts == 0: count only (*out untouched, *n_contexts = required).
  * More contexts than max_contexts -> GPA_ERR_CAPACITY with *n_contexts = required.
- * Synchronizes `stream` (the context count decides the allocation). */
+ * d_inst_hist must be 16-byte aligned.  Synchronizes `stream` (the context count decides
+ * the allocation). */
 GPA_API gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist,
                                gpa_weight_mode mode, uint64_t max_contexts,
                                gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream);
 GPA_API gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *out);
+/* Releases the tree's device memory in stream order on the stream gpa_reconstruct_cct was
+ * called with (no device synchronization); work on other streams that still reads the views
+ * must be ordered before that stream by the caller. */
 GPA_API void gpa_free_cct(gpa_cct c);
 
 /* ---- a-5 + a-10: roll-up and derived metrics -------------------------------------------
@@ -247,7 +251,8 @@ GPA_API void gpa_free_cct(gpa_cct c);
  *   0 S  1 W=v0/S  2 (v0+v9)/S  3 sum_{LAT} v/S  4..15 v[r]/S  16 v[15]
  *   17..32 mix[k]/S (NaN for CCT rows).
  * Any of d_scope_hist, d_scope_mix, d_metrics may be NULL.  For INST rows d_scope_hist
- * receives a copy of d_inst_hist.  Enqueue-only on `stream`. */
+ * receives a copy of d_inst_hist.  d_inst_hist / d_scope_hist / d_scope_mix must be 16-byte
+ * aligned, d_metrics 8-byte aligned (GPA_ERR_INVALID_ARG otherwise).  Enqueue-only. */
 GPA_API gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist,
                               gpa_cct cct, uint64_t *d_scope_hist, uint64_t *d_scope_mix,
                               double *d_metrics, gpa_stream_t stream);

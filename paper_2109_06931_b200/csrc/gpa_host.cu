@@ -314,6 +314,26 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
   for (int k = 0; k < ROLL_KINDS; k++) {
     UP(R[k].d_ptr, ptr[k]);
     UP(R[k].d_inst, lst[k]);
+    // chunks of <= kRollChunk instructions; rows with several chunks get a scratch slot
+    std::vector<uint32_t> chunk, mslot(R[k].rows, NONE), mrows;
+    for (uint32_t r = 0; r < R[k].rows; r++) {
+      uint32_t b = ptr[k][r], e = ptr[k][r + 1];
+      if (e - b > kRollChunk) {
+        mslot[r] = (uint32_t)mrows.size();
+        mrows.push_back(r);
+      }
+      if (b == e) { chunk.push_back(r); chunk.push_back(b); chunk.push_back(e); }
+      for (uint32_t x = b; x < e; x += kRollChunk) {
+        chunk.push_back(r);
+        chunk.push_back(x);
+        chunk.push_back(std::min(e, x + kRollChunk));
+      }
+    }
+    R[k].n_chunks = (uint32_t)(chunk.size() / 3);
+    R[k].n_multi = (uint32_t)mrows.size();
+    UP(R[k].d_chunk, chunk);
+    UP(R[k].d_multi_slot, mslot);
+    UP(R[k].d_multi_rows, mrows);
   }
 
   // ---- Step 1 structure: call graph from call instructions ---------------------
@@ -453,17 +473,23 @@ int sm_count(int dev) {
   } while (0)
 
 // ---- a-6..a-9 ---------------------------------------------------------------------------
+// CCT memory is stream-ordered (the device's default memory pool, on the stream the tree was
+// built on): allocation is a pool hit and freeing does not synchronize the device.
 static void free_cct(gpa_cct_s *c) {
   if (!c) return;
   DeviceGuard g(c->device);
-  for (void *p : c->allocs) cudaFree(p);
+  for (void *p : c->allocs)
+    if (cudaFreeAsync(p, c->stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(p);
+    }
   delete c;
 }
 
 template <class T>
 static cudaError_t calloc_dev(gpa_cct_s *c, T **p, size_t n) {
   *p = nullptr;
-  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (n ? n : 1));
+  cudaError_t e = cudaMallocAsync((void **)p, sizeof(T) * (n ? n : 1), c->stream);
   if (e == cudaSuccess) c->allocs.push_back(*p);
   return e;
 }
@@ -628,6 +654,7 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   if (!s || !n_contexts || (max_contexts && !out)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
   if (mode != GPA_WEIGHTS_SAMPLES) return fail(GPA_ERR_UNSUPPORTED, "only GPA_WEIGHTS_SAMPLES is built");
   if (!d_inst_hist && s->info.n_inst) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  if ((uintptr_t)d_inst_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist must be 16-byte aligned");
   if (out) *out = nullptr;
   DeviceGuard g(s->device);
   CU(g.err);
@@ -635,6 +662,7 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   const gpa_structure_info &I = s->info;
   gpa_cct_s *c = new gpa_cct_s();
   c->device = s->device;
+  c->stream = st;
   c->n_call = I.n_call; c->n_func = I.n_func; c->n_dag = I.n_dag;
   unsigned long long *d_cnt = nullptr;  // [0] total contexts, [1] next-level size
   gpa_status ret = GPA_OK;
@@ -657,8 +685,8 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   CC(calloc_dev(c, &d_cnt, 4));
   // Step 1: edge weights and per-function samples S_f (the FUNC roll-up)
   CC(launch_cct_weights(s, d_inst_hist, c->w, st));
-  CC(launch_rollup(s->roll[ROLL_FUNC].d_ptr, s->roll[ROLL_FUNC].d_inst, s->roll[ROLL_FUNC].rows, false,
-                   d_inst_hist, s->d_inst_class, c->S_f, nullptr, nullptr, sm_count(s->device), st));
+  CC(launch_rollup(&s->roll[ROLL_FUNC], s->roll[ROLL_FUNC].rows, d_inst_hist, s->d_inst_class, c->S_f, nullptr,
+                   nullptr, sm_count(s->device), st));
   // Step 2 + guard (R12) + W + context count (path DP over the DAG)
   CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, st));
   unsigned long long h_cnt[2] = {0, 0};
@@ -685,6 +713,11 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   CC(calloc_dev(c, &c->frac, n));
   CC(calloc_dev(c, &c->excl, n * SLOTS));
   CC(calloc_dev(c, &c->incl, n * SLOTS));
+  if (cct_small_ok(s, n)) {  // one CTA builds the whole tree: no per-level launches or syncs
+    CC(launch_cct_small(s, c, d_cnt + 1, st));
+    *out = c;
+    return GPA_OK;
+  }
   uint32_t *d_tmp = nullptr, *d_bs = nullptr;
   CC(calloc_dev(c, &d_tmp, n + 1));
   CC(calloc_dev(c, &d_bs, 65536));
@@ -752,8 +785,11 @@ gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *
   uint32_t rows = k < 0 ? s->info.n_inst : s->roll[k].rows;
   if (rows == 0 || (!d_scope_hist && !d_scope_mix && !d_metrics)) return GPA_OK;
   if (!d_inst_hist) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
-  CU(launch_rollup(k < 0 ? nullptr : s->roll[k].d_ptr, k < 0 ? nullptr : s->roll[k].d_inst, rows, k < 0,
-                   d_inst_hist, s->d_inst_class, d_scope_hist, d_scope_mix, d_metrics, sm_count(s->device), st));
+  if (((uintptr_t)d_inst_hist | (uintptr_t)d_scope_hist | (uintptr_t)d_scope_mix) & 15)
+    return fail(GPA_ERR_INVALID_ARG, "histogram buffers must be 16-byte aligned");
+  if ((uintptr_t)d_metrics & 7) return fail(GPA_ERR_INVALID_ARG, "d_metrics must be 8-byte aligned");
+  CU(launch_rollup(k < 0 ? nullptr : &s->roll[k], rows, d_inst_hist, s->d_inst_class, d_scope_hist, d_scope_mix,
+                   d_metrics, sm_count(s->device), st));
   return GPA_OK;
 }
 

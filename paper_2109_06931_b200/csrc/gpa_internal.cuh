@@ -31,11 +31,18 @@ struct AttrTables {
   uint32_t n_inst;
 };
 
+constexpr uint32_t kRollChunk = 32;  // instructions per roll-up work item
+
 struct RollSet {
   uint32_t rows = 0;
   uint32_t *d_ptr = nullptr;    // [rows+1]
   uint32_t *d_inst = nullptr;   // [ptr[rows]]
   std::vector<uint32_t> ids;    // host: scope id (or function id) behind each row
+  // work decomposition (load time): rows split into chunks of <= kRollChunk instructions
+  uint32_t n_chunks = 0, n_multi = 0;
+  uint32_t *d_chunk = nullptr;      // [3*n_chunks] (row, begin, end) into d_inst
+  uint32_t *d_multi_slot = nullptr; // [rows] scratch slot of a row with > 1 chunk, else NONE
+  uint32_t *d_multi_rows = nullptr; // [n_multi] the rows with > 1 chunk
 };
 
 }  // namespace gpa
@@ -67,6 +74,7 @@ struct gpa_structure_s {
 
 struct gpa_cct_s {
   int device = 0;
+  cudaStream_t stream = nullptr;  // the build stream: allocations and frees are ordered on it
   uint64_t n = 0;
   uint32_t n_call = 0, n_func = 0, n_dag = 0;
   uint32_t *parent = nullptr, *site = nullptr, *node = nullptr, *first_child = nullptr,
@@ -90,10 +98,11 @@ namespace gpa {
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr,
                              uint32_t *d_rec_inst, int sm_count, cudaStream_t st);
-// Row-wise roll-up with the fused derived-metric epilogue.  identity: row r = instruction r.
-cudaError_t launch_rollup(const uint32_t *d_ptr, const uint32_t *d_inst, uint32_t rows, bool identity,
-                          const uint64_t *d_hist, const uint8_t *d_class, uint64_t *d_out_hist,
-                          uint64_t *d_out_mix, double *d_metrics, int sm_count, cudaStream_t st);
+// Row-wise roll-up with the fused derived-metric epilogue.  set == nullptr: identity rows
+// (row r = instruction r, `rows` rows).
+cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_hist, const uint8_t *d_class,
+                          uint64_t *d_out_hist, uint64_t *d_out_mix, double *d_metrics, int sm_count,
+                          cudaStream_t st);
 cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st);
 
 // CCT pieces (k_cct.cu)
@@ -108,5 +117,8 @@ cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a,
                              uint32_t *d_tmp, uint32_t *d_blocksum, unsigned long long *d_next,
                              cudaStream_t st);
 cudaError_t launch_cct_excl(const gpa_structure_s *s, gpa_cct_s *c, cudaStream_t st);
+// whole Step 4 in one CTA when cct_small_ok (writes the built context count to *d_built)
+bool cct_small_ok(const gpa_structure_s *s, uint64_t n);
+cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, unsigned long long *d_built, cudaStream_t st);
 cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStream_t st);
 }  // namespace gpa

@@ -335,6 +335,111 @@ __global__ void k_incl_level(uint64_t a, uint64_t b, const uint32_t *first_child
   }
 }
 
+// Whole Step 4 in one CTA for small trees (the common case: C1, C2, C4, C5 have <= 2^15
+// contexts): roots, every BFS level (count -> block scan -> write), excl, and the reverse
+// incl fold, separated by __syncthreads instead of kernel launches and host syncs.
+constexpr int kSmallLevels = 1024;
+constexpr uint64_t kSmallMax = 1ull << 16;
+
+__device__ __forceinline__ void write_children(const LevelArgs &A, uint64_t c, uint64_t o) {
+  uint8_t k = A.kind[c];
+  uint32_t nd = A.node[c];
+  double f = A.frac[c];
+  uint32_t cnt = 0;
+  if (k == GPA_CTX_SCC) {
+    for (uint32_t q = A.dmem_ptr[nd]; q < A.dmem_ptr[nd + 1]; q++, cnt++) {
+      uint64_t d = o + cnt;
+      A.parent[d] = (uint32_t)c;
+      A.site[d] = NONE;
+      A.node[d] = A.dmem[q];
+      A.kind[d] = GPA_CTX_SCC_MEMBER;
+      A.frac[d] = f;
+    }
+  } else {
+    uint32_t g = func_of_ctx(A, k, nd);
+    for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) {
+      uint32_t e = A.fout_e[q];
+      uint64_t we = A.w[e];
+      if (!we) continue;
+      uint32_t Y = A.scc_of[A.callee[e]];
+      uint64_t d = o + cnt++;
+      A.parent[d] = (uint32_t)c;
+      A.site[d] = e;
+      A.node[d] = Y;
+      A.kind[d] = A.nontriv[Y] ? GPA_CTX_SCC : GPA_CTX_FUNC;
+      A.frac[d] = __dmul_rn(f, __ddiv_rn(__ull2double_rn(we), __ull2double_rn(A.W[Y])));  // R13
+    }
+  }
+  A.first_child[c] = (uint32_t)o;
+  A.n_children[c] = cnt;
+}
+
+__global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag, const uint32_t *din_ptr,
+                                                    const uint8_t *dact, const uint64_t *S_f, uint64_t n_total,
+                                                    double *excl, double *incl, unsigned long long *built) {
+  __shared__ uint32_t lev[kSmallLevels + 1];
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < n_dag; base += nt) {  // roots in DAG order (R15)
+    uint32_t X = base + t;
+    uint32_t flag = X < n_dag && din_ptr[X] == din_ptr[X + 1] && dact[X];
+    uint32_t tot;
+    uint32_t pos = running + block_exscan(flag, &tot);
+    if (flag) {
+      A.parent[pos] = NONE;
+      A.site[pos] = NONE;
+      A.node[pos] = X;
+      A.kind[pos] = A.nontriv[X] ? GPA_CTX_SCC : GPA_CTX_FUNC;
+      A.frac[pos] = 1.0;
+    }
+    running += tot;
+  }
+  __syncthreads();
+  uint32_t a = 0, b = running, L = 0;
+  if (t == 0) lev[0] = 0;
+  while (b > a && L < kSmallLevels) {
+    if (t == 0) lev[L + 1] = b;
+    L++;
+    uint32_t next = b;
+    for (uint32_t base = a; base < b; base += nt) {
+      uint32_t c = base + t;
+      uint32_t cnt = c < b ? child_count(A, c) : 0;
+      uint32_t tot;
+      uint32_t off = block_exscan(cnt, &tot);
+      if (c < b) write_children(A, c, next + off);
+      next += tot;
+    }
+    __syncthreads();
+    a = b;
+    b = next;
+  }
+  __syncthreads();
+  for (uint64_t x = t; x < n_total * GPA_SLOTS; x += nt) {  // excl (R14)
+    uint64_t c = x >> 4;
+    int r = (int)(x & 15);
+    uint8_t k = A.kind[c];
+    double v = 0.0;
+    if (k != GPA_CTX_SCC) {
+      uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
+      v = __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
+    }
+    excl[x] = v;
+  }
+  __syncthreads();
+  for (int l = (int)L - 1; l >= 0; l--) {  // incl: deepest level first, children in order
+    for (uint64_t x = (uint64_t)lev[l] * GPA_SLOTS + t; x < (uint64_t)lev[l + 1] * GPA_SLOTS; x += nt) {
+      uint64_t c = x >> 4;
+      int r = (int)(x & 15);
+      double v = excl[x];
+      uint32_t d0 = A.first_child[c], nc = A.n_children[c];
+      for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, incl[(uint64_t)d * GPA_SLOTS + r]);
+      incl[x] = v;
+    }
+    __syncthreads();
+  }
+  if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
+}
+
 unsigned grid_for(uint64_t work, unsigned threads) {
   uint64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -403,6 +508,18 @@ cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a,
   k_level_write<<<grid_for(m, 256), 256, 0, st>>>(A, a, b, d_tmp);
   count_launches(5);
   return cudaGetLastError();
+}
+
+cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, unsigned long long *d_built, cudaStream_t st) {
+  LevelArgs A = level_args(s, c);
+  k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, c->S_f, c->n, c->excl, c->incl,
+                                  d_built);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+bool cct_small_ok(const gpa_structure_s *s, uint64_t n) {
+  return n <= kSmallMax && 2ull * s->info.dag_levels + 2 < (uint64_t)kSmallLevels;
 }
 
 cudaError_t launch_cct_excl(const gpa_structure_s *s, gpa_cct_s *c, cudaStream_t st) {

@@ -2,12 +2,10 @@
 // per function P:936-937) with the fused a-10 derived-metric epilogue (§6.1 P:944-948:
 // W = (S - S_stall)/S; stall percentages P:918; readings R3-R5, R18).
 //
-// One warp per row.  The row's instruction list (load-time CSR: every instruction whose
-// scope chain contains the row's scope) is walked two instructions at a time: each
-// half-warp reads one 128-B histogram row (lane = slot), adds it into its accumulator and
-// adds the instruction's valid-sample total S(i) into the class-mix accumulator of lane
-// class(i).  The 16 sums, the 16 mix entries and the 33 derived columns are written by the
-// same warp; nothing goes back to HBM between roll-up and epilogue.
+// Each row's instruction list (load-time CSR: every instruction whose scope chain contains
+// the row's scope) is summed by a quad of lanes; the instruction's valid-sample total S(i)
+// goes to the mix entry of class(i).  The 16 sums, the 16 mix entries and the 33 derived
+// columns are written by the same quad: nothing returns to HBM between roll-up and epilogue.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -16,63 +14,135 @@
 namespace gpa {
 namespace {
 
-constexpr unsigned FULL = 0xFFFFFFFFu;
-
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7FF8000000000000ll); }
 __device__ __forceinline__ bool is_lat(int r) { return r >= 1 && r <= 11 && r != 9; }  // R4
 
-__global__ void __launch_bounds__(256) k_rollup(const uint32_t *__restrict__ ptr, const uint32_t *__restrict__ lst,
-                                                uint32_t rows, int identity, const uint64_t *__restrict__ H,
-                                                const uint8_t *__restrict__ cls, uint64_t *__restrict__ out_hist,
-                                                uint64_t *__restrict__ out_mix, double *__restrict__ metrics) {
-  const int lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t r = warp; r < rows; r += nwarps) {
-    uint32_t lo = identity ? r : __ldg(ptr + r), hi = identity ? r + 1 : __ldg(ptr + r + 1);
-    unsigned long long acc = 0, mix = 0;
-    for (uint32_t j0 = lo; j0 < hi; j0 += 2) {
-      uint32_t j = j0 + half;
-      bool ok = j < hi;
-      uint32_t i = ok ? (identity ? j : __ldg(lst + j)) : 0;
-      unsigned long long h = ok ? __ldg(H + ((uint64_t)i << 4) + sl) : 0ull;
-      acc += h;
-      unsigned long long s = sl < GPA_VALID_SLOTS ? h : 0ull;  // S(i) over the half-warp
-      s += __shfl_xor_sync(FULL, s, 8);
-      s += __shfl_xor_sync(FULL, s, 4);
-      s += __shfl_xor_sync(FULL, s, 2);
-      s += __shfl_xor_sync(FULL, s, 1);
-      if (ok && __ldg(cls + i) == sl) mix += s;
-    }
-    acc += __shfl_down_sync(FULL, acc, 16);
-    mix += __shfl_down_sync(FULL, mix, 16);
-    if (lane < 16) {
-      if (out_hist) out_hist[(uint64_t)r * GPA_SLOTS + lane] = acc;
-      if (out_mix) out_mix[(uint64_t)r * GPA_SLOTS + lane] = mix;
-    }
-    if (metrics) {
-      unsigned long long S = lane < GPA_VALID_SLOTS ? acc : 0ull;
-      unsigned long long L = (lane < GPA_VALID_SLOTS && is_lat(lane)) ? acc : 0ull;
+// Quad layout: 4 lanes per work item, lane q owns slots 4q..4q+3 of a 128-B histogram row
+// (two 16-B loads), so a warp works on 8 rows / chunks at once.  Rows longer than
+// kRollChunk instructions are split into chunks at load time; their partial sums meet in a
+// u64 scratch row (integer adds: exact in any order) and a second pass finalises them.
+__device__ __forceinline__ unsigned quad_mask() { return 0xFu << (threadIdx.x & 28); }
+
+struct Acc {
+  unsigned long long h[4], m[4];
+};
+
+// S(i) and the class-mix contribution of instruction i, added into a
+__device__ __forceinline__ void acc_inst(Acc &a, const uint64_t *__restrict__ H, const uint8_t *__restrict__ cls,
+                                         uint32_t i, int q, unsigned qm) {
+  const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(H + ((uint64_t)i << 4) + 4 * q);
+  ulonglong2 x = __ldg(p), y = __ldg(p + 1);
+  a.h[0] += x.x; a.h[1] += x.y; a.h[2] += y.x; a.h[3] += y.y;
+  unsigned long long s = q < 3 ? (x.x + x.y + y.x + y.y) : 0ull;  // slots 0..11
+  s += __shfl_xor_sync(qm, s, 1, 4);
+  s += __shfl_xor_sync(qm, s, 2, 4);
+  uint32_t k = __ldg(cls + i);
+  if ((int)(k >> 2) == q) a.m[k & 3] += s;
+}
+
+__device__ __forceinline__ void finalize(const Acc &a, uint32_t r, int q, unsigned qm, uint64_t *__restrict__ out_hist,
+                                         uint64_t *__restrict__ out_mix, double *__restrict__ metrics) {
+  if (out_hist) {
+    ulonglong2 *o = reinterpret_cast<ulonglong2 *>(out_hist + (uint64_t)r * GPA_SLOTS + 4 * q);
+    o[0] = make_ulonglong2(a.h[0], a.h[1]);
+    o[1] = make_ulonglong2(a.h[2], a.h[3]);
+  }
+  if (out_mix) {
+    ulonglong2 *o = reinterpret_cast<ulonglong2 *>(out_mix + (uint64_t)r * GPA_SLOTS + 4 * q);
+    o[0] = make_ulonglong2(a.m[0], a.m[1]);
+    o[1] = make_ulonglong2(a.m[2], a.m[3]);
+  }
+  if (!metrics) return;
+  unsigned long long S = 0, L = 0;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        S += __shfl_xor_sync(FULL, S, o);
-        L += __shfl_xor_sync(FULL, L, o);
-      }
-      unsigned long long v0 = __shfl_sync(FULL, acc, 0), v9 = __shfl_sync(FULL, acc, 9),
-                         v15 = __shfl_sync(FULL, acc, 15);
-      double *m = metrics + (uint64_t)r * GPA_NUM_DERIVED;
-      double Sd = __ull2double_rn(S);
-      bool z = S == 0;
-      if (lane == 0) {
-        m[0] = Sd;
-        m[1] = z ? qnan() : __ddiv_rn(__ull2double_rn(v0), Sd);          // W
-        m[2] = z ? qnan() : __ddiv_rn(__ull2double_rn(v0 + v9), Sd);     // latency hiding
-        m[3] = z ? qnan() : __ddiv_rn(__ull2double_rn(L), Sd);           // latency stall
-        m[16] = __ull2double_rn(v15);                                     // invalid samples
-      }
-      if (lane < GPA_VALID_SLOTS) m[4 + lane] = z ? qnan() : __ddiv_rn(__ull2double_rn(acc), Sd);
-      if (lane < 16) m[17 + lane] = z ? qnan() : __ddiv_rn(__ull2double_rn(mix), Sd);
+  for (int t = 0; t < 4; t++) {
+    int r2 = 4 * q + t;
+    if (r2 < GPA_VALID_SLOTS) S += a.h[t];
+    if (r2 < GPA_VALID_SLOTS && is_lat(r2)) L += a.h[t];
+  }
+  S += __shfl_xor_sync(qm, S, 1, 4);
+  S += __shfl_xor_sync(qm, S, 2, 4);
+  L += __shfl_xor_sync(qm, L, 1, 4);
+  L += __shfl_xor_sync(qm, L, 2, 4);
+  unsigned long long v9 = __shfl_sync(qm, a.h[1], 2, 4);   // slot 9 lives in lane 2
+  unsigned long long v15 = __shfl_sync(qm, a.h[3], 3, 4);  // slot 15 lives in lane 3
+  double *m = metrics + (uint64_t)r * GPA_NUM_DERIVED;
+  const double Sd = __ull2double_rn(S);
+  const bool z = S == 0;
+  if (q == 0) {
+    m[0] = Sd;
+    m[1] = z ? qnan() : __ddiv_rn(__ull2double_rn(a.h[0]), Sd);       // W
+    m[2] = z ? qnan() : __ddiv_rn(__ull2double_rn(a.h[0] + v9), Sd);  // latency hiding (R4)
+    m[3] = z ? qnan() : __ddiv_rn(__ull2double_rn(L), Sd);            // latency stall (R4)
+    m[16] = __ull2double_rn(v15);                                      // invalid samples
+  }
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    int r2 = 4 * q + t;
+    if (r2 < GPA_VALID_SLOTS) m[4 + r2] = z ? qnan() : __ddiv_rn(__ull2double_rn(a.h[t]), Sd);
+    m[17 + r2] = z ? qnan() : __ddiv_rn(__ull2double_rn(a.m[t]), Sd);
+  }
+}
+
+// pass 1: one quad per chunk (or per instruction when `identity`)
+__global__ void __launch_bounds__(256) k_rollup(const uint32_t *__restrict__ chunk, const uint32_t *__restrict__ lst,
+                                                uint32_t n_items, int identity,
+                                                const uint32_t *__restrict__ multi_slot, const uint64_t *__restrict__ H,
+                                                const uint8_t *__restrict__ cls, uint64_t *__restrict__ out_hist,
+                                                uint64_t *__restrict__ out_mix, double *__restrict__ metrics,
+                                                unsigned long long *__restrict__ scratch) {
+  const int q = threadIdx.x & 3;
+  const unsigned qm = quad_mask();
+  const uint32_t nq = (gridDim.x * blockDim.x) >> 2;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 2; w < n_items; w += nq) {
+    uint32_t row, b, e;
+    if (identity) {
+      row = w; b = w; e = w + 1;
+    } else {
+      row = __ldg(chunk + 3 * w); b = __ldg(chunk + 3 * w + 1); e = __ldg(chunk + 3 * w + 2);
     }
+    Acc a = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    uint32_t j = b;
+    for (; j + 4 <= e; j += 4) {  // four independent rows in flight per lane
+      uint32_t i0 = identity ? j : __ldg(lst + j), i1 = identity ? j + 1 : __ldg(lst + j + 1);
+      uint32_t i2 = identity ? j + 2 : __ldg(lst + j + 2), i3 = identity ? j + 3 : __ldg(lst + j + 3);
+      acc_inst(a, H, cls, i0, q, qm);
+      acc_inst(a, H, cls, i1, q, qm);
+      acc_inst(a, H, cls, i2, q, qm);
+      acc_inst(a, H, cls, i3, q, qm);
+    }
+    for (; j < e; j++) acc_inst(a, H, cls, identity ? j : __ldg(lst + j), q, qm);
+    const uint32_t slot = identity ? NONE : __ldg(multi_slot + row);
+    if (slot == NONE) {
+      finalize(a, row, q, qm, out_hist, out_mix, metrics);
+    } else {
+      unsigned long long *sp = scratch + (uint64_t)slot * 32;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        if (a.h[t]) atomicAdd(sp + 4 * q + t, a.h[t]);
+        if (a.m[t]) atomicAdd(sp + 16 + 4 * q + t, a.m[t]);
+      }
+    }
+  }
+}
+
+// pass 2: one quad per multi-chunk row: finalise from the scratch sums
+__global__ void __launch_bounds__(256) k_rollup_fin(const uint32_t *__restrict__ multi_rows, uint32_t n_multi,
+                                                    const unsigned long long *__restrict__ scratch,
+                                                    uint64_t *__restrict__ out_hist, uint64_t *__restrict__ out_mix,
+                                                    double *__restrict__ metrics) {
+  const int q = threadIdx.x & 3;
+  const unsigned qm = quad_mask();
+  const uint32_t nq = (gridDim.x * blockDim.x) >> 2;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 2; w < n_multi; w += nq) {
+    const unsigned long long *sp = scratch + (uint64_t)w * 32;
+    Acc a;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      a.h[t] = sp[4 * q + t];
+      a.m[t] = sp[16 + 4 * q + t];
+    }
+    finalize(a, __ldg(multi_rows + w), q, qm, out_hist, out_mix, metrics);
   }
 }
 
@@ -110,17 +180,37 @@ __global__ void __launch_bounds__(256) k_derive_f64(const double *__restrict__ V
 
 }  // namespace
 
-cudaError_t launch_rollup(const uint32_t *d_ptr, const uint32_t *d_inst, uint32_t rows, bool identity,
-                          const uint64_t *d_hist, const uint8_t *d_class, uint64_t *d_out_hist,
-                          uint64_t *d_out_mix, double *d_metrics, int sm_count, cudaStream_t st) {
+cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_hist, const uint8_t *d_class,
+                          uint64_t *d_out_hist, uint64_t *d_out_mix, double *d_metrics, int sm_count,
+                          cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  uint64_t want = ((uint64_t)rows + 7) / 8;  // 8 warps per block
+  const bool identity = set == nullptr;
+  const uint32_t items = identity ? rows : set->n_chunks;
+  unsigned long long *scratch = nullptr;
+  const uint32_t n_multi = identity ? 0 : set->n_multi;
+  if (n_multi) {
+    cudaError_t e = cudaMallocAsync((void **)&scratch, (size_t)n_multi * 32 * 8, st);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(scratch, 0, (size_t)n_multi * 32 * 8, st);
+  }
+  uint64_t want = ((uint64_t)items * 4 + 255) / 256;
   uint64_t cap = (uint64_t)sm_count * 8;
   unsigned blocks = (unsigned)(want < cap ? want : cap);
-  k_rollup<<<blocks, 256, 0, st>>>(d_ptr, d_inst, rows, identity ? 1 : 0, d_hist, d_class, d_out_hist, d_out_mix,
-                                   d_metrics);
+  k_rollup<<<blocks, 256, 0, st>>>(identity ? nullptr : set->d_chunk, identity ? nullptr : set->d_inst, items,
+                                   identity ? 1 : 0, identity ? nullptr : set->d_multi_slot, d_hist, d_class,
+                                   d_out_hist, d_out_mix, d_metrics, scratch);
   count_launches(1);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (n_multi) {
+    uint64_t b2 = ((uint64_t)n_multi * 4 + 255) / 256;
+    k_rollup_fin<<<(unsigned)(b2 < cap ? b2 : cap), 256, 0, st>>>(set->d_multi_rows, n_multi, scratch, d_out_hist,
+                                                                   d_out_mix, d_metrics);
+    count_launches(1);
+    cudaError_t e2 = cudaGetLastError();
+    cudaError_t e3 = cudaFreeAsync(scratch, st);
+    if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
+  }
+  return e;
 }
 
 cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st) {
