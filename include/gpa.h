@@ -72,7 +72,7 @@ typedef enum {
   GPA_ERR_OUT_OF_MEMORY = 4, /* device or host allocation failed                             */
   GPA_ERR_CUDA = 5,          /* a CUDA runtime call or kernel launch failed                  */
   GPA_ERR_INTERNAL = 6,      /* invariant violated inside the library (a bug)                */
-  GPA_ERR_UNSUPPORTED = 7    /* feature not built (e.g. GPA_WEIGHTS_EXACT)                   */
+  GPA_ERR_UNSUPPORTED = 7    /* feature not built                                            */
 } gpa_status;
 
 /* Scope kinds of the program-structure tree ("procedures, inlined functions,
@@ -96,7 +96,10 @@ typedef enum {
 /* CCT context kinds (R14). */
 typedef enum { GPA_CTX_FUNC = 0, GPA_CTX_SCC = 1, GPA_CTX_SCC_MEMBER = 2 } gpa_ctx_kind;
 
-/* Step-1 edge weights: call-instruction sample counts, or exact call counts. */
+/* Step-1 edge weights: call-instruction sample counts, or exact call counts.  With
+ * GPA_WEIGHTS_EXACT the histogram holds exact execution counts (instrumentation, P:376-388;
+ * see gpa_block_counts) and Step 2 and the DAG guard are skipped ("For call graphs
+ * based on samples"; R24): with consistent counts the result equals samples mode. */
 typedef enum { GPA_WEIGHTS_SAMPLES = 0, GPA_WEIGHTS_EXACT = 1 } gpa_weight_mode;
 
 /* One PC sample as a sampler delivers it ("an instruction address, a stall
@@ -236,6 +239,13 @@ GPA_API gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample 
 GPA_API gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist,
                                gpa_weight_mode mode, uint64_t max_contexts,
                                gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream);
+/* Exact counts from instrumentation (execution frequency of each basic block,
+ * propagated to its instructions): for block b, every instruction block_start[b] ..
+ * block_start[b+1]-1 gains d_counts[b] in slot 0 of d_inst_hist (accumulated, u64).
+ * d_block_start: DEVICE [n_blocks+1], ascending instruction indices (indices >= n_inst are
+ * clipped).  Enqueue-only. */
+GPA_API gpa_status gpa_block_counts(gpa_structure s, uint32_t n_blocks, const uint32_t *d_block_start,
+                                    const uint64_t *d_counts, uint64_t *d_inst_hist, gpa_stream_t stream);
 GPA_API gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *out);
 /* Releases the tree's device memory in stream order on the stream gpa_reconstruct_cct was
  * called with (no device synchronization); work on other streams that still reads the views

@@ -64,8 +64,10 @@ def _lib():
     lib.oracle_rollup.restype = None
     lib.oracle_inst_func.argtypes = [u32, vp, u32, vp, u32, vp, vp]
     lib.oracle_inst_func.restype = None
-    lib.oracle_cct.argtypes = [u32, vp, u32, vp, u32, vp, u32, vp, vp, vp, u64]
-    lib.oracle_cct.restype = ctypes.POINTER(_CctResult)
+    lib.oracle_cct_mode.argtypes = [u32, vp, u32, vp, u32, vp, u32, vp, vp, vp, u64, ctypes.c_int]
+    lib.oracle_cct_mode.restype = ctypes.POINTER(_CctResult)
+    lib.oracle_block_counts.argtypes = [u32, vp, vp, vp]
+    lib.oracle_block_counts.restype = None
     lib.oracle_cct_free.argtypes = [ctypes.POINTER(_CctResult)]
     lib.oracle_cct_free.restype = None
     lib.oracle_derive_u64.argtypes = [u64, vp, vp, vp]
@@ -158,14 +160,16 @@ def scope_hist(st: dict, H, scope: str):
 
 
 # ---- D3-D6 ------------------------------------------------------------------------------
-def cct(st: dict, H, max_contexts: int = (1 << 63)) -> dict:
-    """D3-D6: the approximate GPU CCT (BFS numbering) and the Step 1-3 intermediates."""
+def cct(st: dict, H, max_contexts: int = (1 << 63), exact: bool = False) -> dict:
+    """D3-D6: the approximate GPU CCT (BFS numbering) and the Step 1-3 intermediates.
+    exact=True: H holds exact execution counts; Step 2 and the guard are skipped (R24)."""
     n_inst, n_scope = len(st["inst_addr"]), len(st["scope_parent"])
     n_func, n_call = len(st["func_scope"]), len(st["call_inst"])
     a = {k: _c(st[k], np.uint32) for k in ("inst_scope", "scope_parent", "func_scope", "call_inst", "call_callee")}
     Hc, ph = _c(H, np.uint64)
-    r = _lib().oracle_cct(n_inst, a["inst_scope"][1], n_scope, a["scope_parent"][1], n_func,
-                          a["func_scope"][1], n_call, a["call_inst"][1], a["call_callee"][1], ph, max_contexts)
+    r = _lib().oracle_cct_mode(n_inst, a["inst_scope"][1], n_scope, a["scope_parent"][1], n_func,
+                               a["func_scope"][1], n_call, a["call_inst"][1], a["call_callee"][1], ph, max_contexts,
+                               1 if exact else 0)
     try:
         R = r.contents
         n, nd = int(R.n), int(R.n_dag)
@@ -190,6 +194,16 @@ def cct(st: dict, H, max_contexts: int = (1 << 63)) -> dict:
     finally:
         _lib().oracle_cct_free(r)
     return out
+
+
+def block_counts(n_inst: int, block_start, count) -> np.ndarray:
+    """Exact per-instruction counts (slot 0) from basic-block execution counts."""
+    bs, pb = _c(block_start, np.uint32)
+    c, pc = _c(count, np.uint64)
+    H = np.zeros((n_inst, SLOTS), np.uint64)
+    if len(c):
+        _lib().oracle_block_counts(len(c), pb, pc, H.ctypes.data)
+    return H
 
 
 # ---- D7 ---------------------------------------------------------------------------------

@@ -236,11 +236,11 @@ static int o_append(oracle_cct_result *R, uint8_t kind, uint32_t node, uint32_t 
   return 0;
 }
 
-oracle_cct_result *oracle_cct(uint32_t n_inst, const uint32_t *inst_scope,
-                              uint32_t n_scope, const uint32_t *scope_parent,
-                              uint32_t n_func, const uint32_t *func_scope,
-                              uint32_t n_call, const uint32_t *call_inst, const uint32_t *call_callee,
-                              const uint64_t *H, uint64_t max_contexts)
+oracle_cct_result *oracle_cct_mode(uint32_t n_inst, const uint32_t *inst_scope,
+                                   uint32_t n_scope, const uint32_t *scope_parent,
+                                   uint32_t n_func, const uint32_t *func_scope,
+                                   uint32_t n_call, const uint32_t *call_inst, const uint32_t *call_callee,
+                                   const uint64_t *H, uint64_t max_contexts, int exact)
 {
   oracle_cct_result *R = (oracle_cct_result *)calloc(1, sizeof(oracle_cct_result));
   R->n_func = n_func; R->n_call = n_call;
@@ -302,6 +302,7 @@ oracle_cct_result *oracle_cct(uint32_t n_inst, const uint32_t *inst_scope,
     R->func_active[f] = s > 0;
     if (R->func_active[f]) work[nwork++] = f;
   }
+  if (exact) nwork = 0;   /* exact counts: Step 2 is "for call graphs based on samples" (R24) */
   while (nwork > 0) {
     uint32_t f = work[--nwork];
     if (in_ptr[f + 1] == in_ptr[f]) continue;                 /* no incoming edges */
@@ -351,8 +352,9 @@ oracle_cct_result *oracle_cct(uint32_t n_inst, const uint32_t *inst_scope,
    * from outside X. */
   R->dag_active = (uint8_t *)calloc(n_dag + 1, 1);
   for (uint32_t f = 0; f < n_func; f++) if (R->func_active[f]) R->dag_active[R->scc_of[f]] = 1;
-  /* Guard (reading R12): the Step-2 rule once more on the DAG, to its fixpoint. */
-  int changed = 1;
+  /* Guard (reading R12): the Step-2 rule once more on the DAG, to its fixpoint (samples
+   * mode only, like Step 2 itself; R24). */
+  int changed = !exact;
   while (changed) {
     changed = 0;
     for (uint32_t X = 0; X < n_dag; X++) {
@@ -438,6 +440,26 @@ oracle_cct_result *oracle_cct(uint32_t n_inst, const uint32_t *inst_scope,
   free(comp_min); free(comp_to_dag); free(n_members); free(has_ext_in);
   free(dag_members_ptr); free(dag_members);
   return R;
+}
+
+oracle_cct_result *oracle_cct(uint32_t n_inst, const uint32_t *inst_scope,
+                              uint32_t n_scope, const uint32_t *scope_parent,
+                              uint32_t n_func, const uint32_t *func_scope,
+                              uint32_t n_call, const uint32_t *call_inst, const uint32_t *call_callee,
+                              const uint64_t *H, uint64_t max_contexts)
+{
+  return oracle_cct_mode(n_inst, inst_scope, n_scope, scope_parent, n_func, func_scope, n_call, call_inst,
+                         call_callee, H, max_contexts, 0);
+}
+
+/* Exact counts from instrumentation ("count the execution frequency of each basic
+ * block ... propagate the counts to each instruction in the block"): every instruction of
+ * block b (instructions block_start[b] .. block_start[b+1]-1) gains count[b] executions in
+ * slot 0 of H (an executed instruction "issued"; reading R24). */
+void oracle_block_counts(uint32_t n_blocks, const uint32_t *block_start, const uint64_t *count, uint64_t *H)
+{
+  for (uint32_t b = 0; b < n_blocks; b++)
+    for (uint32_t i = block_start[b]; i < block_start[b + 1]; i++) H[(uint64_t)i * O_SLOTS + 0] += count[b];
 }
 
 void oracle_cct_free(oracle_cct_result *R)

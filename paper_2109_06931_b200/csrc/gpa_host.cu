@@ -652,7 +652,7 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
 gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa_weight_mode mode,
                                uint64_t max_contexts, gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream) {
   if (!s || !n_contexts || (max_contexts && !out)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
-  if (mode != GPA_WEIGHTS_SAMPLES) return fail(GPA_ERR_UNSUPPORTED, "only GPA_WEIGHTS_SAMPLES is built");
+  if (mode != GPA_WEIGHTS_SAMPLES && mode != GPA_WEIGHTS_EXACT) return fail(GPA_ERR_INVALID_ARG, "mode %d", (int)mode);
   if (!d_inst_hist && s->info.n_inst) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
   if ((uintptr_t)d_inst_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist must be 16-byte aligned");
   if (out) *out = nullptr;
@@ -688,7 +688,8 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   CC(launch_rollup(&s->roll[ROLL_FUNC], s->roll[ROLL_FUNC].rows, d_inst_hist, s->d_inst_class, c->S_f, nullptr,
                    nullptr, sm_count(s->device), st));
   // Step 2 + guard (R12) + W + context count (path DP over the DAG)
-  CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, st));
+  CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, mode == GPA_WEIGHTS_EXACT,
+                          st));
   unsigned long long h_cnt[2] = {0, 0};
   CC(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
   CC(cudaStreamSynchronize(st));
@@ -746,6 +747,17 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
     CC(launch_cct_incl_level(c, c->level_start[L], c->level_start[L + 1], st));
 #undef CC
   *out = c;
+  return GPA_OK;
+}
+
+gpa_status gpa_block_counts(gpa_structure s, uint32_t n_blocks, const uint32_t *d_block_start,
+                            const uint64_t *d_counts, uint64_t *d_inst_hist, gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (n_blocks == 0) return GPA_OK;
+  if (!d_block_start || !d_counts || !d_inst_hist) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CU(launch_block_counts(n_blocks, d_block_start, d_counts, s->info.n_inst, d_inst_hist, (cudaStream_t)stream));
   return GPA_OK;
 }
 

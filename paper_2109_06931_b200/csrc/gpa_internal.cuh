@@ -110,7 +110,9 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
                                cudaStream_t st);
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
-                                 unsigned long long *d_count, cudaStream_t st);
+                                 unsigned long long *d_count, bool exact, cudaStream_t st);
+cudaError_t launch_block_counts(uint32_t n_blocks, const uint32_t *d_start, const uint64_t *d_cnt, uint32_t n_inst,
+                                uint64_t *d_hist, cudaStream_t st);
 cudaError_t launch_cct_roots(const gpa_structure_s *s, const uint8_t *d_dag_active, gpa_cct_s *c,
                              unsigned long long *d_n, cudaStream_t st);
 cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a, uint64_t b,

@@ -248,8 +248,6 @@ constexpr int kHotSlots = GPA_VALID_SLOTS;
 constexpr int kHotRows = 3328;                     // 3328 x 12 x 4 B = 156 KiB
 using RingHot = Ring<16, 2, 4>;                    // 4 x 16 KiB stages
 constexpr int kLook = 2;                           // tiles of records + codes in flight ahead
-constexpr size_t kHotTab = (size_t)kHotRows * kHotSlots * 4;
-constexpr size_t kHotSmem = RingHot::kBytes + kHotTab + 2 * RingHot::kStages * 8;
 constexpr int kSampleChunks = 64, kSampleChunk = 1 << 15;
 constexpr uint64_t kHotMinRecords = (uint64_t)kSampleChunks * kSampleChunk;
 constexpr int kVBins = 4096;
@@ -356,23 +354,23 @@ __global__ void k_codemap(const uint32_t *__restrict__ gmap, uint64_t n_gran, co
   }
 }
 
-template <bool REC>
-__global__ void __launch_bounds__(RingHot::kThreads, 1)
+template <class RG, int ROWS, bool REC>
+__global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_hot(uint64_t base, uint64_t n_gran, uint32_t gshift, const uint32_t *__restrict__ code,
                const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
                unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
                const uint32_t *__restrict__ row_inst, const uint32_t *__restrict__ thr) {
   extern __shared__ __align__(128) uint8_t smem[];
-  using RG = RingHot;
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = kLook + 1;
+  constexpr size_t TAB = (size_t)ROWS * kHotSlots * 4;
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
   uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + kHotTab);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + TAB);
   uint64_t *empty = full + NST;
   const uint32_t tab_s = smem_u32(tab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t ntiles = (n + S - 1) / S;
-  const uint32_t nhot = min(thr[1], (uint32_t)kHotRows);
+  const uint32_t nhot = min(thr[1], (uint32_t)ROWS);
   for (uint32_t x = threadIdx.x; x < nhot * kHotSlots; x += blockDim.x) tab[x] = 0;
   ring_init(full, empty, NST, NC);
   __syncthreads();
@@ -448,6 +446,18 @@ done:
   }
 }
 
+template <class RG, int ROWS>
+cudaError_t run_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H, unsigned long long *U,
+                    uint32_t *ri, const uint32_t *code, const uint32_t *row_inst, const uint32_t *thr, int sm_count,
+                    cudaStream_t st) {
+  auto kern = ri ? k_attr_hot<RG, ROWS, true> : k_attr_hot<RG, ROWS, false>;
+  const size_t smem = RG::kBytes + (size_t)ROWS * kHotSlots * 4 + 2 * RG::kStages * 8;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<sm_count, RG::kThreads, smem, st>>>(T.base, T.n_gran, T.gshift, code, rec, n, H, U, ri, row_inst, thr);
+  return cudaGetLastError();
+}
+
 int g_attr_kernel = -1;  // gpa_set_attr_kernel; -1 = read GPA_ATTR_VARIANT once (0 if unset)
 
 int attr_variant() {  // 0 auto, 1 stream, 2 tma, 3 hot (when applicable)
@@ -475,13 +485,7 @@ cudaError_t launch_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsign
   k_pick<<<1, 1024, 0, st>>>(V, thr, kHotRows);
   k_assign<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_row, row_inst, kHotRows);
   k_codemap<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_row, code);
-  auto kern = ri ? k_attr_hot<true> : k_attr_hot<false>;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHotSmem);
-  if (e == cudaSuccess) {
-    kern<<<sm_count, RingHot::kThreads, kHotSmem, st>>>(T.base, T.n_gran, T.gshift, code, rec, n, H, U, ri, row_inst,
-                                                       thr);
-    e = cudaGetLastError();
-  }
+  e = run_hot<RingHot, kHotRows>(T, rec, n, H, U, ri, code, row_inst, thr, sm_count, st);
   count_launches(6);
   cudaError_t e2 = cudaFreeAsync(w, st);
   return e != cudaSuccess ? e : e2;

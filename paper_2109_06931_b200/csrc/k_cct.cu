@@ -39,7 +39,7 @@ __global__ void k_weights(const uint32_t *__restrict__ call_inst, uint32_t n_cal
 }
 
 struct PropArgs {
-  uint32_t n_func, n_dag, n_lev;
+  uint32_t n_func, n_dag, n_lev, exact;
   const uint64_t *S_f;
   const uint32_t *fin_ptr, *fin_e, *caller, *scc_of, *din_ptr, *din_e, *dmem_ptr, *dmem, *dlev_ptr, *dlev_node;
   const uint8_t *nontriv;
@@ -65,8 +65,9 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
   // Step 2: "if a function has samples and none of its incoming call edges has a non-zero
   // weight, we assign each of its incoming call edges a weight of one; we repeat this
   // propagation through callers".  Each function's in-edges are written only by
-  // the thread that owns the function, so a round's result is race-free.
-  for (;;) {
+  // the thread that owns the function, so a round's result is race-free.  Exact counts skip
+  // it ("For call graphs based on samples", R24).
+  for (; !A.exact;) {
     __syncthreads();
     if (t == 0) changed = 0;
     __syncthreads();
@@ -87,12 +88,14 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
     if (!changed) break;
   }
   // DAG activity, then the guard (R12): the same rule on external in-edges of DAG nodes
+  // (samples mode only, like Step 2)
+  __syncthreads();
   for (uint32_t X = t; X < A.n_dag; X += nt) {
     uint8_t act = 0;
     for (uint32_t k = A.dmem_ptr[X]; k < A.dmem_ptr[X + 1]; k++) act |= fact[A.dmem[k]];
     dact[X] = act;
   }
-  for (;;) {
+  for (; !A.exact;) {
     __syncthreads();
     if (t == 0) changed = 0;
     __syncthreads();
@@ -440,6 +443,18 @@ __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag,
   if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
 }
 
+// Exact counts from instrumentation: block b's execution count goes to slot 0 of
+// every instruction of the block.  One thread per block; blocks are short and disjoint.
+__global__ void k_block_counts(uint32_t n_blocks, const uint32_t *__restrict__ start, const uint64_t *__restrict__ cnt,
+                               uint32_t n_inst, unsigned long long *__restrict__ H) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < n_blocks; b += gridDim.x * blockDim.x) {
+    uint32_t lo = start[b], hi = min(start[b + 1], n_inst);
+    unsigned long long c = cnt[b];
+    if (c)
+      for (uint32_t i = lo; i < hi; i++) atomicAdd(H + ((uint64_t)i << 4), c);
+  }
+}
+
 unsigned grid_for(uint64_t work, unsigned threads) {
   uint64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -468,14 +483,14 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
 
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
-                                 unsigned long long *d_count, cudaStream_t st) {
+                                 unsigned long long *d_count, bool exact, cudaStream_t st) {
   // paths[] scratch lives behind W in the caller's allocation? keep it separate and simple:
   static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
   uint64_t *paths = nullptr;
   cudaError_t e = cudaMallocAsync((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1), st);
   if (e != cudaSuccess) return e;
   PropArgs A;
-  A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels;
+  A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels; A.exact = exact ? 1 : 0;
   A.S_f = d_S_f; A.fin_ptr = s->d_fin_ptr; A.fin_e = s->d_fin_e; A.caller = s->d_call_caller;
   A.scc_of = s->d_scc_of; A.din_ptr = s->d_din_ptr; A.din_e = s->d_din_e; A.dmem_ptr = s->d_dmem_ptr;
   A.dmem = s->d_dmem; A.dlev_ptr = s->d_dlev_ptr; A.dlev_node = s->d_dlev_node; A.nontriv = s->d_dag_nontrivial;
@@ -507,6 +522,15 @@ cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a,
   k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(d_tmp, m, d_bs);
   k_level_write<<<grid_for(m, 256), 256, 0, st>>>(A, a, b, d_tmp);
   count_launches(5);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_counts(uint32_t n_blocks, const uint32_t *d_start, const uint64_t *d_cnt, uint32_t n_inst,
+                                uint64_t *d_hist, cudaStream_t st) {
+  if (!n_blocks) return cudaSuccess;
+  k_block_counts<<<grid_for(n_blocks, 256), 256, 0, st>>>(n_blocks, d_start, d_cnt, n_inst,
+                                                          (unsigned long long *)d_hist);
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -77,6 +77,7 @@ def _load():
         "gpa_free_cct": ([_vp], None),
         "gpa_derive_metrics": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], S),
         "gpa_kernel_launches": ([], ctypes.c_uint64),
+        "gpa_block_counts": ([_vp, _u32, _vp, _vp, _vp, _vp], S),
         "gpa_set_attr_kernel": ([ctypes.c_int], S),
     }
     for name, (args, res) in sig.items():
@@ -217,6 +218,14 @@ def attribute_samples_host(s: Structure, samples, inst_hist, unattributed, strea
         s.handle, ptr, nb // 16, _ptr(inst_hist, "inst_hist", 128 * s.info["n_inst"]),
         _ptr(unattributed, "unattributed", 128), _stream_ptr(stream, inst_hist.device)),
         "gpa_attribute_samples_host")
+
+
+def block_counts(s: Structure, block_start, counts, inst_hist, stream=None) -> None:
+    """Exact per-instruction counts from basic-block counts (CUDA tensors; see gpa.h)."""
+    nb = counts.numel()
+    _check(_lib.gpa_block_counts(s.handle, nb, _ptr(block_start, "block_start", 4 * (nb + 1)),
+                                 _ptr(counts, "counts", 8 * nb), _ptr(inst_hist, "inst_hist"),
+                                 _stream_ptr(stream, inst_hist.device)), "gpa_block_counts")
 
 
 class _DevArray:

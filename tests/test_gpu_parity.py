@@ -213,12 +213,13 @@ def test_rollup_and_derive_parity(gpa, name, records):
 
 
 # ---- a-6..a-10: CCT ----------------------------------------------------------------------------
-def _cct_compare(gpa, s, st, H_np, bit_exact=True):
+def _cct_compare(gpa, s, st, H_np, bit_exact=True, exact=False):
     H = torch.from_numpy(H_np.view(np.int64)).to(DEV).reshape(-1, 16)
-    n_pred = gpa.reconstruct_cct(s, H, max_contexts=0)
-    R = oracle.cct(st, H_np)
+    mode = gpa.WEIGHTS_EXACT if exact else gpa.WEIGHTS_SAMPLES
+    n_pred = gpa.reconstruct_cct(s, H, mode=mode, max_contexts=0)
+    R = oracle.cct(st, H_np, exact=exact)
     assert n_pred == R["n"]
-    c = gpa.reconstruct_cct(s, H)
+    c = gpa.reconstruct_cct(s, H, mode=mode)
     g = c.to_numpy()
     assert g["n"] == R["n"]
     for k in ["parent", "site", "node", "kind", "first_child", "n_children"]:
@@ -260,12 +261,33 @@ def test_cct_spec_examples(gpa, case):
     _cct_compare(gpa, gpa.load_structure(st, 0), st, H)
 
 
+@pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("seed", range(40))
-def test_cct_random_graphs(gpa, seed):
+def test_cct_random_graphs(gpa, seed, exact):
     from tests.test_oracle_cct import _random_graph
     rng = np.random.default_rng(1000 + seed)
     st, H, _ = build_fixture(_random_graph(rng))
-    _cct_compare(gpa, gpa.load_structure(st, 0), st, H)
+    _cct_compare(gpa, gpa.load_structure(st, 0), st, H, exact=exact)
+
+
+def test_cct_exact_golden_and_block_counts(gpa):
+    g = load_golden("cct_exact.json")
+    st, H, _ = build_fixture(g["inconsistent"]["spec"])
+    R = _cct_compare(gpa, gpa.load_structure(st, 0), st, H, exact=True)
+    assert R["n"] == len(g["inconsistent"]["expect"]["contexts"])
+    # instrumentation counts: basic blocks -> instructions, then an exact-mode CCT
+    w = gen.workload("C3", records=10)
+    s = gpa.load_structure(w.structure, 0)
+    n_inst = s.info["n_inst"]
+    rng = np.random.default_rng(9)
+    cuts = np.sort(rng.choice(np.arange(1, n_inst), 20_000, replace=False))
+    start = np.concatenate([[0], cuts, [n_inst]]).astype(np.uint32)
+    cnt = rng.integers(0, 1000, len(start) - 1).astype(np.uint64)
+    Ht = torch.zeros((n_inst, 16), dtype=torch.int64, device=DEV)
+    gpa.block_counts(s, torch.from_numpy(start.view(np.int32)).to(DEV), torch.from_numpy(cnt.view(np.int64)).to(DEV), Ht)
+    Ho = oracle.block_counts(n_inst, start, cnt)
+    assert np.array_equal(u64(Ht), Ho)
+    _cct_compare(gpa, s, w.structure, Ho, exact=True)
 
 
 @pytest.mark.parametrize("name,records", [("C1", 10_000), ("C2", 1_000_000), ("C3", 2_000_000),
@@ -288,8 +310,8 @@ def test_cct_capacity(gpa):
         gpa.reconstruct_cct(s, Ht, max_contexts=5)
     assert ei.value.status == 3
     with pytest.raises(gpa.GpaError) as ei:
-        gpa.reconstruct_cct(s, Ht, mode=gpa.WEIGHTS_EXACT)
-    assert ei.value.status == 7
+        gpa.reconstruct_cct(s, Ht, mode=5)
+    assert ei.value.status == 1
 
 
 # ---- every attribution kernel, and the u32 wrap repayment of the shared-memory rows -------------

@@ -15,8 +15,8 @@ NONE = oracle.NONE
 KIND = {"FUNC": 0, "SCC": 1, "MEMBER": 2}
 
 
-def _check_expected(st, H, expect):
-    R = oracle.cct(st, H)
+def _check_expected(st, H, expect, exact=False):
+    R = oracle.cct(st, H, exact=exact)
     assert R["status"] == 0
     if "w_step1" in expect:
         assert R["w_step1"].tolist() == expect["w_step1"]
@@ -60,7 +60,7 @@ def test_cct_spec_examples(case):
 # ---------------------------------------------------------------------------------------
 # brute force with exact rationals
 # ---------------------------------------------------------------------------------------
-def brute_cct(st, H):
+def brute_cct(st, H, exact=False):
     n_func, n_call = len(st["func_scope"]), len(st["call_inst"])
     ifunc = oracle.inst_func(st)
     callee = [int(x) for x in st["call_callee"]]
@@ -72,7 +72,7 @@ def brute_cct(st, H):
             S[ifunc[i]][r] += int(H[i, r])
     w = [int(H[st["call_inst"][e], :12].sum()) for e in range(n_call)]
     active = [sum(S[f][:12]) > 0 for f in range(n_func)]
-    changed = True
+    changed = not exact                     # exact counts: no Step 2, no guard (R24)
     while changed:                          # Step 2 by whole-graph sweeps to a fixpoint
         changed = False
         for f in range(n_func):
@@ -99,7 +99,7 @@ def brute_cct(st, H):
     nontriv = {d: len(m) > 1 or reach[m[0]][m[0]] for d, m in members.items()}
     ext_in = {d: [e for e in range(n_call) if scc[callee[e]] == d and scc[caller[e]] != d] for d in members}
     dact = {d: any(active[f] for f in m) for d, m in members.items()}
-    changed = True
+    changed = not exact
     while changed:                          # DAG guard (reading R12)
         changed = False
         for d in members:
@@ -170,12 +170,13 @@ def _random_graph(rng):
     return spec
 
 
+@pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("seed", range(60))
-def test_cct_brute_force_random_graphs(seed):
+def test_cct_brute_force_random_graphs(seed, exact):
     rng = np.random.default_rng(1000 + seed)
     st, H, _ = build(_random_graph(rng))
-    R = oracle.cct(st, H)
-    ctxs, w, scc, W, S, _ = brute_cct(st, H)
+    R = oracle.cct(st, H, exact=exact)
+    ctxs, w, scc, W, S, _ = brute_cct(st, H, exact=exact)
     assert R["w"].tolist() == w
     assert R["scc_of"].tolist() == scc
     assert R["W"].tolist() == [W[d] for d in range(len(W))]
@@ -270,3 +271,29 @@ def test_cct_capacity_and_empty():
     R = oracle.cct(st, np.zeros_like(H))
     assert R["status"] == 0 and R["n"] == 0
     assert R["w"].tolist() == [0] * 6
+
+
+def test_cct_exact_mode_fixtures():
+    """R24: with consistent exact counts Step 2 is a no-op, so the exact
+    tree equals the samples tree; with an executed function behind an unexecuted call,
+    exact mode leaves it out."""
+    g = load_golden("cct_exact.json")
+    st, H, _ = build(g["consistent"])
+    Rs, Re = oracle.cct(st, H), oracle.cct(st, H, exact=True)
+    for k in ["parent", "site", "node", "kind", "frac", "excl", "incl", "w"]:
+        assert np.array_equal(Rs[k], Re[k]), k
+    st, H, _ = build(g["inconsistent"]["spec"])
+    _check_expected(st, H, g["inconsistent"]["expect"], exact=True)
+
+
+def test_block_counts_propagate_to_instructions():
+    """a basic block's execution count is every member instruction's count."""
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        n_inst = int(rng.integers(1, 200))
+        cuts = np.sort(rng.choice(np.arange(1, n_inst), size=min(n_inst - 1, int(rng.integers(0, 20))), replace=False))
+        start = np.concatenate([[0], cuts, [n_inst]]).astype(np.uint32)
+        cnt = rng.integers(0, 2 ** 40, len(start) - 1).astype(np.uint64)
+        H = oracle.block_counts(n_inst, start, cnt)
+        expect = np.repeat(cnt, np.diff(start.astype(np.int64)))
+        assert np.array_equal(H[:, 0], expect) and H[:, 1:].sum() == 0

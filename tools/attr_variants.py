@@ -39,7 +39,8 @@ if __name__ == "__main__":
     records = int(sys.argv[2]) if len(sys.argv) > 2 else 4_000_000_000
     variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["1", "2", "3"]
     for v in variants:
-        env = dict(os.environ, GPA_ATTR_VARIANT=v)
+        var, _, cfg = v.partition(":")
+        env = dict(os.environ, GPA_ATTR_VARIANT=var, GPA_HOT_CFG=cfg or "0")
         out = subprocess.run([sys.executable, "-c", CHILD, name, str(records), "5"], env=env, capture_output=True,
                              text=True)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:].replace("\n", " | ")
