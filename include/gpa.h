@@ -52,6 +52,7 @@ typedef struct CUstream_st *gpa_stream_t;
 #define GPA_CLASSES      16          /* instruction classes (R5)                       */
 #define GPA_NUM_DERIVED  33          /* derived columns per row (R3-R5, DESIGN.md §3 table)    */
 #define GPA_NONE         0xFFFFFFFFu /* "no index" in every u32 index array                    */
+#define GPA_NUM_STATS    6           /* cross-profile statistics: sum min mean max std cv (R25) */
 
 /* Stall slots, modeled on CUPTI's PC-sampling stall enumeration (R2; the paper only says
  * "a stall reason").  Slot 0 = the warp issued (not stalled); W uses it. */
@@ -226,6 +227,25 @@ GPA_API gpa_status gpa_attribute_samples(gpa_structure s, const gpa_sample *d_sa
 GPA_API gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_samples, uint64_t n,
                                       uint64_t *d_inst_hist, uint64_t *d_unattributed,
                                       gpa_stream_t stream);
+
+/* ---- f1: per-profile histograms and cross-profile statistics ----------------------------
+ * P:481-487 (§4.5): derived metrics "for combining metrics from different thread profiles ...
+ * sum, min, mean, max, std. deviation, and coefficient of variation".  A profile is the
+ * record's `stream` field (a GPU stream / rank / thread).
+ * gpa_attribute_profiles: like gpa_attribute_samples, but per profile and per FUNCTION:
+ *   d_prof_hist[(p*n_func + f)*16 + slot] += count for records of profile p attributed to an
+ *   instruction of function f; unattributed records -> d_prof_unattr[p*16 + slot].  Records
+ *   with stream >= n_profiles use profile row n_profiles, so both buffers hold n_profiles+1
+ *   rows ((n_profiles+1)*n_func*16 and (n_profiles+1)*16 u64).  Accumulates; enqueue-only.
+ * gpa_profile_stats: for every function f and slot r, over profiles p < n_profiles (R25,
+ *   population convention, exact integer sums before one rounding):
+ *   d_stats[(f*6 + k)*16 + r], k = 0 sum, 1 min, 2 mean = sum/P, 3 max,
+ *   4 std = sqrt(P*sum(x^2) - sum(x)^2)/P, 5 cv = std/mean (0 when mean = 0).  Enqueue-only. */
+GPA_API gpa_status gpa_attribute_profiles(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+                                          uint32_t n_profiles, uint64_t *d_prof_hist, uint64_t *d_prof_unattr,
+                                          gpa_stream_t stream);
+GPA_API gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles,
+                                     double *d_stats, gpa_stream_t stream);
 
 /* ---- a-6..a-9: approximate GPU calling-context tree (§5.3) -----------------
  * From a per-instruction histogram: Step 1 edge weights w_e = sum_{r<12} H[call_inst[e]][r]

@@ -66,6 +66,10 @@ def _lib():
     lib.oracle_inst_func.restype = None
     lib.oracle_cct_mode.argtypes = [u32, vp, u32, vp, u32, vp, u32, vp, vp, vp, u64, ctypes.c_int]
     lib.oracle_cct_mode.restype = ctypes.POINTER(_CctResult)
+    lib.oracle_attribute_profiles.argtypes = [u32, vp, vp, vp, u32, vp, u64, u32, vp, vp]
+    lib.oracle_attribute_profiles.restype = None
+    lib.oracle_profile_stats.argtypes = [u32, u32, vp, vp]
+    lib.oracle_profile_stats.restype = None
     lib.oracle_block_counts.argtypes = [u32, vp, vp, vp]
     lib.oracle_block_counts.restype = None
     lib.oracle_cct_free.argtypes = [ctypes.POINTER(_CctResult)]
@@ -193,6 +197,32 @@ def cct(st: dict, H, max_contexts: int = (1 << 63), exact: bool = False) -> dict
             dag_active=arr(R.dag_active, nd, np.uint8), W=arr(R.W, nd, np.uint64))
     finally:
         _lib().oracle_cct_free(r)
+    return out
+
+
+def attribute_profiles(st: dict, rec, n_prof: int):
+    """D8: per-profile function histograms Hp [n_prof+1, n_func, 16] and unattributed
+    Up [n_prof+1, 16] (row n_prof collects stream ids >= n_prof)."""
+    rec = _records(rec)
+    n_inst, n_func = len(st["inst_addr"]), len(st["func_scope"])
+    addr, pa = _c(st["inst_addr"], np.uint64)
+    ln, pl = _c(st["inst_len"], np.uint16)
+    ifn, pf = _c(inst_func(st), np.uint32)
+    Hp = np.zeros((n_prof + 1, n_func, SLOTS), np.uint64)
+    Up = np.zeros((n_prof + 1, SLOTS), np.uint64)
+    if len(rec):
+        _lib().oracle_attribute_profiles(n_inst, pa, pl, pf, n_func, rec.ctypes.data, len(rec), n_prof,
+                                         Hp.ctypes.data if Hp.size else None, Up.ctypes.data)
+    return Hp, Up
+
+
+def profile_stats(Hp, n_prof: int) -> np.ndarray:
+    """D8: [rows, 6, 16] = sum, min, mean, max, std (population), cv over profiles 0..n_prof-1."""
+    Hp = np.ascontiguousarray(Hp, np.uint64)
+    rows = Hp.shape[1]
+    out = np.empty((rows, 6, SLOTS), np.float64)
+    if rows:
+        _lib().oracle_profile_stats(n_prof, rows, Hp.ctypes.data, out.ctypes.data)
     return out
 
 

@@ -25,6 +25,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
+#include <math.h>
 
 #define O_SLOTS 16         /* slots per instruction row: 12 reasons, 3 reserved, 1 invalid */
 #define O_VALID 12         /* stall reasons 0..11 (R2)                           */
@@ -470,6 +471,62 @@ void oracle_cct_free(oracle_cct_result *R)
   free(R->w_step1); free(R->w); free(R->func_active); free(R->S_f); free(R->scc_of);
   free(R->dag_nontrivial); free(R->dag_active); free(R->W);
   free(R);
+}
+
+/* ======================================================================================
+ * D8 — per-profile histograms and cross-profile statistics.  P:481-487:
+ * "Built-in derived metrics for combining metrics from different thread profiles ... include
+ * sum, min, mean, max, std. deviation, and coefficient of variation"; a profile is an
+ * application thread, rank or GPU stream — here the record's `stream` field.
+ * Per profile p, function f, slot r: Hp[p][f][r] = sum of counts of p's records attributed
+ * (D1) to an instruction of f; records with stream >= n_prof land in profile row n_prof.
+ * Statistics over p = 0..n_prof-1 of x_p = Hp[p][f][r] (reading R25): population convention,
+ * computed exactly in integers before one conversion:
+ *   sum = Σx, min, max, mean = Σx / P, std = sqrt(P·Σx² − (Σx)²) / P, cv = std / mean
+ *   (cv = 0 when mean = 0).  Output [f][6][16]: 0 sum, 1 min, 2 mean, 3 max, 4 std, 5 cv.
+ * ====================================================================================== */
+void oracle_attribute_profiles(uint32_t n_inst, const uint64_t *inst_addr, const uint16_t *inst_len,
+                               const uint32_t *inst_func, uint32_t n_func, const o_record *rec, uint64_t n,
+                               uint32_t n_prof, uint64_t *Hp, uint64_t *Up)
+{
+  for (uint64_t k = 0; k < n; k++) {
+    uint64_t pc = rec[k].pc;
+    uint32_t slot = rec[k].stall < O_VALID ? rec[k].stall : O_INVALID;
+    uint32_t p = rec[k].stream < n_prof ? rec[k].stream : n_prof;
+    int64_t j = o_last_start_le(inst_addr, n_inst, pc);
+    if (j >= 0 && pc < inst_addr[j] + inst_len[j])
+      Hp[((uint64_t)p * n_func + inst_func[j]) * O_SLOTS + slot] += rec[k].count;
+    else
+      Up[(uint64_t)p * O_SLOTS + slot] += rec[k].count;
+  }
+}
+
+void oracle_profile_stats(uint32_t n_prof, uint32_t rows, const uint64_t *Hp, double *out)
+{
+  for (uint32_t f = 0; f < rows; f++) {
+    for (int r = 0; r < O_SLOTS; r++) {
+      unsigned __int128 sum = 0, sq = 0;
+      uint64_t mn = UINT64_MAX, mx = 0;
+      for (uint32_t p = 0; p < n_prof; p++) {
+        uint64_t x = Hp[((uint64_t)p * rows + f) * O_SLOTS + r];
+        sum += x;
+        sq += (unsigned __int128)x * x;
+        if (x < mn) mn = x;
+        if (x > mx) mx = x;
+      }
+      double *o = out + (uint64_t)f * 6 * O_SLOTS;
+      double P = (double)n_prof, S = (double)sum;
+      unsigned __int128 num = (unsigned __int128)n_prof * sq - sum * sum;   /* P·Σx² − (Σx)² ≥ 0 */
+      double mean = n_prof ? S / P : 0.0;
+      double sd = n_prof ? sqrt((double)num) / P : 0.0;
+      o[0 * O_SLOTS + r] = S;
+      o[1 * O_SLOTS + r] = n_prof ? (double)mn : 0.0;
+      o[2 * O_SLOTS + r] = mean;
+      o[3 * O_SLOTS + r] = (double)mx;
+      o[4 * O_SLOTS + r] = sd;
+      o[5 * O_SLOTS + r] = mean == 0.0 ? 0.0 : sd / mean;
+    }
+  }
 }
 
 /* ======================================================================================

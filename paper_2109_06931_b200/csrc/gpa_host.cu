@@ -341,6 +341,7 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
   UP(s->d_call_inst, ci);
   UP(s->d_call_callee, cc);
   UP(s->d_call_caller, dv.call_caller);
+  UP(s->d_inst_func, dv.inst_func);
   std::vector<uint32_t> order(nc);
   std::iota(order.begin(), order.end(), 0u);
   std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ci[a] < ci[b]; });
@@ -747,6 +748,34 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
     CC(launch_cct_incl_level(c, c->level_start[L], c->level_start[L + 1], st));
 #undef CC
   *out = c;
+  return GPA_OK;
+}
+
+gpa_status gpa_attribute_profiles(gpa_structure s, const gpa_sample *d_samples, uint64_t n, uint32_t n_profiles,
+                                  uint64_t *d_prof_hist, uint64_t *d_prof_unattr, gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (n == 0) return GPA_OK;
+  if (!d_samples || !d_prof_unattr || (!d_prof_hist && s->info.n_func))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer with n=%llu", (unsigned long long)n);
+  if ((uintptr_t)d_samples & 15) return fail(GPA_ERR_INVALID_ARG, "d_samples is not 16-byte aligned");
+  if (n_profiles > 65536) return fail(GPA_ERR_INVALID_ARG, "n_profiles %u > 65536", n_profiles);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
+  CU(launch_attribute_profiles(s->attr, s->d_inst_func, s->info.n_func, d_samples, n, n_profiles,
+                               (unsigned long long *)d_prof_hist, (unsigned long long *)d_prof_unattr,
+                               sm_count(s->device), (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles, double *d_stats,
+                             gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (!s->info.n_func) return GPA_OK;
+  if (!d_prof_hist || !d_stats) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CU(launch_profile_stats(d_prof_hist, n_profiles, s->info.n_func, d_stats, (cudaStream_t)stream));
   return GPA_OK;
 }
 

@@ -55,6 +55,7 @@ struct gpa_structure_s {
   uint64_t *d_inst_addr = nullptr;
   uint16_t *d_inst_len = nullptr;
   uint8_t *d_inst_class = nullptr;
+  uint32_t *d_inst_func = nullptr;  // function of each instruction (per-profile histograms)
   uint32_t *d_gmap = nullptr;
   gpa::RollSet roll[gpa::ROLL_KINDS];
   // call graph (function level)
@@ -111,6 +112,13 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
                                  unsigned long long *d_count, bool exact, cudaStream_t st);
+// per-profile function histograms and cross-profile statistics (k_prof.cu)
+cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, uint32_t n_func,
+                                      const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
+                                      unsigned long long *d_ph, unsigned long long *d_pu, int sm_count,
+                                      cudaStream_t st);
+cudaError_t launch_profile_stats(const uint64_t *d_ph, uint32_t n_prof, uint32_t rows, double *d_stats,
+                                 cudaStream_t st);
 cudaError_t launch_block_counts(uint32_t n_blocks, const uint32_t *d_start, const uint64_t *d_cnt, uint32_t n_inst,
                                 uint64_t *d_hist, cudaStream_t st);
 cudaError_t launch_cct_roots(const gpa_structure_s *s, const uint8_t *d_dag_active, gpa_cct_s *c,

@@ -1,0 +1,164 @@
+// k_prof.cu — f1: per-profile function histograms and cross-profile statistics
+// (§4.5 P:481-487 "sum, min, mean, max, std. deviation, and coefficient of
+// variation"; profiles = GPU streams / ranks / threads; reading R25).
+//
+// k_attr_prof: register streaming (4 records per lane in flight), pc -> instruction through
+//   the granule map (or binary search), -> function, -> (profile, function, slot) bin.  A
+//   warp's records usually share the profile (streams are contiguous) and often the function,
+//   so lanes with equal 64-bit keys are combined (match.any) before one u64 L2 reduction.
+// k_prof_stats: one thread per (function, slot); exact u64 / u128 sums over the profiles,
+//   then one correctly rounded conversion per statistic (bit-identical to the oracle).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gpa_internal.cuh"
+
+namespace gpa {
+namespace {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int kThreads = 256, kUnroll = 4;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <int MODE>
+__device__ __forceinline__ uint32_t lookup(const AttrTables &T, uint64_t pc) {
+  if (MODE == 0) {
+    uint64_t g = (pc - T.base) >> T.gshift;
+    return g < T.n_gran ? __ldg(T.gmap + g) : NONE;
+  } else {
+    if (!(pc >= T.base && pc < T.end)) return NONE;
+    uint32_t lo = 0, hi = T.n_inst;
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(T.inst_addr + mid) <= pc) lo = mid + 1; else hi = mid;
+    }
+    uint32_t j = lo - 1;
+    return pc - __ldg(T.inst_addr + j) < (uint64_t)__ldg(T.inst_len + j) ? j : NONE;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads)
+    k_attr_prof(AttrTables T, const uint32_t *__restrict__ inst_func, uint32_t n_func, const uint4 *__restrict__ rec,
+                uint64_t n, uint32_t n_prof, unsigned long long *__restrict__ PH, unsigned long long *__restrict__ PU) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t base = warp * 32 * kUnroll; base < n; base += nwarps * 32 * kUnroll) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++) {
+      uint64_t k = base + (uint64_t)u * 32 + lane;
+      v[u] = k < n ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t f[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++) {
+      uint32_t i = lookup<MODE>(T, ((uint64_t)v[u].y << 32) | v[u].x);
+      f[u] = i == NONE ? NONE : __ldg(inst_func + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++) {
+      uint64_t k = base + (uint64_t)u * 32 + lane;
+      uint32_t cnt = v[u].z, stall = v[u].w & 0xFFFFu, stream = v[u].w >> 16;
+      uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
+      uint64_t p = stream < n_prof ? stream : n_prof;
+      unsigned long long *target =
+          f[u] == NONE ? PU + (p << 4 | slot) : PH + (((p * n_func + f[u]) << 4) | slot);
+      const bool live = k < n && cnt;
+      unsigned long long key = live ? (unsigned long long)(uintptr_t)target : 0ull;
+      unsigned peers = __match_any_sync(FULL, key);
+      int gmax = __reduce_max_sync(FULL, (unsigned)__popc(peers));
+      unsigned long long total = cnt;
+      if (gmax > 1) {
+        unsigned rest = peers & ~(1u << lane);
+        for (int t = 1; t < gmax; t++) {
+          int src = rest ? __ffs(rest) - 1 : lane;
+          uint32_t x = __shfl_sync(FULL, cnt, src);
+          if (rest) {
+            total += x;
+            rest &= rest - 1;
+          }
+        }
+      }
+      if (live && lane == __ffs(peers) - 1) atomicAdd(target, total);
+    }
+  }
+}
+
+// correctly rounded unsigned 128-bit -> double
+__device__ __forceinline__ double u128_to_double(unsigned __int128 x) {
+  uint64_t hi = (uint64_t)(x >> 64);
+  if (hi == 0) return __ull2double_rn((uint64_t)x);
+  int lz = __clzll((long long)hi);
+  int shift = 64 - lz;                           // bits to drop so the value fits in 64
+  uint64_t m = (uint64_t)(x >> shift);
+  uint64_t sticky = ((x & (((unsigned __int128)1 << shift) - 1)) != 0) ? 1ull : 0ull;
+  return ldexp(__ull2double_rn(m | sticky), shift);
+}
+
+__global__ void k_prof_stats(const uint64_t *__restrict__ PH, uint32_t n_prof, uint32_t rows,
+                             double *__restrict__ out) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < (uint64_t)rows * GPA_SLOTS;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = x >> 4;
+    const int r = (int)(x & 15);
+    unsigned __int128 sum = 0, sq = 0;
+    uint64_t mn = ~0ull, mx = 0;
+    for (uint32_t p = 0; p < n_prof; p++) {
+      uint64_t v = __ldg(PH + ((uint64_t)p * rows + f) * GPA_SLOTS + r);
+      sum += v;
+      sq += (unsigned __int128)v * v;
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+    const double P = __uint2double_rn(n_prof), S = u128_to_double(sum);
+    const unsigned __int128 num = (unsigned __int128)n_prof * sq - sum * sum;  // P·Σx² − (Σx)²
+    const double mean = n_prof ? __ddiv_rn(S, P) : 0.0;
+    const double sd = n_prof ? __ddiv_rn(__dsqrt_rn(u128_to_double(num)), P) : 0.0;
+    double *o = out + f * 6 * GPA_SLOTS;
+    o[0 * GPA_SLOTS + r] = S;
+    o[1 * GPA_SLOTS + r] = n_prof ? __ull2double_rn(mn) : 0.0;
+    o[2 * GPA_SLOTS + r] = mean;
+    o[3 * GPA_SLOTS + r] = __ull2double_rn(mx);
+    o[4 * GPA_SLOTS + r] = sd;
+    o[5 * GPA_SLOTS + r] = mean == 0.0 ? 0.0 : __ddiv_rn(sd, mean);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, uint32_t n_func,
+                                      const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
+                                      unsigned long long *d_ph, unsigned long long *d_pu, int sm_count,
+                                      cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  uint64_t per_block = (uint64_t)kThreads * kUnroll;
+  uint64_t want = (n + per_block - 1) / per_block;
+  uint64_t cap = (uint64_t)sm_count * (2048 / kThreads);
+  unsigned blocks = (unsigned)(want < cap ? want : cap);
+  const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
+  if (T.mode == 0) k_attr_prof<0><<<blocks, kThreads, 0, st>>>(T, d_inst_func, n_func, rec, n, n_prof, d_ph, d_pu);
+  else k_attr_prof<1><<<blocks, kThreads, 0, st>>>(T, d_inst_func, n_func, rec, n, n_prof, d_ph, d_pu);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_profile_stats(const uint64_t *d_ph, uint32_t n_prof, uint32_t rows, double *d_stats,
+                                 cudaStream_t st) {
+  if (!rows) return cudaSuccess;
+  uint64_t blocks = ((uint64_t)rows * GPA_SLOTS + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_prof_stats<<<(unsigned)blocks, 256, 0, st>>>(d_ph, n_prof, rows, d_stats);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace gpa

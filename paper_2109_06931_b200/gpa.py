@@ -16,7 +16,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgpa.so")
 
-SLOTS, VALID_SLOTS, SLOT_INVALID, CLASSES, NUM_DERIVED = 16, 12, 15, 16, 33
+SLOTS, VALID_SLOTS, SLOT_INVALID, CLASSES, NUM_DERIVED, NUM_STATS = 16, 12, 15, 16, 33, 6
 NONE = 0xFFFFFFFF
 SCOPES = {"INST": 0, "LINE": 1, "LOOP": 2, "INLINE": 3, "FUNC": 4, "CCT_EXCL": 5, "CCT_INCL": 6}
 CTX_FUNC, CTX_SCC, CTX_SCC_MEMBER = 0, 1, 2
@@ -78,6 +78,8 @@ def _load():
         "gpa_derive_metrics": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], S),
         "gpa_kernel_launches": ([], ctypes.c_uint64),
         "gpa_block_counts": ([_vp, _u32, _vp, _vp, _vp, _vp], S),
+        "gpa_attribute_profiles": ([_vp, _vp, _u64, _u32, _vp, _vp, _vp], S),
+        "gpa_profile_stats": ([_vp, _vp, _u32, _vp, _vp], S),
         "gpa_set_attr_kernel": ([ctypes.c_int], S),
     }
     for name, (args, res) in sig.items():
@@ -218,6 +220,25 @@ def attribute_samples_host(s: Structure, samples, inst_hist, unattributed, strea
         s.handle, ptr, nb // 16, _ptr(inst_hist, "inst_hist", 128 * s.info["n_inst"]),
         _ptr(unattributed, "unattributed", 128), _stream_ptr(stream, inst_hist.device)),
         "gpa_attribute_samples_host")
+
+
+def attribute_profiles(s: Structure, samples, n_profiles: int, prof_hist, prof_unattr, n: int | None = None,
+                       stream=None) -> None:
+    """f1: per-profile function histograms ((n_profiles+1) x n_func x 16, see gpa.h)."""
+    nb = samples.numel() * samples.element_size()
+    n = nb // 16 if n is None else int(n)
+    rows = int(n_profiles) + 1
+    _check(_lib.gpa_attribute_profiles(
+        s.handle, _ptr(samples, "samples", 16 * n), n, int(n_profiles),
+        _ptr(prof_hist, "prof_hist", 128 * rows * s.info["n_func"]), _ptr(prof_unattr, "prof_unattr", 128 * rows),
+        _stream_ptr(stream, samples.device)), "gpa_attribute_profiles")
+
+
+def profile_stats(s: Structure, prof_hist, n_profiles: int, stats, stream=None) -> None:
+    """f1: sum/min/mean/max/std/cv over profiles per (function, slot) -> stats [n_func, 6, 16]."""
+    _check(_lib.gpa_profile_stats(s.handle, _ptr(prof_hist, "prof_hist"), int(n_profiles),
+                                  _ptr(stats, "stats", 8 * 6 * 16 * s.info["n_func"]),
+                                  _stream_ptr(stream, stats.device)), "gpa_profile_stats")
 
 
 def block_counts(s: Structure, block_start, counts, inst_hist, stream=None) -> None:

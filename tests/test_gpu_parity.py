@@ -346,3 +346,40 @@ def test_attribution_huge_counts_exact(gpa, attr_kernel, kernel):
     Ho, Uo, _ = oracle.attribute(w.structure, rec)
     assert Ho.max() > 2 ** 40
     assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
+
+
+# ---- f1: per-profile histograms + cross-profile statistics --------------------------------------
+@pytest.mark.parametrize("name,records,n_prof", [("C4", 3_000_001, 384), ("C4", 500_000, 100), ("C2", 1_000_000, 1),
+                                                 ("C5", 200_000, 1)])
+def test_profiles_parity(gpa, name, records, n_prof):
+    w = gen.workload(name, records=records)
+    s = gpa.load_structure(w.structure, 0)
+    rec = _device_records(w)
+    nf = s.info["n_func"]
+    PH = torch.zeros((n_prof + 1, nf, 16), dtype=torch.int64, device=DEV)
+    PU = torch.zeros((n_prof + 1, 16), dtype=torch.int64, device=DEV)
+    gpa.attribute_profiles(s, rec, n_prof, PH, PU)
+    stats = torch.empty((nf, 6, 16), dtype=torch.float64, device=DEV)
+    gpa.profile_stats(s, PH, n_prof, stats)
+    torch.cuda.synchronize()
+    Hp, Up = oracle.attribute_profiles(w.structure, w.records_host(), n_prof)
+    assert np.array_equal(u64(PH), Hp) and np.array_equal(u64(PU), Up)
+    So = oracle.profile_stats(Hp, n_prof)
+    got = stats.cpu().numpy()
+    assert np.allclose(got, So, rtol=1e-9, atol=0)
+    assert np.array_equal(got.view(np.uint64), So.view(np.uint64))       # bit-identical
+
+
+def test_profile_stats_huge_values(gpa):
+    """u128 sums of squares and the correctly rounded u128 -> double conversion."""
+    rng = np.random.default_rng(2)
+    n_prof, nf = 7, 25
+    w = gen.workload("C2", records=10)
+    s = gpa.load_structure(w.structure, 0)
+    Hp = rng.integers(0, 2 ** 62, (n_prof + 1, nf, 16)).astype(np.uint64)
+    Hp[:, 0, :] = 2 ** 62 + 12345                                          # equal values: std 0
+    stats = torch.empty((nf, 6, 16), dtype=torch.float64, device=DEV)
+    gpa.profile_stats(s, torch.from_numpy(Hp.view(np.int64)).to(DEV), n_prof, stats)
+    So = oracle.profile_stats(Hp, n_prof)
+    assert np.array_equal(stats.cpu().numpy().view(np.uint64), So.view(np.uint64))
+    assert (So[0, 4] == 0).all()
