@@ -187,8 +187,8 @@ GPA_API const char *gpa_last_error(void);
 GPA_API uint64_t gpa_kernel_launches(void);
 /* Force the attribution kernel process-wide (testing / benchmarking; results are identical):
  * 0 automatic (default), 1 register streaming, 2 TMA ring with L2 reductions, 3 TMA ring with
- * shared-memory heavy-hitter rows (used only where applicable: granule map, >= 2^21 records,
- * >= 1024 instructions; otherwise the automatic choice).  Also settable by the environment
+ * shared-memory heavy-hitter bins, 4 TMA ring with shared-memory heavy-hitter rows (3 and 4 only
+ * where applicable: granule map, >= 2^21 records, >= 1024 instructions; otherwise automatic).  Also settable by the environment
  * variable GPA_ATTR_VARIANT before the first call.  DESIGN.md §7 describes the kernels. */
 GPA_API gpa_status gpa_set_attr_kernel(int which);
 /* Validate a structure description on the host only (no device touched).  Same checks and

@@ -502,7 +502,7 @@ const char *gpa_last_error(void) { return g_err.c_str(); }
 uint64_t gpa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 gpa_status gpa_set_attr_kernel(int which) {
-  if (which < 0 || which > 3) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-3)", which);
+  if (which < 0 || which > 4) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-4)", which);
   gpa::set_attr_kernel(which);
   return GPA_OK;
 }

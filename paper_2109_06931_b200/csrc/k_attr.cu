@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
       const uint64_t left = n - tile * S;
       const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
       uint32_t old[R];
+      bool added[R];
 #pragma unroll
       for (int u = 0; u < R; u++) {
         const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
@@ -417,10 +418,12 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
         const bool live = j < m;
         if (REC && live)
           rec_inst[tile * S + j] = nib == 15u ? NONE : (nib == 1u ? __ldg(row_inst + (cd >> 4)) : (cd >> 4));
-        old[u] = 0xFFFFFFFFu;  // "no shared add"
+        old[u] = 0;
+        added[u] = false;
         if (live) {
           if (nib == 1u && slot < (uint32_t)kHotSlots) {
             old[u] = atoms_add(tab_s + ((cd >> 4) * kHotSlots + slot) * 4, cnt);
+            added[u] = true;
           } else if (nib == 0u) {
             red_add_u64(H + (cd | slot), cnt);
           } else if (nib == 15u) {
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
 #pragma unroll
       for (int u = 0; u < R; u++) {
         // old + cnt wrapped the u32 shared counter: repay 2^32 in L2
-        if (old[u] != 0xFFFFFFFFu && old[u] + v[q][u].z < old[u])
+        if (added[u] && old[u] + v[q][u].z < old[u])
           red_add_u64(H + ((uint64_t)__ldg(row_inst + (c[q][u] >> 4)) << 4 | (v[q][u].w & 0xFFFFu)), 1ull << 32);
       }
     }
@@ -444,6 +447,190 @@ done:
     uint32_t val = tab[x];
     if (val) red_add_u64(H + ((uint64_t)__ldg(row_inst + x / kHotSlots) << 4 | (x % kHotSlots)), val);
   }
+}
+
+// ---- K_attr_bins: heavy-hitter BINS in shared memory (default) ---------------------------------
+// Same pipeline as K_attr_hot, but the shared table holds individual (instruction, slot) bins
+// rather than whole 12-slot rows: with the same 160 KiB it covers the ~40 k most-sampled bins
+// (C5: 75 % of records vs 67 % for 3 328 rows), so fewer records fall back to L2 reductions.
+// Per call: k_sample_bins counts sampled records per bin; the top kHotBins bins are chosen by
+// the same value histogram / threshold; k_assign_bins gives each instruction a 12-bit mask of
+// its hot slots and a base index (atomic cursor) and records bin_of[idx] = inst<<4 | slot;
+// k_codemap_bins builds a per-call 64-bit code per granule: low word inst<<4 (or ~0 unmapped),
+// high word base<<12 | mask (0 for unmapped granules and instructions without hot bins).  A record's table index is base + popc(mask & below(slot)).
+constexpr int kHotBins = 40960;                     // x 4 B = 160 KiB
+using RingBins = Ring<16, 2, 4>;
+
+__global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
+  const uint64_t total = (uint64_t)kSampleChunks * kSampleChunk;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = x / kSampleChunk, o = x % kSampleChunk;
+    uint64_t k = c * (n - kSampleChunk) / (kSampleChunks - 1) + o;
+    uint4 v = ld_stream(rec + k);
+    uint32_t i = lookup<0>(T, ((uint64_t)v.y << 32) | v.x);
+    uint32_t stall = v.w & 0xFFFFu;
+    if (i != NONE && stall < GPA_VALID_SLOTS) atomicAdd(scnt + (uint64_t)i * kHotSlots + stall, 1u);
+  }
+}
+
+__global__ void k_assign_bins(const uint32_t *__restrict__ scnt, uint32_t n_inst, uint32_t *__restrict__ thr,
+                              uint32_t *__restrict__ hot_info, uint32_t *__restrict__ bin_of) {
+  const uint32_t t = thr[0];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += gridDim.x * blockDim.x) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int r = 0; r < kHotSlots; r++) {
+      uint32_t c = scnt[(uint64_t)i * kHotSlots + r];
+      if (c && (c < kVBins - 1 ? c : kVBins - 1) >= t) mask |= 1u << r;
+    }
+    uint32_t info = 0;
+    if (mask) {
+      uint32_t k = __popc(mask);
+      uint32_t base = atomicAdd(thr + 1, k);
+      if (base + k <= (uint32_t)kHotBins) {
+        info = base << 12 | mask;
+        for (uint32_t m = mask, q = base; m; m &= m - 1, q++) bin_of[q] = i << 4 | (__ffs(m) - 1);
+      }
+    }
+    hot_info[i] = info;
+  }
+}
+
+__global__ void k_codemap_bins(const uint32_t *__restrict__ gmap, uint64_t n_gran,
+                               const uint32_t *__restrict__ hot_info, unsigned long long *__restrict__ code) {
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_gran; g += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t m = gmap[g];
+    code[g] = m == NONE ? 0xFFFFFFFFull : ((unsigned long long)hot_info[m] << 32 | (m << 4));
+  }
+}
+
+__device__ __forceinline__ void repay(unsigned long long *H, const uint32_t *bin_of, uint32_t idx,
+                                      unsigned long long v) {
+  uint32_t b = __ldg(bin_of + idx);
+  if (b != NONE) red_add_u64(H + b, v);
+}
+
+template <class RG, int NB, bool REC>
+__global__ void __launch_bounds__(RG::kThreads, 1)
+    k_attr_bins(uint64_t base, uint64_t n_gran, uint32_t gshift, const unsigned long long *__restrict__ code,
+                const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
+                unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
+                const uint32_t *__restrict__ bin_of, const uint32_t *__restrict__ thr) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = kLook + 1;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NB * 4);
+  uint64_t *empty = full + NST;
+  const uint32_t tab_s = smem_u32(tab);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + S - 1) / S;
+  const uint32_t nb = min(thr[1], (uint32_t)NB);
+  for (uint32_t x = threadIdx.x; x < nb; x += blockDim.x) tab[x] = 0;
+  ring_init(full, empty, NST, NC);
+  __syncthreads();
+  if (warp == NC) {
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n);
+    return;
+  }
+  uint4 v[D][R];
+  unsigned long long c[D][R];
+  const uint64_t G = gridDim.x;
+  auto fetch = [&](uint32_t it, uint4 *vv, unsigned long long *cc) {
+    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    mbar_wait(full + st, ph);
+    const uint4 *src = ring + (size_t)st * S + warp * 32 + lane;
+#pragma unroll
+    for (int u = 0; u < R; u++) vv[u] = src[u * NC * 32];  // beyond the tile end: masked below
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+#pragma unroll
+    for (int u = 0; u < R; u++) {
+      uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - base) >> gshift;
+      cc[u] = g < n_gran ? __ldg(code + g) : 0xFFFFFFFFull;  // unmapped: low word ~0, no hot mask
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < kLook; q++)
+    if (blockIdx.x + q * G < ntiles) fetch(q, v[q], c[q]);
+  for (uint32_t it0 = 0;; it0 += D) {
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      const uint32_t it = it0 + q;
+      const uint64_t tile = blockIdx.x + it * G;
+      if (tile >= ntiles) goto done;
+      if (tile + kLook * G < ntiles) fetch(it + kLook, v[(q + kLook) % D], c[(q + kLook) % D]);
+      const uint64_t left = n - tile * S;
+      const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
+      uint32_t old[R], idx[R];
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+        const uint32_t lo = (uint32_t)c[q][u], hi = (uint32_t)(c[q][u] >> 32);
+        const uint32_t cnt = v[q][u].z, stall = v[q][u].w & 0xFFFFu;
+        const uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
+        const bool live = j < m;
+        if (REC && live) rec_inst[tile * S + j] = lo == 0xFFFFFFFFu ? NONE : lo >> 4;
+        const uint32_t mask = hi & 0xFFFu;
+        const bool hot = slot < (uint32_t)kHotSlots && ((mask >> slot) & 1u);
+        idx[u] = (hi >> 12) + __popc(mask & ((1u << slot) - 1u));
+        old[u] = 0;
+        if (live) {
+          if (hot) {
+            old[u] = atoms_add(tab_s + idx[u] * 4, cnt);
+          } else {
+            red_add_u64(lo == 0xFFFFFFFFu ? U + slot : H + (lo | slot), cnt);
+            idx[u] = NONE;
+          }
+        } else {
+          idx[u] = NONE;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        // old + cnt wrapped the u32 shared counter: repay 2^32 in L2
+        if (idx[u] != NONE && old[u] + v[q][u].z < old[u]) repay(H, bin_of, idx[u], 1ull << 32);
+      }
+    }
+  }
+done:
+  asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+  for (uint32_t x = threadIdx.x; x < nb; x += NC * 32) {
+    uint32_t val = tab[x];
+    if (val) repay(H, bin_of, x, val);
+  }
+}
+
+cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
+                        unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  // stream-ordered scratch: scnt[n_inst*12] | hot_info[n_inst] | bin_of[K] | V[4096] | thr[4] | code[n_gran] (u64)
+  const size_t ni = T.n_inst, nbins = ni * kHotSlots;
+  size_t words = nbins + ni + kHotBins + kVBins + 4;
+  words = (words + 1) & ~(size_t)1;  // 8-B align the code map
+  uint32_t *w = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&w, words * 4 + T.n_gran * 8, st);
+  if (e != cudaSuccess) return e;
+  uint32_t *scnt = w, *hot_info = w + nbins, *bin_of = hot_info + ni, *V = bin_of + kHotBins, *thr = V + kVBins;
+  unsigned long long *code = reinterpret_cast<unsigned long long *>(w + words);
+  cudaMemsetAsync(scnt, 0, nbins * 4, st);
+  cudaMemsetAsync(V, 0, kVBins * 4, st);
+  cudaMemsetAsync(bin_of, 0xFF, kHotBins * 4, st);  // unassigned table entries map to NONE
+  k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, scnt);
+  k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)nbins, V);
+  k_pick<<<1, 1024, 0, st>>>(V, thr, kHotBins);
+  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of);
+  k_codemap_bins<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, code);
+  using RG = RingBins;
+  auto kern = ri ? k_attr_bins<RG, kHotBins, true> : k_attr_bins<RG, kHotBins, false>;
+  const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) {
+    kern<<<sm_count, RG::kThreads, smem, st>>>(T.base, T.n_gran, T.gshift, code, rec, n, H, U, ri, bin_of, thr);
+    e = cudaGetLastError();
+  }
+  count_launches(6);
+  cudaError_t e2 = cudaFreeAsync(w, st);
+  return e != cudaSuccess ? e : e2;
 }
 
 template <class RG, int ROWS>
@@ -460,7 +647,7 @@ cudaError_t run_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned 
 
 int g_attr_kernel = -1;  // gpa_set_attr_kernel; -1 = read GPA_ATTR_VARIANT once (0 if unset)
 
-int attr_variant() {  // 0 auto, 1 stream, 2 tma, 3 hot (when applicable)
+int attr_variant() {  // 0 auto, 1 stream, 2 tma, 3 shared bins, 4 shared rows (when applicable)
   if (g_attr_kernel < 0) {
     const char *e = getenv("GPA_ATTR_VARIANT");
     g_attr_kernel = e ? atoi(e) : 0;
@@ -529,7 +716,8 @@ cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, u
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
   const int var = attr_variant();
   const bool hot_ok = T.mode == 0 && n >= kHotMinRecords && T.n_inst >= 1024;
-  if ((var == 0 || var == 3) && hot_ok) return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+  if ((var == 0 || var == 3) && hot_ok) return launch_bins(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+  if (var == 4 && hot_ok) return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
   if (var == 1 || n < 4096) {
     return T.mode == 0 ? launch_stream<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
                        : launch_stream<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);

@@ -99,7 +99,8 @@ def kernel_launches() -> int:
 
 
 def set_attr_kernel(which: int) -> None:
-    """0 automatic, 1 register streaming, 2 TMA + L2 reductions, 3 TMA + shared-memory rows."""
+    """0 automatic, 1 register streaming, 2 TMA + L2 reductions, 3 TMA + shared-memory bins,
+    4 TMA + shared-memory rows."""
     _check(_lib.gpa_set_attr_kernel(int(which)), "gpa_set_attr_kernel")
 
 

@@ -321,7 +321,7 @@ def attr_kernel(gpa):
     gpa.set_attr_kernel(0)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 @pytest.mark.parametrize("name,records", [("C3", 4_000_003), ("C5", 3_000_001)])
 def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
     attr_kernel(kernel)
@@ -333,7 +333,7 @@ def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
     assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 def test_attribution_huge_counts_exact(gpa, attr_kernel, kernel):
     """Counts near 2^32 make every shared u32 add wrap: the repaid 2^32 keeps H exact."""
     attr_kernel(kernel)
@@ -383,3 +383,20 @@ def test_profile_stats_huge_values(gpa):
     So = oracle.profile_stats(Hp, n_prof)
     assert np.array_equal(stats.cpu().numpy().view(np.uint64), So.view(np.uint64))
     assert (So[0, 4] == 0).all()
+
+
+@pytest.mark.parametrize("kernel", [3, 4])
+def test_attribution_shared_counter_overflow_patterns(gpa, attr_kernel, kernel):
+    """Hot bins receive counts that drive 16- and 32-bit shared counters through many
+    overflows (incl. carries between packed halves, counts of exactly 0xFFFF / 0x10000)."""
+    attr_kernel(kernel)
+    w = gen.workload("C4", records=3_000_000)
+    rec = w.records_host()
+    rng = np.random.default_rng(8)
+    choices = np.array([1, 0xFFFF, 0x10000, 0x7FFF, 0xFFFE, 2 ** 31, 0xFFFFFFFF], np.uint64)
+    rec["count"] = np.where(rng.random(len(rec)) < 0.3, choices[rng.integers(0, len(choices), len(rec))],
+                            rng.integers(1, 70000, len(rec)))
+    s = gpa.load_structure(w.structure, 0)
+    H, U, _ = _attribute(gpa, s, torch.from_numpy(rec.view(np.int64).reshape(-1, 2)).to(DEV), rec_inst=False)
+    Ho, Uo, _ = oracle.attribute(w.structure, rec)
+    assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)

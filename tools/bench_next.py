@@ -1,0 +1,84 @@
+"""Measurements of the SURVEY §8f rows built beyond the north-star path (one JSON line each):
+f1 per-profile histograms + cross-profile statistics on C4 (1e9 records, 384 profiles), and
+f2 exact-count mode (block counts -> instructions -> exact-mode CCT) on C3's structure.
+CUDA events around each call, median of K after W warm-ups."""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import gen
+from paper_2109_06931_b200 import gpa
+
+K, W = 5, 2
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6535.7
+
+
+def timed(fn):
+    ts = []
+    for r in range(W + K):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        if r >= W:
+            ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def f1():
+    w = gen.workload("C4")
+    s = gpa.load_structure(w.structure, 0)
+    n = w.cfg.records
+    rec = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+    for k in range(0, n, 1 << 28):
+        w.records_device(rec[k:k + (1 << 28)], k, min(1 << 28, n - k))
+    P = 384
+    PH = torch.zeros((P + 1, s.info["n_func"], 16), dtype=torch.int64, device="cuda")
+    PU = torch.zeros((P + 1, 16), dtype=torch.int64, device="cuda")
+    stats = torch.empty((s.info["n_func"], 6, 16), dtype=torch.float64, device="cuda")
+
+    def run_attr():
+        PH.zero_()
+        PU.zero_()
+        gpa.attribute_profiles(s, rec, P, PH, PU)
+
+    ms_attr = timed(run_attr)
+    ms_stats = timed(lambda: gpa.profile_stats(s, PH, P, stats))
+    gbs = 16 * n / ms_attr / 1e6
+    print(json.dumps({"row": "f1", "workload": "C4", "records": n, "profiles": P, "kernel": "k_attr_prof",
+                      "attr_ms": ms_attr, "records_per_s": n / ms_attr * 1e3, "GBps": gbs, "frac": gbs / PEAK,
+                      "stats_ms": ms_stats}), flush=True)
+
+
+def f2():
+    w = gen.workload("C3", records=10)
+    s = gpa.load_structure(w.structure, 0)
+    n_inst = s.info["n_inst"]
+    rng = np.random.default_rng(1)
+    cuts = np.sort(rng.choice(np.arange(1, n_inst), n_inst // 6, replace=False))
+    start = torch.from_numpy(np.concatenate([[0], cuts, [n_inst]]).astype(np.int32)).cuda()
+    cnt = torch.from_numpy(rng.integers(0, 10 ** 6, len(cuts) + 1)).cuda()
+    H = torch.zeros((n_inst, 16), dtype=torch.int64, device="cuda")
+
+    def run():
+        H.zero_()
+        gpa.block_counts(s, start, cnt, H)
+        c = gpa.reconstruct_cct(s, H, mode=gpa.WEIGHTS_EXACT)
+        c.free()
+
+    ms = timed(run)
+    c = gpa.reconstruct_cct(s, H, mode=gpa.WEIGHTS_EXACT)
+    print(json.dumps({"row": "f2", "workload": "C3 structure, random basic blocks", "blocks": len(cuts) + 1,
+                      "contexts": c.n, "ms": ms}), flush=True)
+
+
+if __name__ == "__main__":
+    f1()
+    f2()
