@@ -129,7 +129,7 @@ def cpu_baseline(w, target_s: float = 12.0):
     """The oracle on the GPU box's host cores over a bounded prefix of the same workload,
     sized (after a calibration pass) for about target_s seconds of timed CPU work."""
     cores = len(os.sched_getaffinity(0))
-    n = 1 << 24
+    n = 1 << 26
     t, ta, tr, _ = oracle_pass(w, n, 0, cores)
     per_rec = ta / n
     n = int(min(w.cfg.records, max(n, (target_s - tr) / max(per_rec, 1e-12))))
@@ -328,7 +328,7 @@ def run_gpa(args):
                        "parallelism": f"record shards x{world}, NCCL reduce of H||U",
                        "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_attr_hot",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_attr_bins",
                          "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
             "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:

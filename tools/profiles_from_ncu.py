@@ -82,5 +82,6 @@ if __name__ == "__main__":
     algo = int(sys.argv[5]) if len(sys.argv) > 5 else 64_000_000_000
     P = os.path.join(ROOT, "profiles")
     tot, s = launches(lcsv, os.path.join(P, f"{rnd}_launches_{cfg}.md"))
-    js = full(rep, os.path.join(P, f"{rnd}_k_attr_hot_{cfg}.md"), os.path.join(P, f"k_attr_traffic_{cfg}.json"), algo)
+    kname = sys.argv[6] if len(sys.argv) > 6 else "k_attr_bins"
+    js = full(rep, os.path.join(P, f"{rnd}_{kname}_{cfg}.md"), os.path.join(P, f"k_attr_traffic_{cfg}.json"), algo)
     print(json.dumps(js))
