@@ -262,6 +262,8 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
       UP(s->d_gmap, gmap);
       T.gmap = s->d_gmap;
       T.mode = 0;
+      for (auto &x : gmap) x = x == NONE ? NONE : dv.inst_func[x];  // granule -> function
+      UP(s->d_gfunc, gmap);
     }
   } else {
     T.base = 1;
@@ -762,7 +764,7 @@ gpa_status gpa_attribute_profiles(gpa_structure s, const gpa_sample *d_samples, 
   DeviceGuard g(s->device);
   CU(g.err);
   CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
-  CU(launch_attribute_profiles(s->attr, s->d_inst_func, s->info.n_func, d_samples, n, n_profiles,
+  CU(launch_attribute_profiles(s->attr, s->d_inst_func, s->d_gfunc, s->info.n_func, d_samples, n, n_profiles,
                                (unsigned long long *)d_prof_hist, (unsigned long long *)d_prof_unattr,
                                sm_count(s->device), (cudaStream_t)stream));
   return GPA_OK;

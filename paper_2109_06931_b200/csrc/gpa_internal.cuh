@@ -56,6 +56,7 @@ struct gpa_structure_s {
   uint16_t *d_inst_len = nullptr;
   uint8_t *d_inst_class = nullptr;
   uint32_t *d_inst_func = nullptr;  // function of each instruction (per-profile histograms)
+  uint32_t *d_gfunc = nullptr;      // function of each granule of the pc map (NONE in gaps)
   uint32_t *d_gmap = nullptr;
   gpa::RollSet roll[gpa::ROLL_KINDS];
   // call graph (function level)
@@ -113,7 +114,8 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
                                  unsigned long long *d_count, bool exact, cudaStream_t st);
 // per-profile function histograms and cross-profile statistics (k_prof.cu)
-cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, uint32_t n_func,
+cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, const uint32_t *d_gfunc,
+                                      uint32_t n_func,
                                       const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
                                       unsigned long long *d_ph, unsigned long long *d_pu, int sm_count,
                                       cudaStream_t st);

@@ -28,61 +28,12 @@
 #include <stdlib.h>
 
 #include "gpa_internal.cuh"
+#include "kern_common.cuh"
 
 namespace gpa {
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
-
-// ---- device helpers ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
-  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ uint32_t atoms_add(uint32_t saddr, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
-  return old;
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity), "r"(0x989680u)
-      : "memory");
-}
-// 1-D bulk copy global -> shared through the TMA engine, completion counted on `bar`
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
 
 // pc -> instruction: granule map (MODE 0) or binary search over the sorted starts (MODE 1)
 template <int MODE>
@@ -160,45 +111,6 @@ __global__ void __launch_bounds__(kStreamThreads)
   }
 }
 
-// ---- TMA ring geometry ----------------------------------------------------------------------------
-template <int NC, int R, int NST>
-struct Ring {
-  static constexpr int kConsumers = NC, kPerLane = R, kStages = NST;
-  static constexpr int kTile = NC * 32 * R;  // records per stage
-  static constexpr size_t kBytes = (size_t)NST * kTile * 16;
-  static constexpr int kThreads = (NC + 1) * 32;
-  static_assert((NST & (NST - 1)) == 0, "stages must be a power of two");
-};
-
-// producer warp body: one elected lane drives the bulk-copy engine over this CTA's tiles
-template <class RG>
-__device__ __forceinline__ void ring_produce(uint4 *ring, uint64_t *full, uint64_t *empty, const uint4 *rec,
-                                             uint64_t n) {
-  constexpr int S = RG::kTile, NST = RG::kStages;
-  const uint64_t ntiles = (n + S - 1) / S;
-  uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-  uint32_t it = 0;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
-    if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
-    uint64_t left = n - tile * S;
-    uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);
-    mbar_arrive_expect_tx(full + st, bytes);
-    bulk_g2s(ring + (size_t)st * S, rec + tile * S, bytes, full + st, policy);
-  }
-}
-
-__device__ __forceinline__ void ring_init(uint64_t *full, uint64_t *empty, int nst, uint32_t consumers) {
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < nst; q++) {
-      mbar_init(full + q, 1);
-      mbar_init(empty + q, consumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-}
-
 // ---- K_attr_tma: TMA ring + warp-aggregated L2 reductions ----------------------------------------
 using RingTma = Ring<16, 4, 4>;
 
@@ -216,7 +128,7 @@ __global__ void __launch_bounds__(RingTma::kThreads, 1)
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n);
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, (n + RG::kTile - 1) / RG::kTile);
     return;
   }
   const uint64_t ntiles = (n + S - 1) / S;
@@ -375,7 +287,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n);
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, (n + RG::kTile - 1) / RG::kTile);
     return;
   }
   uint4 v[D][R];
@@ -530,7 +442,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n);
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, (n + RG::kTile - 1) / RG::kTile);
     return;
   }
   uint4 v[D][R];

@@ -2,6 +2,7 @@
 // (§4.5 P:481-487 "sum, min, mean, max, std. deviation, and coefficient of
 // variation"; profiles = GPU streams / ranks / threads; reading R25).
 //
+// k_attr_prof_tma (granule map): see below.
 // k_attr_prof: register streaming (4 records per lane in flight), pc -> instruction through
 //   the granule map (or binary search), -> function, -> (profile, function, slot) bin.  A
 //   warp's records usually share the profile (streams are contiguous) and often the function,
@@ -12,20 +13,13 @@
 #include <stdint.h>
 
 #include "gpa_internal.cuh"
+#include "kern_common.cuh"
 
 namespace gpa {
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int kThreads = 256, kUnroll = 4;
-
-__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
 
 template <int MODE>
 __device__ __forceinline__ uint32_t lookup(const AttrTables &T, uint64_t pc) {
@@ -93,6 +87,113 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// k_attr_prof_tma: the TMA-fed variant used with the granule map.  Each CTA takes a contiguous
+// range of record tiles; streams are contiguous in the input (one profile's records follow
+// each other), so a CTA meets only a few profiles.  Its shared memory holds u32 counters for
+// K "profile lanes" x n_func functions x 12 slots, lane k = profile p_first + k where p_first
+// is the profile of the CTA's first record; other records, unattributed ones and invalid
+// stalls go straight to L2.  One gather (granule -> function, built at load) per record.
+constexpr int kProfTab = 160 * 1024;  // bytes of shared counters
+using RingProf = Ring<16, 2, 4>;
+constexpr int kProfLook = 2;
+
+template <class RG>
+__global__ void __launch_bounds__(RG::kThreads, 1)
+    k_attr_prof_tma(AttrTables T, const uint32_t *__restrict__ gfunc, uint32_t n_func, const uint4 *__restrict__ rec,
+                    uint64_t n, uint32_t n_prof, uint32_t K, unsigned long long *__restrict__ PH,
+                    unsigned long long *__restrict__ PU) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = kProfLook + 1;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes);
+  uint64_t *empty = full + NST;
+  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes + 2 * NST * 8);
+  const uint32_t tab_s = smem_u32(tab);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + S - 1) / S;
+  const uint64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t nt = K * n_func * GPA_VALID_SLOTS;
+  for (uint32_t x = threadIdx.x; x < nt; x += blockDim.x) tab[x] = 0;
+  uint32_t pf = 0;
+  if (t0 < t1) {
+    uint32_t s0 = __ldg(reinterpret_cast<const uint32_t *>(rec + t0 * S) + 3) >> 16;
+    pf = s0 < n_prof ? s0 : n_prof;
+  }
+  ring_init(full, empty, NST, NC);
+  __syncthreads();
+  if (warp == NC) {
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, t0, 1, t1);
+    return;
+  }
+  uint4 v[D][R];
+  uint32_t c[D][R];
+  auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *cc) {
+    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    mbar_wait(full + st, ph);
+    const uint4 *src = ring + (size_t)st * S + warp * 32 + lane;
+#pragma unroll
+    for (int u = 0; u < R; u++) vv[u] = src[u * NC * 32];  // beyond the tile end: masked below
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+#pragma unroll
+    for (int u = 0; u < R; u++) {
+      uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - T.base) >> T.gshift;
+      cc[u] = g < T.n_gran ? __ldg(gfunc + g) : NONE;
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < kProfLook; q++)
+    if (t0 + q < t1) fetch(q, v[q], c[q]);
+  for (uint32_t it0 = 0;; it0 += D) {
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      const uint32_t it = it0 + q;
+      const uint64_t tile = t0 + it;
+      if (tile >= t1) goto done;
+      if (tile + kProfLook < t1) fetch(it + kProfLook, v[(q + kProfLook) % D], c[(q + kProfLook) % D]);
+      const uint64_t left = n - tile * S;
+      const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
+      uint32_t old[R], idx[R];
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+        const uint32_t f = c[q][u], cnt = v[q][u].z, stall = v[q][u].w & 0xFFFFu, sid = v[q][u].w >> 16;
+        const uint32_t slot = stall < GPA_VALID_SLOTS ? stall : GPA_SLOT_INVALID;
+        const uint32_t p = sid < n_prof ? sid : n_prof;
+        const uint32_t k = p - pf;  // profile lane (wraps to a huge value below pf)
+        idx[u] = NONE;
+        old[u] = 0;
+        if (j < m) {
+          if (f != NONE && slot < (uint32_t)GPA_VALID_SLOTS && k < K) {
+            idx[u] = (k * n_func + f) * GPA_VALID_SLOTS + slot;
+            old[u] = atoms_add(tab_s + idx[u] * 4, cnt);
+          } else if (f == NONE) {
+            red_add_u64(PU + ((uint64_t)p << 4 | slot), cnt);
+          } else {
+            red_add_u64(PH + (((uint64_t)p * n_func + f) << 4 | slot), cnt);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        if (idx[u] != NONE && old[u] + v[q][u].z < old[u]) {  // u32 wrap: repay 2^32 in L2
+          uint32_t x = idx[u], slot = x % GPA_VALID_SLOTS, kf = x / GPA_VALID_SLOTS;
+          red_add_u64(PH + (((uint64_t)(pf + kf / n_func) * n_func + kf % n_func) << 4 | slot), 1ull << 32);
+        }
+      }
+    }
+  }
+done:
+  asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+  for (uint32_t x = threadIdx.x; x < nt; x += NC * 32) {
+    uint32_t val = tab[x];
+    if (val) {
+      uint32_t slot = x % GPA_VALID_SLOTS, kf = x / GPA_VALID_SLOTS;
+      red_add_u64(PH + (((uint64_t)(pf + kf / n_func) * n_func + kf % n_func) << 4 | slot), val);
+    }
+  }
+}
+
 // correctly rounded unsigned 128-bit -> double
 __device__ __forceinline__ double u128_to_double(unsigned __int128 x) {
   uint64_t hi = (uint64_t)(x >> 64);
@@ -135,11 +236,25 @@ __global__ void k_prof_stats(const uint64_t *__restrict__ PH, uint32_t n_prof, u
 
 }  // namespace
 
-cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, uint32_t n_func,
-                                      const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
+cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, const uint32_t *d_gfunc,
+                                      uint32_t n_func, const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
                                       unsigned long long *d_ph, unsigned long long *d_pu, int sm_count,
                                       cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  const uint32_t K0 = n_func ? (uint32_t)(kProfTab / ((size_t)n_func * GPA_VALID_SLOTS * 4)) : 0;
+  if (T.mode == 0 && n >= 4096 && K0 >= 1) {  // else: register streaming with warp aggregation
+    using RG = RingProf;
+    const uint32_t K = K0 > 16 ? 16 : K0;
+    const size_t smem = RG::kBytes + 2 * RG::kStages * 8 + (size_t)K * n_func * GPA_VALID_SLOTS * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_attr_prof_tma<RG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    uint64_t ntiles = (n + RG::kTile - 1) / RG::kTile;
+    unsigned blocks = (unsigned)(ntiles < (uint64_t)sm_count ? ntiles : (uint64_t)sm_count);
+    k_attr_prof_tma<RG><<<blocks, RG::kThreads, smem, st>>>(T, d_gfunc, n_func, reinterpret_cast<const uint4 *>(d_samples),
+                                                          n, n_prof, K, d_ph, d_pu);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   uint64_t per_block = (uint64_t)kThreads * kUnroll;
   uint64_t want = (n + per_block - 1) / per_block;
   uint64_t cap = (uint64_t)sm_count * (2048 / kThreads);
