@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -24,6 +25,29 @@ static thread_local std::string g_err;
 static std::atomic<unsigned long long> g_launches{0};
 
 void gpa::count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, st);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) return e;
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pools[dev], st);
+}
 
 static gpa_status fail(gpa_status st, const char *fmt, ...) {
   char buf[512];
@@ -492,7 +516,7 @@ static void free_cct(gpa_cct_s *c) {
 template <class T>
 static cudaError_t calloc_dev(gpa_cct_s *c, T **p, size_t n) {
   *p = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)p, sizeof(T) * (n ? n : 1), c->stream);
+  cudaError_t e = pool_alloc((void **)p, sizeof(T) * (n ? n : 1), c->stream);
   if (e == cudaSuccess) c->allocs.push_back(*p);
   return e;
 }
@@ -725,6 +749,24 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   uint32_t *d_tmp = nullptr, *d_bs = nullptr;
   CC(calloc_dev(c, &d_tmp, n + 1));
   CC(calloc_dev(c, &d_bs, 65536));
+  {  // one cooperative launch walks every level (falls back to per-level launches if refused)
+    const uint32_t max_lev = 2 * I.dag_levels + 4;
+    uint32_t *d_lev = nullptr;
+    CC(calloc_dev(c, &d_lev, max_lev + 2));
+    cudaError_t e = launch_cct_coop(s, c, d_tmp, d_bs, d_lev, max_lev, d_cnt + 1, sm_count(s->device), st);
+    if (e == cudaSuccess) {
+      CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      CC(cudaStreamSynchronize(st));
+      if (h_cnt[1] != n) {
+        free_cct(c);
+        return fail(GPA_ERR_INTERNAL, "cooperative BFS built %llu contexts, path count said %llu", h_cnt[1],
+                    (unsigned long long)n);
+      }
+      *out = c;
+      return GPA_OK;
+    }
+    cudaGetLastError();
+  }
   // Step 4: breadth-first split of the DAG into the tree, level by level
   CC(launch_cct_roots(s, c->dag_active, c, d_cnt + 1, st));
   CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));

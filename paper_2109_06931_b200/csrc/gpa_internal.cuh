@@ -93,6 +93,10 @@ struct gpa_cct_s {
 namespace gpa {
 void count_launches(uint64_t k);
 void set_attr_kernel(int which);
+// Stream-ordered scratch from the library's own memory pool on the current device (release
+// threshold = unlimited, so memory freed at one call is reused by the next without going
+// back to the driver; the process's default pool is left untouched).
+cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 }
 
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------
@@ -131,6 +135,9 @@ cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a,
 cudaError_t launch_cct_excl(const gpa_structure_s *s, gpa_cct_s *c, cudaStream_t st);
 // whole Step 4 in one CTA when cct_small_ok (writes the built context count to *d_built)
 bool cct_small_ok(const gpa_structure_s *s, uint64_t n);
+// whole Step 4 in one cooperative grid launch (large trees); d_bsum >= 2*SMs entries
+cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_tmp, uint32_t *d_bsum, uint32_t *d_lev,
+                            uint32_t max_lev, unsigned long long *d_built, int sm_count, cudaStream_t st);
 cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, unsigned long long *d_built, cudaStream_t st);
 cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStream_t st);
 }  // namespace gpa

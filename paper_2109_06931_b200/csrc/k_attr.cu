@@ -520,7 +520,7 @@ cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsig
   size_t words = nbins + ni + kHotBins + kVBins + 4;
   words = (words + 1) & ~(size_t)1;  // 8-B align the code map
   uint32_t *w = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&w, words * 4 + T.n_gran * 8, st);
+  cudaError_t e = pool_alloc((void **)&w, words * 4 + T.n_gran * 8, st);
   if (e != cudaSuccess) return e;
   uint32_t *scnt = w, *hot_info = w + nbins, *bin_of = hot_info + ni, *V = bin_of + kHotBins, *thr = V + kVBins;
   unsigned long long *code = reinterpret_cast<unsigned long long *>(w + words);
@@ -573,7 +573,7 @@ cudaError_t launch_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsign
   size_t ni = T.n_inst;
   size_t words = 2 * ni + kHotRows + kVBins + 4 + T.n_gran;
   uint32_t *w = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&w, words * 4, st);
+  cudaError_t e = pool_alloc((void **)&w, words * 4, st);
   if (e != cudaSuccess) return e;
   uint32_t *scnt = w, *hot_row = w + ni, *row_inst = hot_row + ni, *V = row_inst + kHotRows, *thr = V + kVBins,
            *code = thr + 4;

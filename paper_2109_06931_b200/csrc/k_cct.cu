@@ -13,6 +13,7 @@
 //                  k_incl_level   incl = excl + children's incl in child order, deepest
 //                                 level first.
 // Every fp64 operation is one correctly rounded __d*_rn call in the oracle's order.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -455,6 +456,106 @@ __global__ void k_block_counts(uint32_t n_blocks, const uint32_t *__restrict__ s
   }
 }
 
+// Step 4 for large trees in ONE cooperative launch: the grid walks the BFS levels itself,
+// separated by grid-wide barriers (no host round trip per level).  Per level [a, b):
+//   A  block i counts the children of its contiguous chunk and scans them locally
+//   B  block 0 scans the per-block totals -> the next level's size
+//   C  every block writes its chunk's children at b + block offset + local offset
+// then excl for every context, then incl level by level from the deepest.
+namespace cg = cooperative_groups;
+constexpr int kCoopThreads = 512;
+
+__global__ void __launch_bounds__(kCoopThreads) k_cct_coop(LevelArgs A, uint32_t n_dag, const uint32_t *din_ptr,
+                                                          const uint8_t *dact, const uint64_t *S_f, uint64_t n_total,
+                                                          double *excl, double *incl, uint32_t *tmp, uint32_t *bsum,
+                                                          uint32_t *lev, uint32_t max_lev,
+                                                          unsigned long long *built) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t t = threadIdx.x, nt = blockDim.x, B = gridDim.x, bi = blockIdx.x;
+  __shared__ uint32_t s_off;
+  if (bi == 0) {  // roots in DAG order (R15)
+    uint32_t running = 0;
+    for (uint32_t base = 0; base < n_dag; base += nt) {
+      uint32_t X = base + t;
+      uint32_t flag = X < n_dag && din_ptr[X] == din_ptr[X + 1] && dact[X];
+      uint32_t tot;
+      uint32_t pos = running + block_exscan(flag, &tot);
+      if (flag) {
+        A.parent[pos] = NONE;
+        A.site[pos] = NONE;
+        A.node[pos] = X;
+        A.kind[pos] = A.nontriv[X] ? GPA_CTX_SCC : GPA_CTX_FUNC;
+        A.frac[pos] = 1.0;
+      }
+      running += tot;
+    }
+    if (t == 0) {
+      lev[0] = 0;
+      lev[1] = running;
+    }
+  }
+  grid.sync();
+  uint32_t L = 0;
+  for (; L < max_lev; L++) {
+    const uint32_t a = lev[L], b = lev[L + 1];
+    if (b == a) break;
+    const uint32_t m = b - a, chunk = (m + B - 1) / B;
+    const uint32_t c0 = a + min(m, bi * chunk), c1 = a + min(m, (bi + 1) * chunk);
+    uint32_t run = 0;  // A: local counts + scan
+    for (uint32_t base = c0; base < c1; base += nt) {
+      uint32_t c = base + t;
+      uint32_t cnt = c < c1 ? child_count(A, c) : 0;
+      uint32_t tot;
+      uint32_t off = block_exscan(cnt, &tot);
+      if (c < c1) tmp[c - a] = run + off;
+      run += tot;
+    }
+    if (t == 0) bsum[bi] = run;
+    grid.sync();
+    if (bi == 0) {  // B: scan the block totals
+      uint32_t running = 0;
+      for (uint32_t base = 0; base < B; base += nt) {
+        uint32_t i = base + t;
+        uint32_t v = i < B ? bsum[i] : 0, tot;
+        uint32_t ex = block_exscan(v, &tot);
+        if (i < B) bsum[i] = running + ex;
+        running += tot;
+      }
+      if (t == 0) lev[L + 2] = b + running;
+    }
+    grid.sync();
+    if (t == 0) s_off = bsum[bi];  // C: write the children
+    __syncthreads();
+    for (uint32_t c = c0 + t; c < c1; c += nt) write_children(A, c, (uint64_t)b + s_off + tmp[c - a]);
+    grid.sync();
+  }
+  const uint64_t gt = (uint64_t)bi * nt + t, gs = (uint64_t)B * nt;
+  for (uint64_t x = gt; x < n_total * GPA_SLOTS; x += gs) {  // excl (R14)
+    uint64_t c = x >> 4;
+    int r = (int)(x & 15);
+    uint8_t k = A.kind[c];
+    double v = 0.0;
+    if (k != GPA_CTX_SCC) {
+      uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
+      v = __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
+    }
+    excl[x] = v;
+  }
+  grid.sync();
+  for (int l = (int)L - 1; l >= 0; l--) {  // incl: deepest level first, children in order
+    for (uint64_t x = (uint64_t)lev[l] * GPA_SLOTS + gt; x < (uint64_t)lev[l + 1] * GPA_SLOTS; x += gs) {
+      uint64_t c = x >> 4;
+      int r = (int)(x & 15);
+      double v = excl[x];
+      uint32_t d0 = A.first_child[c], nc = A.n_children[c];
+      for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, incl[(uint64_t)d * GPA_SLOTS + r]);
+      incl[x] = v;
+    }
+    grid.sync();
+  }
+  if (bi == 0 && t == 0) built[0] = L < max_lev ? lev[L] : ~0ull;
+}
+
 unsigned grid_for(uint64_t work, unsigned threads) {
   uint64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -487,7 +588,7 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
   // paths[] scratch lives behind W in the caller's allocation? keep it separate and simple:
   static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
   uint64_t *paths = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1), st);
+  cudaError_t e = pool_alloc((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1), st);
   if (e != cudaSuccess) return e;
   PropArgs A;
   A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels; A.exact = exact ? 1 : 0;
@@ -532,6 +633,26 @@ cudaError_t launch_block_counts(uint32_t n_blocks, const uint32_t *d_start, cons
                                                           (unsigned long long *)d_hist);
   count_launches(1);
   return cudaGetLastError();
+}
+
+cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_tmp, uint32_t *d_bsum, uint32_t *d_lev,
+                            uint32_t max_lev, unsigned long long *d_built, int sm_count, cudaStream_t st) {
+  LevelArgs A = level_args(s, c);
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cct_coop, kCoopThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  unsigned blocks = (unsigned)(sm_count * (per_sm < 2 ? per_sm : 2));
+  uint32_t n_dag = s->info.n_dag;
+  const uint32_t *din_ptr = s->d_din_ptr;
+  const uint8_t *dact = c->dag_active;
+  const uint64_t *S_f = c->S_f;
+  uint64_t n_total = c->n;
+  double *excl = c->excl, *incl = c->incl;
+  void *args[] = {&A, &n_dag, &din_ptr, &dact, &S_f, &n_total, &excl, &incl, &d_tmp, &d_bsum, &d_lev, &max_lev, &d_built};
+  e = cudaLaunchCooperativeKernel((void *)k_cct_coop, dim3(blocks), dim3(kCoopThreads), args, 0, st);
+  count_launches(1);
+  return e;
 }
 
 cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, unsigned long long *d_built, cudaStream_t st) {

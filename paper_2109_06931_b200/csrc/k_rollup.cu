@@ -189,7 +189,7 @@ cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_h
   unsigned long long *scratch = nullptr;
   const uint32_t n_multi = identity ? 0 : set->n_multi;
   if (n_multi) {
-    cudaError_t e = cudaMallocAsync((void **)&scratch, (size_t)n_multi * 32 * 8, st);
+    cudaError_t e = pool_alloc((void **)&scratch, (size_t)n_multi * 32 * 8, st);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(scratch, 0, (size_t)n_multi * 32 * 8, st);
   }
