@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(RingTma::kThreads, 1)
 #pragma unroll
     for (int u = 0; u < R; u++) v[u] = ring[(size_t)st * S + (u * NC + warp) * 32 + lane];
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
+    if (lane == 0) ring_release(empty + st);
     uint32_t inst[R];
 #pragma unroll
     for (int u = 0; u < R; u++) inst[u] = lookup<MODE>(T, ((uint64_t)v[u].y << 32) | v[u].x);
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
 #pragma unroll
     for (int u = 0; u < R; u++) vv[u] = src[u * NC * 32];  // beyond the tile end: masked below
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
+    if (lane == 0) ring_release(empty + st);
 #pragma unroll
     for (int u = 0; u < R; u++) {
       uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - base) >> gshift;
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
 #pragma unroll
     for (int u = 0; u < R; u++) vv[u] = src[u * NC * 32];  // beyond the tile end: masked below
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
+    if (lane == 0) ring_release(empty + st);
 #pragma unroll
     for (int u = 0; u < R; u++) {
       uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - base) >> gshift;

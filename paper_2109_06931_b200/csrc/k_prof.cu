@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
 #pragma unroll
     for (int u = 0; u < R; u++) vv[u] = src[u * NC * 32];  // beyond the tile end: masked below
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
+    if (lane == 0) ring_release(empty + st);
 #pragma unroll
     for (int u = 0; u < R; u++) {
       uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - T.base) >> T.gshift;

@@ -48,6 +48,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+// consumer side of a ring stage: order this warp's generic-proxy reads of the stage before the
+// producer's next async-proxy (TMA) write into it, then count the warp as done
+__device__ __forceinline__ void ring_release(uint64_t *empty_bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_arrive(empty_bar);
+}
 // 1-D bulk copy global -> shared through the TMA engine, completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
   asm volatile(
