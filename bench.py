@@ -215,17 +215,28 @@ def run_gpa(args):
             ev_a1.append(e1)
         reduce_histogram(HU, dst=0)
         if rank == 0:
-            for sc in SCOPES:
-                gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=stream)
-            cct = gpa.reconstruct_cct(s, H, stream=stream)
-            cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
-            gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
-            gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
-            stream.synchronize()
-            nctx = cct.n
-            cct.free()
-            return nctx
+            return analyse()
         return 0
+
+    side = torch.cuda.Stream(dev)
+
+    def analyse():
+        """Roll-up + metrics of the five scopes on a side stream, concurrently with the CCT
+        (both only read H)."""
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        side.wait_event(ready)
+        for sc in SCOPES:
+            gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=side)
+        cct = gpa.reconstruct_cct(s, H, stream=stream)
+        cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+        gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
+        gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+        stream.wait_stream(side)
+        stream.synchronize()
+        nctx = cct.n
+        cct.free()
+        return nctx
 
     for _ in range(args.warmup):
         nctx = step(False)
@@ -272,15 +283,10 @@ def run_gpa(args):
             gpa.attribute_samples_host(s, host, H, U, stream=stream)
             reduce_histogram(HU, dst=0)
             if rank == 0:
-                for sc in SCOPES:
-                    gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=stream)
-                cct = gpa.reconstruct_cct(s, H, stream=stream)
-                cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
-                gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+                analyse()
                 res_h.copy_(HU, non_blocking=True)
                 fm_h.copy_(met["FUNC"], non_blocking=True)
                 stream.synchronize()
-                cct.free()
 
         e_w = min(args.warmup, 1) if args.e2e_steps else args.warmup
         e_k = args.e2e_steps or args.steps

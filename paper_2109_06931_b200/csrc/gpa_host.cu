@@ -633,13 +633,13 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
   gpa_status ret = GPA_OK;
   auto cleanup = [&]() {
     if (cp) cudaStreamSynchronize(cp);
-    cudaStreamSynchronize(st);
     for (int b = 0; b < NBUF; b++) {
-      if (buf[b]) cudaFree(buf[b]);
+      if (buf[b]) cudaFreeAsync(buf[b], st);
       if (copied[b]) cudaEventDestroy(copied[b]);
       if (consumed[b]) cudaEventDestroy(consumed[b]);
     }
     if (cp) cudaStreamDestroy(cp);
+    cudaStreamSynchronize(st);
   };
 #define HC(call)                                                                          \
   do {                                                                                    \
@@ -654,10 +654,12 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
   } while (0)
   HC(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
   for (int b = 0; b < NBUF; b++) {
-    HC(cudaMalloc((void **)&buf[b], per * sizeof(gpa_sample)));
+    HC(pool_alloc((void **)&buf[b], per * sizeof(gpa_sample), st));
     HC(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
     HC(cudaEventCreateWithFlags(&consumed[b], cudaEventDisableTiming));
   }
+  HC(cudaEventRecord(consumed[0], st));  // the staging buffers exist (stream-ordered) before any copy
+  HC(cudaStreamWaitEvent(cp, consumed[0], 0));
   for (uint64_t off = 0, j = 0; off < n; off += per, j++) {
     int b = (int)(j % NBUF);
     uint64_t m = std::min(per, n - off);
