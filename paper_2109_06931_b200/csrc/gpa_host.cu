@@ -716,10 +716,44 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   CC(launch_cct_weights(s, d_inst_hist, c->w, st));
   CC(launch_rollup(&s->roll[ROLL_FUNC], s->roll[ROLL_FUNC].rows, d_inst_hist, s->d_inst_class, c->S_f, nullptr,
                    nullptr, sm_count(s->device), st));
+  unsigned long long h_cnt[2] = {0, 0};
+  if (max_contexts && cct_small_ok(s, I.cct_path_bound)) {
+    // Small static bound: build straight into bound-sized arrays with one CTA and read the
+    // size back once at the end (no separate path count, one host synchronization).
+    CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, mode == GPA_WEIGHTS_EXACT,
+                            false, st));
+    const uint64_t nb = I.cct_path_bound;
+    c->n = nb;
+    CC(calloc_dev(c, &c->parent, nb));
+    CC(calloc_dev(c, &c->site, nb));
+    CC(calloc_dev(c, &c->node, nb));
+    CC(calloc_dev(c, &c->first_child, nb));
+    CC(calloc_dev(c, &c->n_children, nb));
+    CC(calloc_dev(c, &c->kind, nb));
+    CC(calloc_dev(c, &c->frac, nb));
+    CC(calloc_dev(c, &c->excl, nb * SLOTS));
+    CC(calloc_dev(c, &c->incl, nb * SLOTS));
+    CC(launch_cct_small(s, c, d_cnt + 1, st));
+    CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CC(cudaStreamSynchronize(st));
+    if (h_cnt[1] > nb) {
+      free_cct(c);
+      return fail(GPA_ERR_INTERNAL, "tree of %llu contexts exceeds the static bound %llu", h_cnt[1],
+                  (unsigned long long)nb);
+    }
+    c->n = h_cnt[1];
+    *n_contexts = c->n;
+    if (c->n > max_contexts) {
+      free_cct(c);
+      return fail(GPA_ERR_CAPACITY, "%llu contexts > max_contexts %llu", (unsigned long long)*n_contexts,
+                  (unsigned long long)max_contexts);
+    }
+    *out = c;
+    return GPA_OK;
+  }
   // Step 2 + guard (R12) + W + context count (path DP over the DAG)
   CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, mode == GPA_WEIGHTS_EXACT,
-                          st));
-  unsigned long long h_cnt[2] = {0, 0};
+                          true, st));
   CC(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
   CC(cudaStreamSynchronize(st));
   *n_contexts = h_cnt[0];

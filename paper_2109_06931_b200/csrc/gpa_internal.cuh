@@ -116,7 +116,7 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
                                cudaStream_t st);
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
-                                 unsigned long long *d_count, bool exact, cudaStream_t st);
+                                 unsigned long long *d_count, bool exact, bool count, cudaStream_t st);
 // per-profile function histograms and cross-profile statistics (k_prof.cu)
 cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, const uint32_t *d_gfunc,
                                       uint32_t n_func,

@@ -40,7 +40,7 @@ __global__ void k_weights(const uint32_t *__restrict__ call_inst, uint32_t n_cal
 }
 
 struct PropArgs {
-  uint32_t n_func, n_dag, n_lev, exact;
+  uint32_t n_func, n_dag, n_lev, exact, do_count;
   const uint64_t *S_f;
   const uint32_t *fin_ptr, *fin_e, *caller, *scc_of, *din_ptr, *din_e, *dmem_ptr, *dmem, *dlev_ptr, *dlev_node;
   const uint8_t *nontriv;
@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
     A.W[X] = s;
   }
   // exact context count: paths from active roots through edges with w > 0, level by level
+  // (skipped when the caller builds the tree into a static-bound allocation and reads the
+  // size back afterwards)
+  if (!A.do_count) return;
   volatile uint64_t *paths = A.paths;
   for (uint32_t L = 0; L < A.n_lev; L++) {
     __syncthreads();
@@ -418,7 +421,8 @@ __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag,
     b = next;
   }
   __syncthreads();
-  for (uint64_t x = t; x < n_total * GPA_SLOTS; x += nt) {  // excl (R14)
+  const uint64_t n_built = b < n_total ? b : n_total;  // the arrays may be sized by a static bound
+  for (uint64_t x = t; x < n_built * GPA_SLOTS; x += nt) {  // excl (R14)
     uint64_t c = x >> 4;
     int r = (int)(x & 15);
     uint8_t k = A.kind[c];
@@ -584,14 +588,14 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
 
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
-                                 unsigned long long *d_count, bool exact, cudaStream_t st) {
+                                 unsigned long long *d_count, bool exact, bool count, cudaStream_t st) {
   // paths[] scratch lives behind W in the caller's allocation? keep it separate and simple:
   static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
   uint64_t *paths = nullptr;
   cudaError_t e = pool_alloc((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1), st);
   if (e != cudaSuccess) return e;
   PropArgs A;
-  A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels; A.exact = exact ? 1 : 0;
+  A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels; A.exact = exact ? 1 : 0; A.do_count = count ? 1 : 0;
   A.S_f = d_S_f; A.fin_ptr = s->d_fin_ptr; A.fin_e = s->d_fin_e; A.caller = s->d_call_caller;
   A.scc_of = s->d_scc_of; A.din_ptr = s->d_din_ptr; A.din_e = s->d_din_e; A.dmem_ptr = s->d_dmem_ptr;
   A.dmem = s->d_dmem; A.dlev_ptr = s->d_dlev_ptr; A.dlev_node = s->d_dlev_node; A.nontriv = s->d_dag_nontrivial;
