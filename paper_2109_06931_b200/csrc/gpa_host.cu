@@ -733,7 +733,9 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
     CC(calloc_dev(c, &c->frac, nb));
     CC(calloc_dev(c, &c->excl, nb * SLOTS));
     CC(calloc_dev(c, &c->incl, nb * SLOTS));
-    CC(launch_cct_small(s, c, d_cnt + 1, st));
+    uint32_t *d_lev = nullptr;
+    CC(calloc_dev(c, &d_lev, 1100));
+    CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
     CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CC(cudaStreamSynchronize(st));
     if (h_cnt[1] > nb) {
@@ -778,7 +780,9 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   CC(calloc_dev(c, &c->excl, n * SLOTS));
   CC(calloc_dev(c, &c->incl, n * SLOTS));
   if (cct_small_ok(s, n)) {  // one CTA builds the whole tree: no per-level launches or syncs
-    CC(launch_cct_small(s, c, d_cnt + 1, st));
+    uint32_t *d_lev = nullptr;
+    CC(calloc_dev(c, &d_lev, 1100));
+    CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
     *out = c;
     return GPA_OK;
   }

@@ -138,6 +138,7 @@ bool cct_small_ok(const gpa_structure_s *s, uint64_t n);
 // whole Step 4 in one cooperative grid launch (large trees); d_bsum >= 2*SMs entries
 cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_tmp, uint32_t *d_bsum, uint32_t *d_lev,
                             uint32_t max_lev, unsigned long long *d_built, int sm_count, cudaStream_t st);
-cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, unsigned long long *d_built, cudaStream_t st);
+cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_lev, unsigned long long *d_built,
+                             int sm_count, cudaStream_t st);
 cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStream_t st);
 }  // namespace gpa

@@ -382,8 +382,8 @@ __device__ __forceinline__ void write_children(const LevelArgs &A, uint64_t c, u
 }
 
 __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag, const uint32_t *din_ptr,
-                                                    const uint8_t *dact, const uint64_t *S_f, uint64_t n_total,
-                                                    double *excl, double *incl, unsigned long long *built) {
+                                                    const uint8_t *dact, uint32_t *lev_out,
+                                                    unsigned long long *built) {
   __shared__ uint32_t lev[kSmallLevels + 1];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   uint32_t running = 0;
@@ -421,30 +421,8 @@ __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag,
     b = next;
   }
   __syncthreads();
-  const uint64_t n_built = b < n_total ? b : n_total;  // the arrays may be sized by a static bound
-  for (uint64_t x = t; x < n_built * GPA_SLOTS; x += nt) {  // excl (R14)
-    uint64_t c = x >> 4;
-    int r = (int)(x & 15);
-    uint8_t k = A.kind[c];
-    double v = 0.0;
-    if (k != GPA_CTX_SCC) {
-      uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
-      v = __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
-    }
-    excl[x] = v;
-  }
-  __syncthreads();
-  for (int l = (int)L - 1; l >= 0; l--) {  // incl: deepest level first, children in order
-    for (uint64_t x = (uint64_t)lev[l] * GPA_SLOTS + t; x < (uint64_t)lev[l + 1] * GPA_SLOTS; x += nt) {
-      uint64_t c = x >> 4;
-      int r = (int)(x & 15);
-      double v = excl[x];
-      uint32_t d0 = A.first_child[c], nc = A.n_children[c];
-      for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, incl[(uint64_t)d * GPA_SLOTS + r]);
-      incl[x] = v;
-    }
-    __syncthreads();
-  }
+  for (uint32_t l = t; l <= L; l += nt) lev_out[l + 1] = lev[l];  // lev_out[0] = number of levels
+  if (t == 0) lev_out[0] = L;
   if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
 }
 
@@ -560,6 +538,40 @@ __global__ void __launch_bounds__(kCoopThreads) k_cct_coop(LevelArgs A, uint32_t
   if (bi == 0 && t == 0) built[0] = L < max_lev ? lev[L] : ~0ull;
 }
 
+// excl for every context, then incl level by level (deepest first), over the whole grid with
+// grid-wide barriers; the level boundaries come from k_cct_small (lev[0] = levels,
+// lev[1 + l] = first context of level l).
+__global__ void __launch_bounds__(512) k_cct_fold(LevelArgs A, const uint32_t *__restrict__ lev,
+                                                 const uint64_t *__restrict__ S_f, double *excl, double *incl) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t L = lev[0];
+  const uint64_t n = lev[1 + L];
+  const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t x = gt; x < n * GPA_SLOTS; x += gs) {  // excl (R14)
+    uint64_t c = x >> 4;
+    int r = (int)(x & 15);
+    uint8_t k = A.kind[c];
+    double v = 0.0;
+    if (k != GPA_CTX_SCC) {
+      uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
+      v = __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
+    }
+    excl[x] = v;
+  }
+  grid.sync();
+  for (int l = (int)L - 1; l >= 0; l--) {  // incl: children in index order
+    for (uint64_t x = (uint64_t)lev[1 + l] * GPA_SLOTS + gt; x < (uint64_t)lev[2 + l] * GPA_SLOTS; x += gs) {
+      uint64_t c = x >> 4;
+      int r = (int)(x & 15);
+      double v = excl[x];
+      uint32_t d0 = A.first_child[c], nc = A.n_children[c];
+      for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, incl[(uint64_t)d * GPA_SLOTS + r]);
+      incl[x] = v;
+    }
+    grid.sync();
+  }
+}
+
 unsigned grid_for(uint64_t work, unsigned threads) {
   uint64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -659,12 +671,24 @@ cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_
   return e;
 }
 
-cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, unsigned long long *d_built, cudaStream_t st) {
+cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_lev, unsigned long long *d_built,
+                             int sm_count, cudaStream_t st) {
   LevelArgs A = level_args(s, c);
-  k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, c->S_f, c->n, c->excl, c->incl,
-                                  d_built);
+  k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built);
   count_launches(1);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cct_fold, 512, 0);
+  if (e != cudaSuccess) return e;
+  unsigned blocks = (unsigned)(sm_count * (per_sm < 2 ? (per_sm < 1 ? 1 : per_sm) : 2));
+  const uint32_t *lev = d_lev;
+  const uint64_t *S_f = c->S_f;
+  double *excl = c->excl, *incl = c->incl;
+  void *args[] = {&A, &lev, &S_f, &excl, &incl};
+  e = cudaLaunchCooperativeKernel((void *)k_cct_fold, dim3(blocks), dim3(512), args, 0, st);
+  count_launches(1);
+  return e;
 }
 
 bool cct_small_ok(const gpa_structure_s *s, uint64_t n) {
