@@ -370,7 +370,10 @@ done:
 // its hot slots and a base index (atomic cursor) and records bin_of[idx] = inst<<4 | slot;
 // k_codemap_bins builds a per-call 64-bit code per granule: low word inst<<4 (or ~0 unmapped),
 // high word base<<12 | mask (0 for unmapped granules and instructions without hot bins).  A record's table index is base + popc(mask & below(slot)).
-constexpr int kHotBins = 40960;                     // x 4 B = 160 KiB
+#ifndef GPA_HOT_BINS
+#define GPA_HOT_BINS 32768
+#endif
+constexpr int kHotBins = GPA_HOT_BINS;               // x 4 B = 128 KiB (the rest of the SM's 256 KiB is L1 for the code-map gathers)
 using RingBins = Ring<16, 2, 4>;
 
 __global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
