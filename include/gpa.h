@@ -247,6 +247,32 @@ GPA_API gpa_status gpa_attribute_profiles(gpa_structure s, const gpa_sample *d_s
 GPA_API gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles,
                                      double *d_stats, gpa_stream_t stream);
 
+/* ---- f3: sparse cubes (PMS / CMS) of the per-profile histograms -------------------------
+ * PAPER.md §5.2: "Profile Major Sparse" and "CCT Major Sparse" formats, one modified
+ * CSR per plane.  The cube is d_prof_hist of gpa_attribute_profiles with all n_profiles+1
+ * profile rows (p x function row c x slot m).  GPA_SPARSE_CMS: plane = c, its values ordered
+ * by (m, p) with ids[] = p, and a sparse metric index of (m, start) pairs; GPA_SPARSE_PMS:
+ * plane = p, values ordered by (c, m) with ids[] = m, sparse context index of (c, start).
+ * Every plane's index ends with a sentinel (GPA_NONE, end).  plane_off / index_off
+ * [n_planes+1] are element offsets into the value / index arrays.  Library-owned result;
+ * synchronizes `stream` (the non-zero count decides the allocation). */
+typedef enum { GPA_SPARSE_PMS = 0, GPA_SPARSE_CMS = 1 } gpa_sparse_major;
+typedef struct gpa_sparse_s *gpa_sparse;
+typedef struct {
+  uint32_t major, n_planes;
+  uint64_t n_values, n_index;
+  const uint64_t *plane_off;   /* [n_planes+1] */
+  const uint64_t *index_off;   /* [n_planes+1] */
+  const uint64_t *vals;        /* [n_values] non-zero values                       */
+  const uint32_t *ids;         /* [n_values] profile id (CMS) or metric id (PMS)   */
+  const uint64_t *index_start; /* [n_index] start of each inner run in vals        */
+  const uint32_t *index_id;    /* [n_index] metric (CMS) / context (PMS) id; GPA_NONE = sentinel */
+} gpa_sparse_view;
+GPA_API gpa_status gpa_sparse_build(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles,
+                                    gpa_sparse_major major, gpa_sparse *out, gpa_stream_t stream);
+GPA_API gpa_status gpa_get_sparse_view(gpa_sparse sp, gpa_sparse_view *out);
+GPA_API void gpa_free_sparse(gpa_sparse sp);
+
 /* ---- a-6..a-9: approximate GPU calling-context tree (§5.3) -----------------
  * From a per-instruction histogram: Step 1 edge weights w_e = sum_{r<12} H[call_inst[e]][r]
  * (R10); Step 2 zero-weight propagation to the least fixpoint (R11) and the

@@ -31,6 +31,12 @@ _u8p = ctypes.POINTER(ctypes.c_uint8)
 _f64p = ctypes.POINTER(ctypes.c_double)
 
 
+class _Sparse(ctypes.Structure):
+    _fields_ = [("n_planes", ctypes.c_uint32), ("n_values", ctypes.c_uint64), ("n_index", ctypes.c_uint64),
+                ("plane_off", _u64p), ("index_off", _u64p), ("vals", _u64p), ("index_start", _u64p),
+                ("ids", _u32p), ("index_id", _u32p)]
+
+
 class _CctResult(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_uint64), ("cap", ctypes.c_uint64),
@@ -70,6 +76,10 @@ def _lib():
     lib.oracle_attribute_profiles.restype = None
     lib.oracle_profile_stats.argtypes = [u32, u32, vp, vp]
     lib.oracle_profile_stats.restype = None
+    lib.oracle_sparse_build.argtypes = [vp, u32, u32, ctypes.c_int]
+    lib.oracle_sparse_build.restype = ctypes.POINTER(_Sparse)
+    lib.oracle_sparse_free.argtypes = [ctypes.POINTER(_Sparse)]
+    lib.oracle_sparse_free.restype = None
     lib.oracle_block_counts.argtypes = [u32, vp, vp, vp]
     lib.oracle_block_counts.restype = None
     lib.oracle_cct_free.argtypes = [ctypes.POINTER(_CctResult)]
@@ -224,6 +234,25 @@ def profile_stats(Hp, n_prof: int) -> np.ndarray:
     if rows:
         _lib().oracle_profile_stats(n_prof, rows, Hp.ctypes.data, out.ctypes.data)
     return out
+
+
+def sparse_build(Hp, cms: bool) -> dict:
+    """D9: CMS (cms=True) or PMS of the cube Hp [P, C, 16] (see gpa_oracle.c)."""
+    Hp = np.ascontiguousarray(Hp, np.uint64)
+    P, C = Hp.shape[0], Hp.shape[1]
+    r = _lib().oracle_sparse_build(Hp.ctypes.data if Hp.size else None, P, C, 1 if cms else 0)
+    try:
+        S = r.contents
+        nq, nv, ni = S.n_planes, S.n_values, S.n_index
+
+        def arr(p, cnt, dt):
+            return np.ctypeslib.as_array(p, shape=(cnt,)).astype(dt, copy=True) if cnt else np.zeros(0, dt)
+        return dict(n_planes=nq, n_values=nv, n_index=ni, plane_off=arr(S.plane_off, nq + 1, np.uint64),
+                    index_off=arr(S.index_off, nq + 1, np.uint64), vals=arr(S.vals, nv, np.uint64),
+                    ids=arr(S.ids, nv, np.uint32), index_start=arr(S.index_start, ni, np.uint64),
+                    index_id=arr(S.index_id, ni, np.uint32))
+    finally:
+        _lib().oracle_sparse_free(r)
 
 
 def block_counts(n_inst: int, block_start, count) -> np.ndarray:

@@ -530,6 +530,75 @@ void oracle_profile_stats(uint32_t n_prof, uint32_t rows, const uint64_t *Hp, do
 }
 
 /* ======================================================================================
+ * D9 — sparse cube formats (§5.2, Fig. sf).  The cube is
+ * the per-profile histogram Hp[p][c][m] (p < P, c < C, m < 16; "context" = the function row,
+ * metric = the slot).  Like CSR but over planes:
+ *   CMS (context-major): plane c holds its non-zeros ordered by (metric, profile) as vals[]
+ *     and pids[]; its sparse metric index is a list of (metric id, start) pairs for the
+ *     non-empty metrics followed by a sentinel (GPA_NONE, end) ("we make midxs a sparse
+ *     array: each entry is a pair of metric ID and this metric's starting index").
+ *   PMS (profile-major): plane p holds its non-zeros ordered by (context, metric) as vals[]
+ *     and mids[]; its sparse context index lists (context id, start) + sentinel.
+ * plane_off[q] / index_off[q] give where plane q starts in the value / index arrays
+ * ("a vector of ... offsets, one per ..."); element offsets, not bytes.
+ * ====================================================================================== */
+typedef struct {
+  uint32_t n_planes; uint64_t n_values, n_index;
+  uint64_t *plane_off, *index_off, *vals, *index_start;
+  uint32_t *ids, *index_id;
+} oracle_sparse;
+
+oracle_sparse *oracle_sparse_build(const uint64_t *Hp, uint32_t P, uint32_t C, int cms)
+{
+  oracle_sparse *S = (oracle_sparse *)calloc(1, sizeof(oracle_sparse));
+  uint32_t planes = cms ? C : P, inner = cms ? O_SLOTS : C, leaf = cms ? P : O_SLOTS;
+  S->n_planes = planes;
+  uint64_t nv = 0, ni = 0;
+  for (uint64_t x = 0; x < (uint64_t)P * C * O_SLOTS; x++) nv += Hp[x] != 0;
+  /* index entries: one per non-empty (plane, inner) pair, plus a sentinel per plane */
+  for (uint32_t a = 0; a < planes; a++) {
+    for (uint32_t b = 0; b < inner; b++) {
+      int any = 0;
+      for (uint32_t l = 0; l < leaf; l++) {
+        uint64_t v = cms ? Hp[((uint64_t)l * C + a) * O_SLOTS + b] : Hp[((uint64_t)a * C + b) * O_SLOTS + l];
+        if (v) any = 1;
+      }
+      ni += any;
+    }
+    ni += 1;
+  }
+  S->n_values = nv; S->n_index = ni;
+  S->plane_off = (uint64_t *)malloc(sizeof(uint64_t) * (planes + 1));
+  S->index_off = (uint64_t *)malloc(sizeof(uint64_t) * (planes + 1));
+  S->vals = (uint64_t *)malloc(sizeof(uint64_t) * (nv + 1));
+  S->ids = (uint32_t *)malloc(sizeof(uint32_t) * (nv + 1));
+  S->index_start = (uint64_t *)malloc(sizeof(uint64_t) * (ni + 1));
+  S->index_id = (uint32_t *)malloc(sizeof(uint32_t) * (ni + 1));
+  uint64_t v0 = 0, i0 = 0;
+  for (uint32_t a = 0; a < planes; a++) {
+    S->plane_off[a] = v0; S->index_off[a] = i0;
+    for (uint32_t b = 0; b < inner; b++) {
+      uint64_t start = v0;
+      for (uint32_t l = 0; l < leaf; l++) {
+        uint64_t v = cms ? Hp[((uint64_t)l * C + a) * O_SLOTS + b] : Hp[((uint64_t)a * C + b) * O_SLOTS + l];
+        if (v) { S->vals[v0] = v; S->ids[v0] = l; v0++; }
+      }
+      if (v0 > start) { S->index_id[i0] = b; S->index_start[i0] = start; i0++; }
+    }
+    S->index_id[i0] = O_NONE; S->index_start[i0] = v0; i0++;   /* sentinel: end of plane */
+  }
+  S->plane_off[planes] = v0; S->index_off[planes] = i0;
+  return S;
+}
+
+void oracle_sparse_free(oracle_sparse *S)
+{
+  if (!S) return;
+  free(S->plane_off); free(S->index_off); free(S->vals); free(S->ids); free(S->index_start); free(S->index_id);
+  free(S);
+}
+
+/* ======================================================================================
  * D7 — derived metrics ("based on the number of total PC samples (S) and
  * stalled PC samples (S_stall), we can estimate the Warp Issue Rate (W) of schedulers as
  * W = (S - S_stall)/S"; "stall percentages").  S = sum of the 12 valid slots;

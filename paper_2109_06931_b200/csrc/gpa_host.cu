@@ -863,6 +863,91 @@ gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint3
   return GPA_OK;
 }
 
+static void free_sparse(gpa_sparse_s *sp) {
+  if (!sp) return;
+  DeviceGuard g(sp->device);
+  for (void *p : sp->allocs)
+    if (cudaFreeAsync(p, sp->stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(p);
+    }
+  delete sp;
+}
+
+gpa_status gpa_sparse_build(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles, gpa_sparse_major major,
+                            gpa_sparse *out, gpa_stream_t stream) {
+  if (!s || !out) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (major != GPA_SPARSE_PMS && major != GPA_SPARSE_CMS) return fail(GPA_ERR_INVALID_ARG, "major %d", (int)major);
+  const uint32_t P = n_profiles + 1, C = s->info.n_func;
+  if (C && !d_prof_hist) return fail(GPA_ERR_INVALID_ARG, "d_prof_hist is NULL");
+  if ((uint64_t)P * C * GPA_SLOTS >= (1ull << 32))
+    return fail(GPA_ERR_UNSUPPORTED, "cube of %llu cells exceeds 2^32", (unsigned long long)P * C * GPA_SLOTS);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  gpa_sparse_s *sp = new gpa_sparse_s();
+  sp->device = s->device;
+  sp->stream = st;
+  sp->major = major;
+  const bool cms = major == GPA_SPARSE_CMS;
+  sp->n_planes = cms ? C : P;
+  const uint64_t cells = cms ? (uint64_t)C * GPA_SLOTS : (uint64_t)P * C;
+  auto alloc = [&](void **p, size_t bytes) {
+    cudaError_t e = pool_alloc(p, bytes ? bytes : 8, st);
+    if (e == cudaSuccess) sp->allocs.push_back(*p);
+    return e;
+  };
+#define SC(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      gpa_status r_ = fail(e_ == cudaErrorMemoryAllocation ? GPA_ERR_OUT_OF_MEMORY : GPA_ERR_CUDA, "%s: %s", \
+                           #call, cudaGetErrorString(e_));                                \
+      cudaGetLastError();                                                                 \
+      free_sparse(sp);                                                                    \
+      return r_;                                                                          \
+    }                                                                                     \
+  } while (0)
+  uint32_t *ov = nullptr, *oi = nullptr, *bs = nullptr;
+  unsigned long long *tot = nullptr;
+  SC(alloc((void **)&ov, cells * 4));
+  SC(alloc((void **)&oi, cells * 4));
+  SC(alloc((void **)&bs, 65536 * 4));
+  SC(alloc((void **)&tot, 16));
+  SC(alloc((void **)&sp->plane_off, (sp->n_planes + 1) * 8));
+  SC(alloc((void **)&sp->index_off, (sp->n_planes + 1) * 8));
+  if (cells == 0) {  // no function rows: every plane is empty except for its sentinel
+    free_sparse(sp);
+    return fail(GPA_ERR_UNSUPPORTED, "no function rows to encode");
+  }
+  SC(sparse_count(d_prof_hist, P, C, cms, ov, oi, bs, tot, st));
+  unsigned long long h_tot[2] = {0, 0};
+  SC(cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
+  SC(cudaStreamSynchronize(st));
+  sp->n_values = h_tot[0];
+  sp->n_index = h_tot[1];
+  SC(alloc((void **)&sp->vals, sp->n_values * 8));
+  SC(alloc((void **)&sp->ids, sp->n_values * 4));
+  SC(alloc((void **)&sp->index_start, sp->n_index * 8));
+  SC(alloc((void **)&sp->index_id, sp->n_index * 4));
+  SC(sparse_write(d_prof_hist, P, C, cms, ov, oi, tot, sp->plane_off, sp->index_off, sp->vals, sp->ids,
+                  sp->index_start, sp->index_id, st));
+#undef SC
+  *out = sp;
+  return GPA_OK;
+}
+
+gpa_status gpa_get_sparse_view(gpa_sparse sp, gpa_sparse_view *v) {
+  if (!sp || !v) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  v->major = sp->major; v->n_planes = sp->n_planes; v->n_values = sp->n_values; v->n_index = sp->n_index;
+  v->plane_off = sp->plane_off; v->index_off = sp->index_off; v->vals = sp->vals; v->ids = sp->ids;
+  v->index_start = sp->index_start; v->index_id = sp->index_id;
+  return GPA_OK;
+}
+
+void gpa_free_sparse(gpa_sparse sp) { free_sparse(sp); }
+
 gpa_status gpa_block_counts(gpa_structure s, uint32_t n_blocks, const uint32_t *d_block_start,
                             const uint64_t *d_counts, uint64_t *d_inst_hist, gpa_stream_t stream) {
   if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");

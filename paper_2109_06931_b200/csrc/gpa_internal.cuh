@@ -74,6 +74,16 @@ struct gpa_structure_s {
   std::vector<void *> allocs;
 };
 
+struct gpa_sparse_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t major = 0, n_planes = 0;
+  uint64_t n_values = 0, n_index = 0;
+  uint64_t *plane_off = nullptr, *index_off = nullptr, *vals = nullptr, *index_start = nullptr;
+  uint32_t *ids = nullptr, *index_id = nullptr;
+  std::vector<void *> allocs;
+};
+
 struct gpa_cct_s {
   int device = 0;
   cudaStream_t stream = nullptr;  // the build stream: allocations and frees are ordered on it
@@ -125,6 +135,12 @@ cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_ins
                                       cudaStream_t st);
 cudaError_t launch_profile_stats(const uint64_t *d_ph, uint32_t n_prof, uint32_t rows, double *d_stats,
                                  cudaStream_t st);
+// sparse cubes (k_sparse.cu): counts + offsets (tot[0] values, tot[1] index entries), then the write
+cudaError_t sparse_count(const uint64_t *H, uint32_t P, uint32_t C, bool cms, uint32_t *ov, uint32_t *oi,
+                         uint32_t *bs, unsigned long long *tot, cudaStream_t st);
+cudaError_t sparse_write(const uint64_t *H, uint32_t P, uint32_t C, bool cms, const uint32_t *ov, const uint32_t *oi,
+                         const unsigned long long *tot, uint64_t *plane_off, uint64_t *index_off, uint64_t *vals,
+                         uint32_t *ids, uint64_t *index_start, uint32_t *index_id, cudaStream_t st);
 cudaError_t launch_block_counts(uint32_t n_blocks, const uint32_t *d_start, const uint64_t *d_cnt, uint32_t n_inst,
                                 uint64_t *d_hist, cudaStream_t st);
 cudaError_t launch_cct_roots(const gpa_structure_s *s, const uint8_t *d_dag_active, gpa_cct_s *c,

@@ -18,14 +18,12 @@
 #include <stdint.h>
 
 #include "gpa_internal.cuh"
+#include "kern_common.cuh"
 
 namespace gpa {
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 2;
-constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long SAT = 1ull << 62;
 
 __global__ void k_weights(const uint32_t *__restrict__ call_inst, uint32_t n_call, const uint64_t *__restrict__ H,
@@ -161,33 +159,6 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
   }
 }
 
-// block-wide exclusive scan of one u32 per thread; returns the block total in *total
-__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t *total) {
-  __shared__ uint32_t wsum[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  __syncthreads();
-  if (lane == 31) wsum[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t s = lane < nw ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(FULL, s, o);
-      if (lane >= o) s += y;
-    }
-    wsum[lane] = s;  // inclusive warp-prefix
-  }
-  __syncthreads();
-  *total = wsum[nw - 1];
-  return x - v + (wid ? wsum[wid - 1] : 0);
-}
-
 // roots: active DAG nodes without external in-edges, in DAG order (R15)
 __global__ void __launch_bounds__(1024) k_roots(uint32_t n_dag, const uint32_t *din_ptr, const uint8_t *dact,
                                                 const uint8_t *nontriv, uint32_t *parent, uint32_t *site,
@@ -236,45 +207,6 @@ __device__ __forceinline__ uint32_t child_count(const LevelArgs &A, uint64_t c) 
 __global__ void k_level_count(LevelArgs A, uint64_t a, uint64_t b, uint32_t *tmp) {
   for (uint64_t c = a + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < b; c += (uint64_t)gridDim.x * blockDim.x)
     tmp[c - a] = child_count(A, c);
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *v, uint64_t m, uint32_t *bs) {
-  uint64_t i0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-  uint32_t s = 0;
-#pragma unroll
-  for (int q = 0; q < kScanItems; q++) s += i0 + q < m ? v[i0 + q] : 0;
-  uint32_t tot;
-  block_exscan(s, &tot);
-  if (threadIdx.x == 0) bs[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_top(uint32_t *bs, uint32_t nb, unsigned long long *total) {
-  uint32_t running = 0;
-  for (uint32_t base = 0; base < nb; base += blockDim.x) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = i < nb ? bs[i] : 0, tot;
-    uint32_t ex = block_exscan(v, &tot);
-    if (i < nb) bs[i] = running + ex;
-    running += tot;
-  }
-  if (threadIdx.x == 0) total[0] = running;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t *v, uint64_t m, const uint32_t *bs) {
-  uint64_t i0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-  uint32_t x[kScanItems], s = 0;
-#pragma unroll
-  for (int q = 0; q < kScanItems; q++) {
-    x[q] = i0 + q < m ? v[i0 + q] : 0;
-    s += x[q];
-  }
-  uint32_t tot;
-  uint32_t ex = block_exscan(s, &tot) + bs[blockIdx.x];
-#pragma unroll
-  for (int q = 0; q < kScanItems; q++) {
-    if (i0 + q < m) v[i0 + q] = ex;
-    ex += x[q];
-  }
 }
 
 __global__ void k_level_write(LevelArgs A, uint64_t a, uint64_t b, const uint32_t *off) {

@@ -102,5 +102,79 @@ __device__ __forceinline__ void ring_init(uint64_t *full, uint64_t *empty, int n
   }
 }
 
+// ---- scans ---------------------------------------------------------------------------------
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 2;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// block-wide exclusive scan of one u32 per thread; returns the block total in *total
+__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t *total) {
+  __shared__ uint32_t wsum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(kFull, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s;  // inclusive warp-prefix
+  }
+  __syncthreads();
+  *total = wsum[nw - 1];
+  return x - v + (wid ? wsum[wid - 1] : 0);
+}
+
+// multi-block exclusive scan of u32 values in place (k_scan_reduce -> k_scan_top -> k_scan_down;
+// up to 65536 tiles of kScanTile); the grand total goes to *total
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *v, uint64_t m, uint32_t *bs) {
+  uint64_t i0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) s += i0 + q < m ? v[i0 + q] : 0;
+  uint32_t tot;
+  block_exscan(s, &tot);
+  if (threadIdx.x == 0) bs[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(uint32_t *bs, uint32_t nb, unsigned long long *total) {
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < nb; base += blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t v = i < nb ? bs[i] : 0, tot;
+    uint32_t ex = block_exscan(v, &tot);
+    if (i < nb) bs[i] = running + ex;
+    running += tot;
+  }
+  if (threadIdx.x == 0) total[0] = running;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t *v, uint64_t m, const uint32_t *bs) {
+  uint64_t i0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t x[kScanItems], s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    x[q] = i0 + q < m ? v[i0 + q] : 0;
+    s += x[q];
+  }
+  uint32_t tot;
+  uint32_t ex = block_exscan(s, &tot) + bs[blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    if (i0 + q < m) v[i0 + q] = ex;
+    ex += x[q];
+  }
+}
+
 }  // namespace
 }  // namespace gpa

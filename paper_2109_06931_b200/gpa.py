@@ -57,6 +57,12 @@ class CctView(ctypes.Structure):
                 ("func_hist", _vp)]
 
 
+class SparseView(ctypes.Structure):
+    _fields_ = [("major", _u32), ("n_planes", _u32), ("n_values", _u64), ("n_index", _u64),
+                ("plane_off", _vp), ("index_off", _vp), ("vals", _vp), ("ids", _vp),
+                ("index_start", _vp), ("index_id", _vp)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
@@ -81,6 +87,9 @@ def _load():
         "gpa_attribute_profiles": ([_vp, _vp, _u64, _u32, _vp, _vp, _vp], S),
         "gpa_profile_stats": ([_vp, _vp, _u32, _vp, _vp], S),
         "gpa_set_attr_kernel": ([ctypes.c_int], S),
+        "gpa_sparse_build": ([_vp, _vp, _u32, ctypes.c_int, ctypes.POINTER(_vp), _vp], S),
+        "gpa_get_sparse_view": ([_vp, ctypes.POINTER(SparseView)], S),
+        "gpa_free_sparse": ([_vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -320,6 +329,63 @@ class Cct:
             self.free()
         except Exception:
             pass
+
+
+SPARSE_PMS, SPARSE_CMS = 0, 1
+
+
+class Sparse:
+    """f3: a PMS or CMS sparse cube (gpa_sparse), library-owned device arrays (§5.2)."""
+
+    def __init__(self, h, device):
+        self._h = h
+        self.device = device
+        v = SparseView()
+        _check(_lib.gpa_get_sparse_view(h, ctypes.byref(v)), "gpa_get_sparse_view")
+        self._v = v
+        self.cms = bool(v.major == SPARSE_CMS)
+        self.n_planes, self.n_values, self.n_index = v.n_planes, v.n_values, v.n_index
+
+    def tensors(self) -> dict:
+        """Zero-copy torch views (valid until free()); u64 arrays as int64, u32 as int32."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        v = self._v
+        spec = {"plane_off": ("<i8", v.n_planes + 1), "index_off": ("<i8", v.n_planes + 1),
+                "vals": ("<i8", v.n_values), "ids": ("<i4", v.n_values),
+                "index_start": ("<i8", v.n_index), "index_id": ("<i4", v.n_index)}
+        dt = {"<i4": torch.int32, "<i8": torch.int64}
+        return {k: torch.as_tensor(_DevArray(getattr(v, k), (m,), ts), device=dev) if m else
+                torch.empty(0, dtype=dt[ts], device=dev) for k, (ts, m) in spec.items()}
+
+    def to_numpy(self) -> dict:
+        out = {}
+        for k, x in self.tensors().items():
+            a = x.cpu().numpy()
+            out[k] = a.view(np.uint64) if a.dtype == np.int64 else a.view(np.uint32)
+        out.update(n_planes=self.n_planes, n_values=self.n_values, n_index=self.n_index)
+        return out
+
+    def free(self):
+        if self._h is not None:
+            _lib.gpa_free_sparse(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sparse_build(s: Structure, prof_hist, n_profiles: int, cms: bool, stream=None) -> Sparse:
+    """f3: encode the per-profile cube prof_hist [(n_profiles+1), n_func, 16] as CMS or PMS."""
+    h = _vp()
+    _check(_lib.gpa_sparse_build(s.handle, _ptr(prof_hist, "prof_hist",
+                                                 128 * (int(n_profiles) + 1) * s.info["n_func"]),
+                                 int(n_profiles), SPARSE_CMS if cms else SPARSE_PMS, ctypes.byref(h),
+                                 _stream_ptr(stream, prof_hist.device)), "gpa_sparse_build")
+    return Sparse(h, s.device)
 
 
 def reconstruct_cct(s: Structure, inst_hist, mode: int = WEIGHTS_SAMPLES, max_contexts: int = (1 << 63) - 1,

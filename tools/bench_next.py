@@ -1,5 +1,6 @@
 """Measurements of the SURVEY §8f rows built beyond the north-star path (one JSON line each):
 f1 per-profile histograms + cross-profile statistics on C4 (1e9 records, 384 profiles), and
+f3 sparse PMS/CMS encoding of f1's cube, and
 f2 exact-count mode (block counts -> instructions -> exact-mode CCT) on C3's structure.
 CUDA events around each call, median of K after W warm-ups."""
 import json
@@ -55,6 +56,22 @@ def f1():
     print(json.dumps({"row": "f1", "workload": "C4", "records": n, "profiles": P, "kernel": "k_attr_prof",
                       "attr_ms": ms_attr, "records_per_s": n / ms_attr * 1e3, "GBps": gbs, "frac": gbs / PEAK,
                       "stats_ms": ms_stats}), flush=True)
+    f3(s, PH, P)
+
+
+def f3(s, PH, P):
+    """Sparse PMS / CMS encoding of f1's cube (one build = count + scans + sync + write)."""
+    for cms in (False, True):
+        def run():
+            gpa.sparse_build(s, PH, P, cms).free()
+        ms = timed(run)
+        sp = gpa.sparse_build(s, PH, P, cms)
+        cube = PH.numel() * 8
+        out = sp.n_values * 12 + sp.n_index * 12 + 16 * (sp.n_planes + 1)
+        print(json.dumps({"row": "f3", "format": "CMS" if cms else "PMS", "cube_bytes": cube,
+                          "n_values": sp.n_values, "n_index": sp.n_index, "ms": ms,
+                          "GBps_cube_2pass_plus_out": (2 * cube + out) / ms / 1e6}), flush=True)
+        sp.free()
 
 
 def f2():
