@@ -88,6 +88,8 @@ def _lib():
     lib.oracle_derive_u64.restype = None
     lib.oracle_derive_f64.argtypes = [u64, vp, vp]
     lib.oracle_derive_f64.restype = None
+    lib.oracle_blame.argtypes = [u32, vp, vp, vp, vp, vp, u32, u32, u32, vp, vp, vp, vp, vp]
+    lib.oracle_blame.restype = ctypes.c_int
     return lib
 
 
@@ -281,3 +283,27 @@ def derive_f64(V) -> np.ndarray:
     if len(V):
         _lib().oracle_derive_f64(len(V), V.ctypes.data, out.ctypes.data)
     return out
+
+
+# ---- D10 --------------------------------------------------------------------------------
+def blame(tr: dict) -> dict:
+    """D10: GPU-idleness blame of a trace set (keys line_off, line_kind, line_scope, time, ctx,
+    n_scopes, n_routines).  Returns num [S, R, kmax+1] u64, total [S], gpu_idle [S], blame and
+    share [S, R] f64, kmax.  Raises ValueError on an invalid trace set."""
+    lo, plo = _c(tr["line_off"], np.uint64)
+    lk, plk = _c(tr["line_kind"], np.uint8)
+    ls, pls = _c(tr["line_scope"], np.uint32)
+    t, pt = _c(tr["time"], np.uint64)
+    cx, pcx = _c(tr["ctx"], np.uint32)
+    S, R = int(tr["n_scopes"]), int(tr["n_routines"])
+    nl = len(lk)
+    kmax = int(np.bincount(ls[lk == 1], minlength=S).max()) if (lk == 1).any() and S else 0
+    kmax = max(kmax, 1)
+    num = np.zeros((S, R, kmax + 1), np.uint64)
+    total, idle = np.zeros(S, np.uint64), np.zeros(S, np.uint64)
+    bl, sh = np.zeros((S, R), np.float64), np.zeros((S, R), np.float64)
+    rc = _lib().oracle_blame(nl, plo, plk, pls, pt, pcx, S, R, kmax, num.ctypes.data, total.ctypes.data,
+                             idle.ctypes.data, bl.ctypes.data, sh.ctypes.data)
+    if rc != 0:
+        raise ValueError("invalid trace set")
+    return dict(num=num, total=total, gpu_idle=idle, blame=bl, share=sh, kmax=kmax)

@@ -17,6 +17,10 @@
  *   D3-D6 oracle_cct      — pinned by hand-worked fixtures (tests/golden), brute-force path
  *                           enumeration with exact rationals, conservation, gprof identity
  *   D7 oracle_derive_*    — pinned by closed forms (P:948 W(100,75)=0.25, NaN at S=0, sums)
+ *   D8 oracle_attribute_profiles / oracle_profile_stats — per-record brute force, SPEC stats
+ *   D9 oracle_sparse_build — worked lookups, round trips through an independent decoder
+ *   D10 oracle_blame       — SPEC's worked blame examples, a 1-ns brute force with exact
+ *                           rationals, integer conservation
  * Parity is unpinned against the PAPER (pinned only against our own readings) for the stall
  * taxonomy (R2), the latency-hiding columns (R4) and the instruction mix (R5): the paper
  * gives no numbers for them.  See DESIGN.md §3.
@@ -660,4 +664,96 @@ void oracle_derive_f64(uint64_t rows, const double *V, double *out)
     for (int r = 0; r < O_VALID; r++) o[4 + r] = v[r] / S;
     for (int k = 0; k < 16; k++) o[17 + k] = o_nan();
   }
+}
+
+/* ======================================================================================
+ * D10 — GPU-idleness blame ("it identifies times when all GPU streams are idle
+ * and at least one CPU thread is active. In such cases, it partitions the cost of GPU
+ * idleness among routines being executed by active CPU threads"; SPEC's blame_idleness:
+ * equal division among the active CPU threads; reading R27).
+ * A trace line is a sequence of change points (time, ctx), non-decreasing in time: from
+ * time[i] to time[i+1] the line is in state ctx[i] (GPA NONE = idle); after its last change
+ * point a line is idle.  Lines are grouped into scopes (ranks); for each scope, sweep the
+ * union of its lines' change-point times: on every elementary interval [ta, tb) with all of
+ * the scope's GPU lines idle, gpu_idle += tb-ta; if also k >= 1 CPU lines are active,
+ * total += tb-ta and each active CPU line adds tb-ta to num[scope][its routine][k].
+ * blame = sum_{k=1..kmax} num/k (one division and one addition per k, ascending k);
+ * share = blame / total (NaN when total = 0).  Returns 0, or -1 when a line goes back in
+ * time, a CPU routine id is >= n_routines, a scope has no GPU line, or the lines are not
+ * grouped by non-decreasing scope.
+ * ====================================================================================== */
+static int o_cmp_u64b(const void *a, const void *b)
+{
+  uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : x > y;
+}
+
+int oracle_blame(uint32_t n_lines, const uint64_t *line_off, const uint8_t *line_kind, const uint32_t *line_scope,
+                 const uint64_t *time, const uint32_t *ctx, uint32_t n_scopes, uint32_t n_routines, uint32_t kmax,
+                 uint64_t *num, uint64_t *total, uint64_t *gpu_idle, double *blame, double *share)
+{
+  const uint64_t kw = (uint64_t)kmax + 1;
+  memset(num, 0, sizeof(uint64_t) * n_scopes * n_routines * kw);
+  memset(total, 0, sizeof(uint64_t) * n_scopes);
+  memset(gpu_idle, 0, sizeof(uint64_t) * n_scopes);
+  for (uint32_t l = 0; l < n_lines; l++) {
+    if (line_scope[l] >= n_scopes || (l && line_scope[l] < line_scope[l - 1])) return -1;
+    for (uint64_t e = line_off[l]; e < line_off[l + 1]; e++) {
+      if (e > line_off[l] && time[e] < time[e - 1]) return -1;
+      if (line_kind[l] == 1 && ctx[e] != O_NONE && ctx[e] >= n_routines && e + 1 < line_off[l + 1]) return -1;
+    }
+  }
+  uint32_t l0 = 0;
+  for (uint32_t sc = 0; sc < n_scopes; sc++) {
+    uint32_t l1 = l0;
+    while (l1 < n_lines && line_scope[l1] == sc) l1++;
+    uint32_t n_gpu = 0, n_cpu = 0;
+    uint64_t n_ev = 0;
+    for (uint32_t l = l0; l < l1; l++) {
+      if (line_kind[l] == 0) n_gpu++; else n_cpu++;
+      n_ev += line_off[l + 1] - line_off[l];
+    }
+    if (n_gpu == 0 || n_cpu > kmax) return -1;
+    uint64_t *ts = (uint64_t *)malloc(sizeof(uint64_t) * (n_ev ? n_ev : 1));
+    uint64_t *cur = (uint64_t *)calloc(l1 - l0 + 1, sizeof(uint64_t));
+    uint64_t m = 0;
+    for (uint32_t l = l0; l < l1; l++)
+      for (uint64_t e = line_off[l]; e < line_off[l + 1]; e++) ts[m++] = time[e];
+    qsort(ts, m, sizeof(uint64_t), o_cmp_u64b);
+    for (uint64_t i = 0; i + 1 < m; i++) {
+      const uint64_t ta = ts[i], tb = ts[i + 1];
+      if (ta == tb) continue;
+      uint32_t cov = 0, k = 0;
+      for (uint32_t l = l0; l < l1; l++) {   /* state of every line on [ta, tb) */
+        const uint64_t len = line_off[l + 1] - line_off[l];
+        while (cur[l - l0] < len && time[line_off[l] + cur[l - l0]] <= ta) cur[l - l0]++;
+        const uint64_t c = cur[l - l0];
+        const int active = c > 0 && c < len && ctx[line_off[l] + c - 1] != O_NONE;
+        if (active) { if (line_kind[l] == 0) cov++; else k++; }
+      }
+      if (cov) continue;
+      gpu_idle[sc] += tb - ta;
+      if (!k) continue;
+      total[sc] += tb - ta;
+      for (uint32_t l = l0; l < l1; l++) {
+        if (line_kind[l] != 1) continue;
+        const uint64_t len = line_off[l + 1] - line_off[l], c = cur[l - l0];
+        if (c > 0 && c < len && ctx[line_off[l] + c - 1] != O_NONE)
+          num[((uint64_t)sc * n_routines + ctx[line_off[l] + c - 1]) * kw + k] += tb - ta;
+      }
+    }
+    free(ts);
+    free(cur);
+    l0 = l1;
+  }
+  if (l0 != n_lines) return -1;
+  for (uint32_t sc = 0; sc < n_scopes; sc++)
+    for (uint32_t r = 0; r < n_routines; r++) {
+      const uint64_t *v = num + ((uint64_t)sc * n_routines + r) * kw;
+      double b = 0.0;
+      for (uint32_t k = 1; k <= kmax; k++) b = b + (double)v[k] / (double)k;
+      blame[(uint64_t)sc * n_routines + r] = b;
+      share[(uint64_t)sc * n_routines + r] = total[sc] ? b / (double)total[sc] : o_nan();
+    }
+  return 0;
 }
