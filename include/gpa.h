@@ -273,6 +273,38 @@ GPA_API gpa_status gpa_sparse_build(gpa_structure s, const uint64_t *d_prof_hist
 GPA_API gpa_status gpa_get_sparse_view(gpa_sparse sp, gpa_sparse_view *out);
 GPA_API void gpa_free_sparse(gpa_sparse sp);
 
+/* ---- f4: GPU-idleness blame over trace lines ----------------------------------------------
+ * PAPER.md §6.2: "identifies times when all GPU streams are idle and at least one
+ * CPU thread is active. In such cases, it partitions the cost of GPU idleness among routines
+ * being executed by active CPU threads" (normalized blame per CPU routine).  DESIGN.md R27:
+ * a trace line is a sequence of change points (time, ctx), non-decreasing in time; on
+ * [time[i], time[i+1]) the line is in state ctx[i] (GPA_NONE = idle); after its last change
+ * point it is idle (the last ctx is ignored).  GPU lines are streams (ctx = any kernel id),
+ * CPU lines are threads (ctx = routine id < n_routines, already mapped to the attribution
+ * depth by the caller).  Lines are grouped into scopes (ranks).  Per scope, on every interval
+ * where all its GPU lines are idle: gpu_idle += length; if k >= 1 of its CPU lines are
+ * active: total += length and each active thread's routine gets length/k.  Outputs:
+ * blame f64 [n_scopes][n_routines] = sum_k num_k / k with num_k the exact integer time
+ * routine r was blamed while k threads were active (ascending k, one IEEE division and
+ * addition each), share = blame / total (canonical NaN when total = 0), total and
+ * gpu_idle u64 [n_scopes] (ns).  Any output pointer may be NULL.  Events are device arrays
+ * d_time u64 [E] and d_ctx u32 [E], E = line_off[n_lines] <= 2^27, laid out line after line.
+ * Errors: GPA_ERR_INVALID_ARG for a malformed line table (line_off not starting at 0 or
+ * decreasing, line_scope decreasing or >= n_scopes, kind not 0/1, a scope without a GPU
+ * line), a line going back in time or a CPU routine id >= n_routines (detected on the device;
+ * the call synchronizes `stream`); GPA_ERR_UNSUPPORTED beyond the size limits (E > 2^27,
+ * > 65535 lines of a kind per scope, E * max CPU lines per scope >= 2^32). */
+typedef struct {
+  uint32_t n_lines;
+  const uint64_t *line_off;   /* HOST [n_lines+1] event offsets, line_off[0] = 0          */
+  const uint8_t *line_kind;   /* HOST [n_lines] 0 = GPU stream, 1 = CPU thread            */
+  const uint32_t *line_scope; /* HOST [n_lines] scope (rank) id, non-decreasing            */
+  uint32_t n_scopes, n_routines;
+} gpa_trace_desc;
+GPA_API gpa_status gpa_idleness_blame(const gpa_trace_desc *desc, const uint64_t *d_time, const uint32_t *d_ctx,
+                                      double *d_blame, double *d_share, uint64_t *d_total, uint64_t *d_gpu_idle,
+                                      int device, gpa_stream_t stream);
+
 /* ---- a-6..a-9: approximate GPU calling-context tree (§5.3) -----------------
  * From a per-instruction histogram: Step 1 edge weights w_e = sum_{r<12} H[call_inst[e]][r]
  * (R10); Step 2 zero-weight propagation to the least fixpoint (R11) and the

@@ -86,6 +86,26 @@ struct DeviceGuard {
   }
 };
 
+namespace {
+struct PoolScratch {  // stream-ordered scratch, released on the stream at scope exit
+  cudaStream_t st;
+  std::vector<void *> ptrs;
+  explicit PoolScratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  cudaError_t get(T **p, uint64_t count) {
+    void *q = nullptr;
+    cudaError_t e = pool_alloc(&q, count ? count * sizeof(T) : 8, st);
+    if (e == cudaSuccess) ptrs.push_back(q);
+    *p = (T *)q;
+    return e;
+  }
+  ~PoolScratch() {
+    for (void *p : ptrs)
+      if (cudaFreeAsync(p, st) != cudaSuccess) cudaGetLastError();
+  }
+};
+}  // namespace
+
 // Everything validation derives on the way (needed again by the loader).
 struct Derived {
   std::vector<uint32_t> inst_func;     // function of each instruction
@@ -860,6 +880,123 @@ gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint3
   DeviceGuard g(s->device);
   CU(g.err);
   CU(launch_profile_stats(d_prof_hist, n_profiles, s->info.n_func, d_stats, (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, const uint32_t *d_ctx, double *d_blame,
+                              double *d_share, uint64_t *d_total, uint64_t *d_gpu_idle, int device,
+                              gpa_stream_t stream) {
+  if (!d || (d->n_lines && (!d->line_off || !d->line_kind || !d->line_scope)))
+    return fail(GPA_ERR_INVALID_ARG, "NULL trace descriptor array");
+  if (d->n_scopes == 0 || d->n_routines == 0) return fail(GPA_ERR_INVALID_ARG, "n_scopes and n_routines must be > 0");
+  const uint32_t L = d->n_lines, S = d->n_scopes, R = d->n_routines;
+  if (L == 0 || d->line_off[0] != 0) return fail(GPA_ERR_INVALID_ARG, "line_off[0] must be 0 (and n_lines > 0)");
+  std::vector<uint32_t> n_gpu(S, 0), n_cpu(S, 0);
+  for (uint32_t l = 0; l < L; l++) {
+    if (d->line_off[l + 1] < d->line_off[l]) return fail(GPA_ERR_INVALID_ARG, "line_off decreases at line %u", l);
+    if (d->line_scope[l] >= S || (l && d->line_scope[l] < d->line_scope[l - 1]))
+      return fail(GPA_ERR_INVALID_ARG, "line_scope[%u] out of range or not grouped", l);
+    if (d->line_kind[l] > 1) return fail(GPA_ERR_INVALID_ARG, "line_kind[%u] = %u", l, d->line_kind[l]);
+    (d->line_kind[l] ? n_cpu : n_gpu)[d->line_scope[l]]++;
+  }
+  uint32_t kmax = 1;
+  for (uint32_t sc = 0; sc < S; sc++) {
+    if (!n_gpu[sc]) return fail(GPA_ERR_INVALID_ARG, "scope %u has no GPU line", sc);
+    if (n_gpu[sc] > 65535 || n_cpu[sc] > 65535) return fail(GPA_ERR_UNSUPPORTED, "scope %u has > 65535 lines", sc);
+    kmax = std::max(kmax, n_cpu[sc]);
+  }
+  const uint64_t n = d->line_off[L];
+  if (n > (1ull << 27)) return fail(GPA_ERR_UNSUPPORTED, "%llu events > 2^27", (unsigned long long)n);
+  if (n * kmax >= (1ull << 32)) return fail(GPA_ERR_UNSUPPORTED, "events x CPU lines per scope >= 2^32");
+  if (n && (!d_time || !d_ctx)) return fail(GPA_ERR_INVALID_ARG, "NULL event arrays");
+  DeviceGuard g(device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+
+  // merge plan: per scope, the non-empty lines are the sorted runs; pair adjacent runs per round
+  std::vector<std::vector<std::pair<uint64_t, uint64_t>>> runs(S);
+  size_t max_runs = 1;
+  for (uint32_t l = 0; l < L; l++)
+    if (d->line_off[l + 1] > d->line_off[l]) runs[d->line_scope[l]].push_back({d->line_off[l], d->line_off[l + 1]});
+  for (auto &r : runs) max_runs = std::max(max_runs, r.size());
+  int rounds = 1;
+  while ((size_t(1) << rounds) < max_runs) rounds++;
+  std::vector<MergePair> pairs;
+  std::vector<uint64_t> chunks;
+  std::vector<uint32_t> round_np;
+  for (int r = 0; r < rounds; r++) {
+    uint32_t np = 0;
+    uint64_t c = 0;
+    chunks.push_back(0);
+    for (auto &rs : runs) {
+      std::vector<std::pair<uint64_t, uint64_t>> next;
+      for (size_t i = 0; i < rs.size(); i += 2) {
+        MergePair p{rs[i].first, rs[i].second, i + 1 < rs.size() ? rs[i + 1].second : rs[i].second};
+        pairs.push_back(p);
+        c += (p.b1 - p.a0 + kMergeChunkHost - 1) / kMergeChunkHost;
+        chunks.push_back(c);
+        next.push_back({p.a0, p.b1});
+        np++;
+      }
+      rs.swap(next);
+    }
+    round_np.push_back(np);
+  }
+
+  PoolScratch mem(st);
+  BlameArgs a{};
+  a.n = n; a.n_scopes = S; a.n_routines = R; a.kmax = kmax;
+  a.time = d_time; a.ctx = d_ctx;
+  a.blame = d_blame; a.share = d_share; a.total = d_total; a.gpu_idle = d_gpu_idle;
+  uint64_t *d_off = nullptr, *t0 = nullptr, *t1 = nullptr, *d_chunks = nullptr;
+  uint8_t *d_kind = nullptr;
+  uint32_t *d_scope = nullptr, *i0 = nullptr, *i1 = nullptr, *line_of = nullptr;
+  MergePair *d_pairs = nullptr;
+  const uint64_t nsr = (uint64_t)S * R * (kmax + 1);
+  CU(mem.get(&d_off, L + 1));
+  CU(mem.get(&d_kind, L));
+  CU(mem.get(&d_scope, L));
+  CU(mem.get(&d_pairs, pairs.size()));
+  CU(mem.get(&d_chunks, chunks.size()));
+  CU(mem.get(&t0, n)); CU(mem.get(&t1, n)); CU(mem.get(&i0, n)); CU(mem.get(&i1, n)); CU(mem.get(&line_of, n));
+  CU(mem.get(&a.pos, n)); CU(mem.get(&a.delta, n)); CU(mem.get(&a.scan, n)); CU(mem.get(&a.psc, n));
+  CU(mem.get(&a.bidx, n)); CU(mem.get(&a.pk, n)); CU(mem.get(&a.cnt, n)); CU(mem.get(&a.pdur, n));
+  CU(mem.get(&a.bs, 65536)); CU(mem.get(&a.err, 1)); CU(mem.get(&a.tots, 4));
+  CU(mem.get(&a.acc, 2ull * S)); CU(mem.get(&a.num, nsr));
+  CU(cudaMemcpyAsync(d_off, d->line_off, (L + 1) * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_kind, d->line_kind, L, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_scope, d->line_scope, L * 4, cudaMemcpyHostToDevice, st));
+  if (!pairs.empty()) CU(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(MergePair), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_chunks, chunks.data(), chunks.size() * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(a.err, 0, 4, st));
+  CU(cudaMemsetAsync(a.acc, 0, 16ull * S, st));
+  CU(cudaMemsetAsync(a.num, 0, nsr * 8, st));
+  a.line_off = d_off; a.line_kind = d_kind; a.line_scope = d_scope; a.line_of = line_of;
+  if (n) {
+    CU(blame_line_of(d_off, L, n, line_of, st));
+    const uint64_t *src_t = d_time;
+    const uint32_t *src_i = nullptr;
+    uint64_t *dst_t = t0;
+    uint32_t *dst_i = i0;
+    size_t pofs = 0, cofs = 0;
+    for (int r = 0; r < rounds; r++) {
+      const uint32_t np = round_np[r];
+      CU(blame_merge(d_pairs + pofs, d_chunks + cofs, np, chunks[cofs + np], src_t, src_i, dst_t, dst_i, st));
+      pofs += np;
+      cofs += np + 1;
+      src_t = dst_t; src_i = dst_i;
+      dst_t = dst_t == t0 ? t1 : t0;
+      dst_i = dst_i == i0 ? i1 : i0;
+    }
+    a.st = src_t;
+    a.ord = src_i;
+  }
+  CU(blame_sweep(a, st));
+  uint32_t h_err = 0;
+  CU(cudaMemcpyAsync(&h_err, a.err, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (h_err & 1) return fail(GPA_ERR_INVALID_ARG, "a trace line goes back in time");
+  if (h_err & 2) return fail(GPA_ERR_INVALID_ARG, "a CPU routine id is >= n_routines");
   return GPA_OK;
 }
 

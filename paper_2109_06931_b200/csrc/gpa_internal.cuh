@@ -135,6 +135,32 @@ cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_ins
                                       cudaStream_t st);
 cudaError_t launch_profile_stats(const uint64_t *d_ph, uint32_t n_prof, uint32_t rows, double *d_stats,
                                  cudaStream_t st);
+// GPU-idleness blame (k_blame.cu)
+constexpr int kMergeChunkHost = 32;  // outputs per merge thread (k_blame.cu)
+struct MergePair {
+  uint64_t a0, a1, b1;  // merge [a0, a1) with [a1, b1)
+};
+struct BlameArgs {
+  uint64_t n;
+  uint32_t n_scopes, n_routines, kmax;
+  const uint32_t *ord, *line_of;
+  const uint64_t *line_off;
+  const uint8_t *line_kind;
+  const uint32_t *line_scope;
+  const uint64_t *time;
+  const uint32_t *ctx;
+  const uint64_t *st;
+  uint32_t *pos, *delta, *scan, *psc, *bidx, *pk, *cnt, *bs, *err;
+  uint64_t *pdur;
+  unsigned long long *tots, *acc, *num;
+  double *blame, *share;
+  uint64_t *total, *gpu_idle;
+};
+cudaError_t blame_line_of(const uint64_t *line_off, uint32_t n_lines, uint64_t n, uint32_t *line_of, cudaStream_t st);
+cudaError_t blame_merge(const MergePair *pairs, const uint64_t *chunk_start, uint32_t np, uint64_t n_chunks,
+                        const uint64_t *st_in, const uint32_t *si, uint64_t *dt, uint32_t *di, cudaStream_t st);
+cudaError_t blame_sweep(const BlameArgs &a, cudaStream_t st);
+
 // sparse cubes (k_sparse.cu): counts + offsets (tot[0] values, tot[1] index entries), then the write
 cudaError_t sparse_count(const uint64_t *H, uint32_t P, uint32_t C, bool cms, uint32_t *ov, uint32_t *oi,
                          uint32_t *bs, unsigned long long *tot, cudaStream_t st);

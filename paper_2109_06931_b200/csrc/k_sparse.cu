@@ -82,17 +82,6 @@ __global__ void k_sparse_write(Geo g, const uint64_t *__restrict__ H, const uint
   }
 }
 
-cudaError_t scan_u32(uint32_t *v, uint64_t m, uint32_t *bs, unsigned long long *total, cudaStream_t st) {
-  uint64_t nb = (m + kScanTile - 1) / kScanTile;
-  if (nb > 65536) return cudaErrorInvalidValue;
-  if (nb == 0) nb = 1;
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(v, m, bs);
-  k_scan_top<<<1, kScanThreads, 0, st>>>(bs, (uint32_t)nb, total);
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(v, m, bs);
-  count_launches(3);
-  return cudaGetLastError();
-}
-
 unsigned grid(uint64_t n) {
   uint64_t b = (n + 255) / 256;
   return (unsigned)(b < 148 * 16 ? (b ? b : 1) : 148 * 16);

@@ -177,4 +177,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t *v, uint64_
 }
 
 }  // namespace
+
+void count_launches(uint64_t k);
+
+namespace {
+// host side: exclusive scan of m u32 values in place on `st`; the total lands in *total (device)
+inline cudaError_t scan_u32(uint32_t *v, uint64_t m, uint32_t *bs, unsigned long long *total, cudaStream_t st) {
+  uint64_t nb = (m + kScanTile - 1) / kScanTile;
+  if (nb > 65536) return cudaErrorInvalidValue;
+  if (nb == 0) nb = 1;
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(v, m, bs);
+  k_scan_top<<<1, kScanThreads, 0, st>>>(bs, (uint32_t)nb, total);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(v, m, bs);
+  count_launches(3);
+  return cudaGetLastError();
+}
+}  // namespace
 }  // namespace gpa

@@ -57,6 +57,11 @@ class CctView(ctypes.Structure):
                 ("func_hist", _vp)]
 
 
+class TraceDesc(ctypes.Structure):
+    _fields_ = [("n_lines", _u32), ("line_off", _vp), ("line_kind", _vp), ("line_scope", _vp),
+                ("n_scopes", _u32), ("n_routines", _u32)]
+
+
 class SparseView(ctypes.Structure):
     _fields_ = [("major", _u32), ("n_planes", _u32), ("n_values", _u64), ("n_index", _u64),
                 ("plane_off", _vp), ("index_off", _vp), ("vals", _vp), ("ids", _vp),
@@ -90,6 +95,7 @@ def _load():
         "gpa_sparse_build": ([_vp, _vp, _u32, ctypes.c_int, ctypes.POINTER(_vp), _vp], S),
         "gpa_get_sparse_view": ([_vp, ctypes.POINTER(SparseView)], S),
         "gpa_free_sparse": ([_vp], None),
+        "gpa_idleness_blame": ([ctypes.POINTER(TraceDesc), _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp], S),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -386,6 +392,24 @@ def sparse_build(s: Structure, prof_hist, n_profiles: int, cms: bool, stream=Non
                                  int(n_profiles), SPARSE_CMS if cms else SPARSE_PMS, ctypes.byref(h),
                                  _stream_ptr(stream, prof_hist.device)), "gpa_sparse_build")
     return Sparse(h, s.device)
+
+
+def idleness_blame(lines: dict, time, ctx, blame=None, share=None, total=None, gpu_idle=None, device: int = 0,
+                   stream=None) -> None:
+    """f4: GPU-idleness blame.  `lines` holds the host line table (line_off u64 [L+1], line_kind u8,
+    line_scope u32, n_scopes, n_routines); time (int64) / ctx (int32) are device tensors of the
+    events; outputs blame / share f64 [S, R], total / gpu_idle int64 [S] (any may be None)."""
+    lo = np.ascontiguousarray(lines["line_off"], np.uint64)
+    lk = np.ascontiguousarray(lines["line_kind"], np.uint8)
+    ls = np.ascontiguousarray(lines["line_scope"], np.uint32)
+    S, R = int(lines["n_scopes"]), int(lines["n_routines"])
+    d = TraceDesc(len(lk), lo.ctypes.data, lk.ctypes.data, ls.ctypes.data, S, R)
+    n = int(lo[-1]) if len(lo) else 0
+    _check(_lib.gpa_idleness_blame(ctypes.byref(d), _ptr(time, "time", 8 * n), _ptr(ctx, "ctx", 4 * n),
+                                   _ptr(blame, "blame", 8 * S * R), _ptr(share, "share", 8 * S * R),
+                                   _ptr(total, "total", 8 * S), _ptr(gpu_idle, "gpu_idle", 8 * S), int(device),
+                                   _stream_ptr(stream, int(device))),
+           "gpa_idleness_blame")
 
 
 def reconstruct_cct(s: Structure, inst_hist, mode: int = WEIGHTS_SAMPLES, max_contexts: int = (1 << 63) - 1,

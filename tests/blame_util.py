@@ -55,3 +55,23 @@ def brute_force(tr):
                 num[(s, r, len(active))] = num.get((s, r, len(active)), 0) + 1
                 blame[s][r] += Fraction(1, len(active))
     return num, total, idle, blame
+
+
+def random_trace(rng, scopes, max_lines=(4, 5), t_max=60, max_events=9):
+    cases = []
+    R = int(rng.integers(1, 5))
+    for _ in range(scopes):
+        lines = []
+        n_gpu, n_cpu = int(rng.integers(1, max_lines[0])), int(rng.integers(0, max_lines[1]))
+        kinds = ["gpu"] * n_gpu + ["cpu"] * n_cpu
+        rng.shuffle(kinds)
+        for k in kinds:
+            m = int(rng.integers(1, max_events))
+            ts = np.sort(rng.integers(0, t_max, m))
+            ev = []
+            for t in ts:
+                idle = rng.random() < 0.4
+                ev.append([int(t), None if idle else int(rng.integers(0, R if k == "cpu" else 9))])
+            lines.append([k, ev])
+        cases.append((R, lines))
+    return from_lines(cases)

@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from gen.trace import trace_set
-from tests.blame_util import NONE, brute_force, from_lines
+from tests.blame_util import brute_force, from_lines, random_trace
 from tests.fixtures import load_golden
 
 G = load_golden("blame_examples.json")["cases"]
@@ -42,30 +42,10 @@ def test_scopes_are_independent():
         assert np.array_equal(r["blame"][s, :R], one["blame"][0])
 
 
-def _random_trace(rng, scopes):
-    cases = []
-    R = int(rng.integers(1, 5))
-    for _ in range(scopes):
-        lines = []
-        n_gpu, n_cpu = int(rng.integers(1, 4)), int(rng.integers(0, 5))
-        kinds = ["gpu"] * n_gpu + ["cpu"] * n_cpu
-        rng.shuffle(kinds)
-        for k in kinds:
-            m = int(rng.integers(1, 9))
-            ts = np.sort(rng.integers(0, 60, m))
-            ev = []
-            for t in ts:
-                idle = rng.random() < 0.4
-                ev.append([int(t), None if idle else int(rng.integers(0, R if k == "cpu" else 9))])
-            lines.append([k, ev])
-        cases.append((R, lines))
-    return from_lines(cases)
-
-
 @pytest.mark.parametrize("seed", range(40))
 def test_brute_force_exact_rationals(seed):
     rng = np.random.default_rng(seed)
-    tr = _random_trace(rng, int(rng.integers(1, 4)))
+    tr = random_trace(rng, int(rng.integers(1, 4)))
     r = oracle.blame(tr)
     num, total, idle, blame = brute_force(tr)
     assert list(r["total"]) == total and list(r["gpu_idle"]) == idle

@@ -1,7 +1,7 @@
 """Measurements of the SURVEY §8f rows built beyond the north-star path (one JSON line each):
 f1 per-profile histograms + cross-profile statistics on C4 (1e9 records, 384 profiles), and
 f3 sparse PMS/CMS encoding of f1's cube, and
-f2 exact-count mode (block counts -> instructions -> exact-mode CCT) on C3's structure.
+f4 GPU-idleness blame on the B3 trace set, and\nf2 exact-count mode (block counts -> instructions -> exact-mode CCT) on C3's structure.
 CUDA events around each call, median of K after W warm-ups."""
 import json
 import os
@@ -96,6 +96,22 @@ def f2():
                       "contexts": c.n, "ms": ms}), flush=True)
 
 
+def f4():
+    """GPU-idleness blame over the B3 trace set (64 ranks x 14 lines, 31 M change points)."""
+    from gen.trace import trace_set
+    tr = trace_set("B3")
+    S, R = tr["n_scopes"], tr["n_routines"]
+    t = torch.from_numpy(tr["time"].view(np.int64)).cuda()
+    c = torch.from_numpy(tr["ctx"].view(np.int32)).cuda()
+    bl = torch.empty((S, R), dtype=torch.float64, device="cuda")
+    sh = torch.empty_like(bl)
+    n = len(tr["time"])
+    ms = timed(lambda: gpa.idleness_blame(tr, t, c, bl, sh))
+    print(json.dumps({"row": "f4", "workload": "B3", "events": n, "ranks": S, "ms": ms,
+                      "events_per_s": n / ms * 1e3, "GBps_12B_per_event": 12 * n / ms / 1e6}), flush=True)
+
+
 if __name__ == "__main__":
-    f1()
-    f2()
+    which = sys.argv[1:] or ["f1", "f2", "f4"]
+    for w in which:
+        globals()[w]()
