@@ -908,6 +908,7 @@ gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, c
   const uint64_t n = d->line_off[L];
   if (n > (1ull << 27)) return fail(GPA_ERR_UNSUPPORTED, "%llu events > 2^27", (unsigned long long)n);
   if (n * kmax >= (1ull << 32)) return fail(GPA_ERR_UNSUPPORTED, "events x CPU lines per scope >= 2^32");
+  if (S >= (1u << 28)) return fail(GPA_ERR_UNSUPPORTED, "n_scopes >= 2^28");
   if (n && (!d_time || !d_ctx)) return fail(GPA_ERR_INVALID_ARG, "NULL event arrays");
   DeviceGuard g(device);
   CU(g.err);
@@ -950,7 +951,7 @@ gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, c
   a.blame = d_blame; a.share = d_share; a.total = d_total; a.gpu_idle = d_gpu_idle;
   uint64_t *d_off = nullptr, *t0 = nullptr, *t1 = nullptr, *d_chunks = nullptr;
   uint8_t *d_kind = nullptr;
-  uint32_t *d_scope = nullptr, *i0 = nullptr, *i1 = nullptr, *line_of = nullptr;
+  uint32_t *d_scope = nullptr, *i0 = nullptr, *i1 = nullptr;
   MergePair *d_pairs = nullptr;
   const uint64_t nsr = (uint64_t)S * R * (kmax + 1);
   CU(mem.get(&d_off, L + 1));
@@ -958,22 +959,29 @@ gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, c
   CU(mem.get(&d_scope, L));
   CU(mem.get(&d_pairs, pairs.size()));
   CU(mem.get(&d_chunks, chunks.size()));
-  CU(mem.get(&t0, n)); CU(mem.get(&t1, n)); CU(mem.get(&i0, n)); CU(mem.get(&i1, n)); CU(mem.get(&line_of, n));
+  CU(mem.get(&t0, n)); CU(mem.get(&t1, n)); CU(mem.get(&i0, n)); CU(mem.get(&i1, n)); CU(mem.get(&a.info, n));
   CU(mem.get(&a.pos, n)); CU(mem.get(&a.delta, n)); CU(mem.get(&a.scan, n)); CU(mem.get(&a.psc, n));
-  CU(mem.get(&a.bidx, n)); CU(mem.get(&a.pk, n)); CU(mem.get(&a.cnt, n)); CU(mem.get(&a.pdur, n));
-  CU(mem.get(&a.bs, 65536)); CU(mem.get(&a.err, 1)); CU(mem.get(&a.tots, 4));
+  CU(mem.get(&a.bidx, n)); CU(mem.get(&a.pk, n)); CU(mem.get(&a.pdur, n));
+  CU(mem.get(&a.ovf, n * kmax / 256 + 1));
+  CU(mem.get(&a.seg, n));
+  CU(mem.get(&a.seg_n, n / 8192 + 1));
+  CU(mem.get(&a.bs, 65536)); CU(mem.get(&a.err, 4)); CU(mem.get(&a.tots, 4));
   CU(mem.get(&a.acc, 2ull * S)); CU(mem.get(&a.num, nsr));
+  uint64_t max_tiles = 0, *d_split = nullptr;
+  for (size_t r = 0, cofs = 0; r < round_np.size(); cofs += round_np[r] + 1, r++)
+    max_tiles = std::max(max_tiles, chunks[cofs + round_np[r]]);
+  CU(mem.get(&d_split, max_tiles + 1));
   CU(cudaMemcpyAsync(d_off, d->line_off, (L + 1) * 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_kind, d->line_kind, L, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_scope, d->line_scope, L * 4, cudaMemcpyHostToDevice, st));
   if (!pairs.empty()) CU(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(MergePair), cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_chunks, chunks.data(), chunks.size() * 8, cudaMemcpyHostToDevice, st));
-  CU(cudaMemsetAsync(a.err, 0, 4, st));
+  CU(cudaMemsetAsync(a.err, 0, 16, st));
   CU(cudaMemsetAsync(a.acc, 0, 16ull * S, st));
   CU(cudaMemsetAsync(a.num, 0, nsr * 8, st));
-  a.line_off = d_off; a.line_kind = d_kind; a.line_scope = d_scope; a.line_of = line_of;
+  a.line_off = d_off; a.line_kind = d_kind; a.line_scope = d_scope;
   if (n) {
-    CU(blame_line_of(d_off, L, n, line_of, st));
+    CU(blame_prep(a, L, st));
     const uint64_t *src_t = d_time;
     const uint32_t *src_i = nullptr;
     uint64_t *dst_t = t0;
@@ -981,7 +989,7 @@ gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, c
     size_t pofs = 0, cofs = 0;
     for (int r = 0; r < rounds; r++) {
       const uint32_t np = round_np[r];
-      CU(blame_merge(d_pairs + pofs, d_chunks + cofs, np, chunks[cofs + np], src_t, src_i, dst_t, dst_i, st));
+      CU(blame_merge(d_pairs + pofs, d_chunks + cofs, np, chunks[cofs + np], src_t, src_i, dst_t, dst_i, d_split, st));
       pofs += np;
       cofs += np + 1;
       src_t = dst_t; src_i = dst_i;

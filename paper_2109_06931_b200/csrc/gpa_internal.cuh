@@ -136,29 +136,32 @@ cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_ins
 cudaError_t launch_profile_stats(const uint64_t *d_ph, uint32_t n_prof, uint32_t rows, double *d_stats,
                                  cudaStream_t st);
 // GPU-idleness blame (k_blame.cu)
-constexpr int kMergeChunkHost = 32;  // outputs per merge thread (k_blame.cu)
+constexpr int kMergeChunkHost = 2048;  // outputs per merge CTA tile (k_blame.cu)
 struct MergePair {
   uint64_t a0, a1, b1;  // merge [a0, a1) with [a1, b1)
 };
 struct BlameArgs {
   uint64_t n;
   uint32_t n_scopes, n_routines, kmax;
-  const uint32_t *ord, *line_of;
+  const uint32_t *ord;
   const uint64_t *line_off;
   const uint8_t *line_kind;
   const uint32_t *line_scope;
   const uint64_t *time;
   const uint32_t *ctx;
   const uint64_t *st;
-  uint32_t *pos, *delta, *scan, *psc, *bidx, *pk, *cnt, *bs, *err;
+  uint32_t *info, *pos /* bpos: first blameable piece at/after each change point */, *delta, *scan, *psc, *bidx, *pk, *bs, *err;
   uint64_t *pdur;
+  uint2 *seg, *ovf;
+  uint32_t *seg_n;
   unsigned long long *tots, *acc, *num;
   double *blame, *share;
   uint64_t *total, *gpu_idle;
 };
-cudaError_t blame_line_of(const uint64_t *line_off, uint32_t n_lines, uint64_t n, uint32_t *line_of, cudaStream_t st);
+cudaError_t blame_prep(const BlameArgs &a, uint32_t n_lines, cudaStream_t st);
 cudaError_t blame_merge(const MergePair *pairs, const uint64_t *chunk_start, uint32_t np, uint64_t n_chunks,
-                        const uint64_t *st_in, const uint32_t *si, uint64_t *dt, uint32_t *di, cudaStream_t st);
+                        const uint64_t *st_in, const uint32_t *si, uint64_t *dt, uint32_t *di, uint64_t *split,
+                        cudaStream_t st);
 cudaError_t blame_sweep(const BlameArgs &a, cudaStream_t st);
 
 // sparse cubes (k_sparse.cu): counts + offsets (tot[0] values, tot[1] index entries), then the write

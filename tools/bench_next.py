@@ -1,7 +1,8 @@
 """Measurements of the SURVEY §8f rows built beyond the north-star path (one JSON line each):
 f1 per-profile histograms + cross-profile statistics on C4 (1e9 records, 384 profiles), and
 f3 sparse PMS/CMS encoding of f1's cube, and
-f4 GPU-idleness blame on the B3 trace set, and\nf2 exact-count mode (block counts -> instructions -> exact-mode CCT) on C3's structure.
+f4 GPU-idleness blame on the B3 trace set, and
+f2 exact-count mode (block counts -> instructions -> exact-mode CCT) on C3's structure.
 CUDA events around each call, median of K after W warm-ups."""
 import json
 import os
