@@ -26,3 +26,28 @@ def reduce_histogram(hist, dst: int = 0, group=None) -> None:
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
     dist.reduce(hist, dst=dst, op=dist.ReduceOp.SUM, group=group)
+
+
+def shard_trace(lines: dict, rank: int, world: int) -> dict:
+    """f4: ranks of a trace set are independent problems, so worker r of N takes
+    the contiguous range of trace ranks whose change points fall in [floor(r*E/N),
+    floor((r+1)*E/N)) by their first change point (balanced by change points; no collective).
+    Returns the sub-table (line_off rebased to 0, line_scope rebased to 0) plus scope0 /
+    event0 / event1: slice the device event arrays with [event0:event1] and write results
+    to rows scope0 .. scope0 + n_scopes of the full outputs."""
+    import numpy as np
+    lo = np.asarray(lines["line_off"], np.uint64)
+    ls = np.asarray(lines["line_scope"], np.uint32)
+    S = int(lines["n_scopes"])
+    E = int(lo[-1]) if len(lo) else 0
+    first = np.searchsorted(ls, np.arange(S + 1), side="left")     # first line of each scope
+    scope_start = lo[np.minimum(first, len(lo) - 1)].astype(np.int64)
+    a, b = shard_range(E, rank, world)
+    s0 = int(np.searchsorted(scope_start[:S], a, side="left")) if rank else 0
+    s1 = int(np.searchsorted(scope_start[:S], b, side="left")) if rank < world - 1 else S
+    l0, l1 = int(first[s0]), int(first[s1])
+    e0, e1 = int(lo[l0]), int(lo[l1])
+    return dict(line_off=(lo[l0:l1 + 1] - np.uint64(e0)).astype(np.uint64),
+                line_kind=np.asarray(lines["line_kind"], np.uint8)[l0:l1],
+                line_scope=(ls[l0:l1] - np.uint32(s0)).astype(np.uint32),
+                n_scopes=s1 - s0, n_routines=int(lines["n_routines"]), scope0=s0, event0=e0, event1=e1)

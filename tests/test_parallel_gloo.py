@@ -62,3 +62,54 @@ def test_shard_range_partitions():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def _blame_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from gen.trace import trace_set
+        from paper_2109_06931_b200.parallel import shard_trace
+        tr = trace_set("B2")
+        sh = shard_trace(tr, rank, world)
+        S = tr["n_scopes"]
+        blame = torch.zeros((S, tr["n_routines"]), dtype=torch.float64)
+        total = torch.zeros(S, dtype=torch.int64)
+        if sh["n_scopes"]:
+            sub = dict(sh, time=tr["time"][sh["event0"]:sh["event1"]], ctx=tr["ctx"][sh["event0"]:sh["event1"]])
+            r = oracle.blame(sub)
+            s0, s1 = sh["scope0"], sh["scope0"] + sh["n_scopes"]
+            blame[s0:s1] = torch.from_numpy(r["blame"])
+            total[s0:s1] = torch.from_numpy(r["total"].view(np.int64))
+        dist.reduce(blame, dst=0)        # disjoint rows: the sum assembles them (test only)
+        dist.reduce(total, dst=0)
+        if rank == 0:
+            np.savez(out_path, blame=blame.numpy(), total=total.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_blame_shards_by_rank(tmp_path, world):
+    """f4: every trace rank lands on exactly one worker and the per-worker results, placed at
+    their scope offsets, equal the single-process oracle bit for bit."""
+    from gen.trace import trace_set
+    out = str(tmp_path / "blame.npz")
+    mp.start_processes(_blame_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
+    got = np.load(out)
+    r = oracle.blame(trace_set("B2"))
+    assert np.array_equal(got["blame"].view(np.uint64), r["blame"].view(np.uint64))
+    assert np.array_equal(got["total"].view(np.uint64), r["total"])
+
+
+def test_shard_trace_partitions():
+    from gen.trace import trace_set
+    from paper_2109_06931_b200.parallel import shard_trace
+    tr = trace_set("B2")
+    for world in (1, 2, 3, 5, 8, 16):
+        parts = [shard_trace(tr, r, world) for r in range(world)]
+        assert parts[0]["scope0"] == 0 and parts[0]["event0"] == 0
+        assert sum(p["n_scopes"] for p in parts) == tr["n_scopes"]
+        assert parts[-1]["event1"] == len(tr["time"])
+        for a, b in zip(parts, parts[1:]):
+            assert a["scope0"] + a["n_scopes"] == b["scope0"] and a["event1"] == b["event0"]
