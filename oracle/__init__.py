@@ -88,6 +88,10 @@ def _lib():
     lib.oracle_derive_u64.restype = None
     lib.oracle_derive_f64.argtypes = [u64, vp, vp]
     lib.oracle_derive_f64.restype = None
+    lib.oracle_cct_profiles.argtypes = [u64, vp, vp, vp, vp, u32, u32, vp, vp, vp]
+    lib.oracle_cct_profiles.restype = None
+    lib.oracle_profile_stats_f64.argtypes = [u32, u64, vp, vp]
+    lib.oracle_profile_stats_f64.restype = None
     lib.oracle_blame.argtypes = [u32, vp, vp, vp, vp, vp, u32, u32, u32, vp, vp, vp, vp, vp]
     lib.oracle_blame.restype = ctypes.c_int
     return lib
@@ -226,6 +230,61 @@ def attribute_profiles(st: dict, rec, n_prof: int):
         _lib().oracle_attribute_profiles(n_inst, pa, pl, pf, n_func, rec.ctypes.data, len(rec), n_prof,
                                          Hp.ctypes.data if Hp.size else None, Up.ctypes.data)
     return Hp, Up
+
+
+def attribute_profiles_inst(st: dict, rec, n_prof: int):
+    """D8 at instruction level: Hp [n_prof+1, n_inst, 16], Up [n_prof+1, 16] (the per-function
+    attribution with every instruction its own row)."""
+    rec = _records(rec)
+    n_inst = len(st["inst_addr"])
+    addr, pa = _c(st["inst_addr"], np.uint64)
+    ln, pl = _c(st["inst_len"], np.uint16)
+    ident, pi = _c(np.arange(n_inst, dtype=np.uint32), np.uint32)
+    Hp = np.zeros((n_prof + 1, n_inst, SLOTS), np.uint64)
+    Up = np.zeros((n_prof + 1, SLOTS), np.uint64)
+    if len(rec):
+        _lib().oracle_attribute_profiles(n_inst, pa, pl, pi, n_inst, rec.ctypes.data, len(rec), n_prof,
+                                         Hp.ctypes.data if Hp.size else None, Up.ctypes.data)
+    return Hp, Up
+
+
+def cct_ctx_func(R: dict) -> np.ndarray:
+    """Function of each context of an oracle CCT (NONE for SCC contexts): FUNC contexts name a
+    trivial DAG node (its single member), SCC_MEMBER contexts name the function."""
+    dag_func = np.full(R["n_dag"], NONE, np.uint32)
+    for f, X in enumerate(R["scc_of"]):
+        if not R["dag_nontrivial"][X]:
+            dag_func[X] = f
+    out = np.full(R["n"], NONE, np.uint32)
+    k, nd = R["kind"], R["node"]
+    out[k == 0] = dag_func[nd[k == 0]]
+    out[k == 2] = nd[k == 2]
+    return out
+
+
+def cct_profiles(R: dict, Hp) -> tuple:
+    """D11: per-profile excl / incl cubes [P1, n, 16] over the aggregate tree R (from cct())."""
+    Hp = np.ascontiguousarray(Hp, np.uint64)
+    P1, n_func, n = Hp.shape[0], Hp.shape[1], R["n"]
+    cf, pcf = _c(cct_ctx_func(R), np.uint32)
+    fr, pfr = _c(R["frac"], np.float64)
+    fc, pfc = _c(R["first_child"], np.uint32)
+    nc, pnc = _c(R["n_children"], np.uint32)
+    E = np.zeros((P1, n, SLOTS), np.float64)
+    I = np.zeros((P1, n, SLOTS), np.float64)
+    if n and P1:
+        _lib().oracle_cct_profiles(n, pcf, pfr, pfc, pnc, P1, n_func, Hp.ctypes.data, E.ctypes.data, I.ctypes.data)
+    return E, I
+
+
+def profile_stats_f64(X, n_prof: int) -> np.ndarray:
+    """D11: statistics of an fp64 cube [>= n_prof, rows, 16] over profiles 0..n_prof-1."""
+    X = np.ascontiguousarray(X, np.float64)
+    rows = X.shape[1]
+    out = np.empty((rows, 6, SLOTS), np.float64)
+    if rows:
+        _lib().oracle_profile_stats_f64(n_prof, rows, X.ctypes.data, out.ctypes.data)
+    return out
 
 
 def profile_stats(Hp, n_prof: int) -> np.ndarray:

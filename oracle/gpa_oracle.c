@@ -19,6 +19,9 @@
  *   D7 oracle_derive_*    — pinned by closed forms (P:948 W(100,75)=0.25, NaN at S=0, sums)
  *   D8 oracle_attribute_profiles / oracle_profile_stats — per-record brute force, SPEC stats
  *   D9 oracle_sparse_build — worked lookups, round trips through an independent decoder
+ *   D11 oracle_cct_profiles / oracle_profile_stats_f64 — the single-profile identity with the
+ *                           aggregate CCT, hand-worked fractions of the Fig.-4 fixture, numpy
+ *                           two-pass statistics
  *   D10 oracle_blame       — SPEC's worked blame examples, a 1-ns brute force with exact
  *                           rationals, integer conservation
  * Parity is unpinned against the PAPER (pinned only against our own readings) for the stall
@@ -756,4 +759,62 @@ int oracle_blame(uint32_t n_lines, const uint64_t *line_off, const uint8_t *line
       share[(uint64_t)sc * n_routines + r] = total[sc] ? b / (double)total[sc] : o_nan();
     }
   return 0;
+}
+
+/* ======================================================================================
+ * D11 — f1 at CCT level (SURVEY §8f f1 "per instruction, function or CCT context"; P:481-487
+ * statistics over thread profiles of each CCT node; P:711-714 values propagated up the CCT).
+ * Reading R28: the unified CCT is the tree reconstructed from the aggregate histogram (R9);
+ * profile p's exclusive value at a FUNC / SCC_MEMBER context c of function g is
+ * excl_p(c)[r] = frac(c) * (double)Hp[p][g][r] (the aggregate formula of D6 with p's function
+ * histogram), 0 at SCC contexts; incl_p(c) = excl_p(c) + the children's incl_p in index order.
+ * ctx_func[c] = the context's function (GPA NONE for SCC contexts).  Cubes are [P1][n][16].
+ * Statistics of fp64 values over profiles 0..n_prof-1 (R28): sum = left fold in profile order,
+ * min, max, mean = sum / P, std = sqrt(sum_p (x - mean)^2 / P) (two passes), cv = std / mean
+ * (0 when mean = 0); all zero when n_prof = 0.  Output [rows][6][16] as in D8.
+ * ====================================================================================== */
+void oracle_cct_profiles(uint64_t n, const uint32_t *ctx_func, const double *frac, const uint32_t *first_child,
+                         const uint32_t *n_children, uint32_t P1, uint32_t n_func, const uint64_t *Hp,
+                         double *excl, double *incl)
+{
+  for (uint32_t p = 0; p < P1; p++) {
+    double *E = excl + (uint64_t)p * n * O_SLOTS, *I = incl + (uint64_t)p * n * O_SLOTS;
+    for (uint64_t c = 0; c < n; c++)
+      for (int r = 0; r < O_SLOTS; r++)
+        E[c * O_SLOTS + r] = ctx_func[c] == O_NONE ? 0.0
+                           : frac[c] * (double)Hp[((uint64_t)p * n_func + ctx_func[c]) * O_SLOTS + r];
+    for (uint64_t c = n; c-- > 0;)
+      for (int r = 0; r < O_SLOTS; r++) {
+        double v = E[c * O_SLOTS + r];
+        for (uint32_t d = first_child[c]; d < first_child[c] + n_children[c]; d++) v = v + I[(uint64_t)d * O_SLOTS + r];
+        I[c * O_SLOTS + r] = v;
+      }
+  }
+}
+
+void oracle_profile_stats_f64(uint32_t n_prof, uint64_t rows, const double *X, double *out)
+{
+  for (uint64_t f = 0; f < rows; f++)
+    for (int r = 0; r < O_SLOTS; r++) {
+      double sum = 0.0, mn = 0.0, mx = 0.0;
+      for (uint32_t p = 0; p < n_prof; p++) {
+        double x = X[((uint64_t)p * rows + f) * O_SLOTS + r];
+        sum = sum + x;
+        if (p == 0 || x < mn) mn = x;
+        if (p == 0 || x > mx) mx = x;
+      }
+      double mean = n_prof ? sum / (double)n_prof : 0.0, ss = 0.0;
+      for (uint32_t p = 0; p < n_prof; p++) {
+        double d = X[((uint64_t)p * rows + f) * O_SLOTS + r] - mean;
+        ss = ss + d * d;
+      }
+      double sd = n_prof ? sqrt(ss / (double)n_prof) : 0.0;
+      double *o = out + f * 6 * O_SLOTS;
+      o[0 * O_SLOTS + r] = sum;
+      o[1 * O_SLOTS + r] = mn;
+      o[2 * O_SLOTS + r] = mean;
+      o[3 * O_SLOTS + r] = mx;
+      o[4 * O_SLOTS + r] = sd;
+      o[5 * O_SLOTS + r] = mean == 0.0 ? 0.0 : sd / mean;
+    }
 }
