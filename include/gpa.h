@@ -247,6 +247,30 @@ GPA_API gpa_status gpa_attribute_profiles(gpa_structure s, const gpa_sample *d_s
 GPA_API gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles,
                                      double *d_stats, gpa_stream_t stream);
 
+/* f1 at instruction and CCT level (SURVEY §8f f1 "per instruction, function or CCT context").
+ * gpa_attribute_profiles_inst: as gpa_attribute_profiles with instruction rows:
+ *   d_prof_inst_hist[(p*n_inst + i)*16 + slot] (n_profiles+1 rows of n_inst x 16 u64).
+ * gpa_profile_stats_rows: the statistics of gpa_profile_stats for any u64 cube of `rows` rows
+ *   ([n_profiles+1][rows][16], profiles 0..n_profiles-1 enter): d_stats [rows][6][16].
+ * gpa_cct_profiles (reading R28): per-profile values on the tree `cct` (reconstructed from the
+ *   aggregate histogram): d_prof_excl[(p*n + c)*16 + r] = frac(c) * d_prof_hist[p][g(c)][r] for
+ *   FUNC / SCC_MEMBER contexts of function g (0 at SCC contexts), d_prof_incl = excl + children's
+ *   incl in child order; d_prof_hist is gpa_attribute_profiles' function cube; both outputs are
+ *   [n_profiles+1][n][16] f64.  Synchronizes the tree's build stream once (level table).
+ * gpa_profile_stats_f64: statistics of an f64 cube [n_profiles+1][rows][16] over profiles
+ *   0..n_profiles-1: sum (left fold in profile order), min, mean = sum/P, max, population std
+ *   = sqrt(sum (x-mean)^2 / P) (two passes), cv = std/mean (0 when mean = 0) -> [rows][6][16].
+ * All enqueue on `stream` (device memory of `device` for the two rows-only calls). */
+GPA_API gpa_status gpa_attribute_profiles_inst(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+                                               uint32_t n_profiles, uint64_t *d_prof_inst_hist,
+                                               uint64_t *d_prof_unattr, gpa_stream_t stream);
+GPA_API gpa_status gpa_profile_stats_rows(uint64_t rows, const uint64_t *d_prof_hist, uint32_t n_profiles,
+                                          double *d_stats, int device, gpa_stream_t stream);
+GPA_API gpa_status gpa_cct_profiles(gpa_structure s, gpa_cct cct, const uint64_t *d_prof_hist, uint32_t n_profiles,
+                                    double *d_prof_excl, double *d_prof_incl, gpa_stream_t stream);
+GPA_API gpa_status gpa_profile_stats_f64(uint64_t rows, const double *d_prof_vals, uint32_t n_profiles,
+                                         double *d_stats, int device, gpa_stream_t stream);
+
 /* ---- f3: sparse cubes (PMS / CMS) of the per-profile histograms -------------------------
  * PAPER.md §5.2: "Profile Major Sparse" and "CCT Major Sparse" formats, one modified
  * CSR per plane.  The cube is d_prof_hist of gpa_attribute_profiles with all n_profiles+1

@@ -755,6 +755,7 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
     CC(calloc_dev(c, &c->incl, nb * SLOTS));
     uint32_t *d_lev = nullptr;
     CC(calloc_dev(c, &d_lev, 1100));
+    c->d_lev = d_lev; c->lev_fmt = 1; c->lev_len = 1100;
     CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
     CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CC(cudaStreamSynchronize(st));
@@ -802,6 +803,7 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   if (cct_small_ok(s, n)) {  // one CTA builds the whole tree: no per-level launches or syncs
     uint32_t *d_lev = nullptr;
     CC(calloc_dev(c, &d_lev, 1100));
+    c->d_lev = d_lev; c->lev_fmt = 1; c->lev_len = 1100;
     CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
     *out = c;
     return GPA_OK;
@@ -815,6 +817,7 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
     CC(calloc_dev(c, &d_lev, max_lev + 2));
     cudaError_t e = launch_cct_coop(s, c, d_tmp, d_bs, d_lev, max_lev, d_cnt + 1, sm_count(s->device), st);
     if (e == cudaSuccess) {
+      c->d_lev = d_lev; c->lev_fmt = 2; c->lev_len = max_lev + 2;
       CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
       CC(cudaStreamSynchronize(st));
       if (h_cnt[1] != n) {
@@ -880,6 +883,83 @@ gpa_status gpa_profile_stats(gpa_structure s, const uint64_t *d_prof_hist, uint3
   DeviceGuard g(s->device);
   CU(g.err);
   CU(launch_profile_stats(d_prof_hist, n_profiles, s->info.n_func, d_stats, (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_attribute_profiles_inst(gpa_structure s, const gpa_sample *d_samples, uint64_t n, uint32_t n_profiles,
+                                       uint64_t *d_prof_inst_hist, uint64_t *d_prof_unattr, gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (n == 0) return GPA_OK;
+  if (!d_samples || !d_prof_unattr || (!d_prof_inst_hist && s->info.n_inst))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer with n=%llu", (unsigned long long)n);
+  if ((uintptr_t)d_samples & 15) return fail(GPA_ERR_INVALID_ARG, "d_samples is not 16-byte aligned");
+  if (n_profiles > 65536) return fail(GPA_ERR_INVALID_ARG, "n_profiles %u > 65536", n_profiles);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
+  CU(launch_attribute_profiles_inst(s->attr, s->info.n_inst, d_samples, n, n_profiles,
+                                    (unsigned long long *)d_prof_inst_hist, (unsigned long long *)d_prof_unattr,
+                                    sm_count(s->device), (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_profile_stats_rows(uint64_t rows, const uint64_t *d_prof_hist, uint32_t n_profiles, double *d_stats,
+                                  int device, gpa_stream_t stream) {
+  if (!rows) return GPA_OK;
+  if (!d_prof_hist || !d_stats) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  if (rows >= (1ull << 32)) return fail(GPA_ERR_UNSUPPORTED, "rows >= 2^32");
+  DeviceGuard g(device);
+  CU(g.err);
+  CU(launch_profile_stats(d_prof_hist, n_profiles, (uint32_t)rows, d_stats, (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_profile_stats_f64(uint64_t rows, const double *d_prof_vals, uint32_t n_profiles, double *d_stats,
+                                 int device, gpa_stream_t stream) {
+  if (!rows) return GPA_OK;
+  if (!d_prof_vals || !d_stats) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  DeviceGuard g(device);
+  CU(g.err);
+  CU(launch_profile_stats_f64(d_prof_vals, n_profiles, rows, d_stats, (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+// BFS level boundaries of a tree, whichever build path made it (synchronizes c->stream once)
+static gpa_status cct_levels(gpa_cct_s *c) {
+  if (!c->level_start.empty() || c->n == 0) return GPA_OK;
+  if (!c->d_lev) return fail(GPA_ERR_INTERNAL, "tree has no level table");
+  std::vector<uint32_t> h(c->lev_len);
+  CU(cudaMemcpyAsync(h.data(), c->d_lev, 4ull * c->lev_len, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  std::vector<uint64_t> ls;
+  if (c->lev_fmt == 1) {
+    const uint32_t L = h[0];
+    for (uint32_t l = 0; l <= L && 1 + l < c->lev_len; l++) ls.push_back(h[1 + l]);
+  } else {
+    ls.push_back(h[0]);
+    for (uint32_t l = 1; l < c->lev_len && ls.back() < c->n; l++) ls.push_back(h[l]);
+  }
+  if (ls.empty() || ls.front() != 0 || ls.back() != c->n)
+    return fail(GPA_ERR_INTERNAL, "inconsistent level table (%zu levels)", ls.size());
+  c->level_start = ls;
+  return GPA_OK;
+}
+
+gpa_status gpa_cct_profiles(gpa_structure s, gpa_cct cct, const uint64_t *d_prof_hist, uint32_t n_profiles,
+                            double *d_prof_excl, double *d_prof_incl, gpa_stream_t stream) {
+  if (!s || !cct) return fail(GPA_ERR_INVALID_ARG, "NULL handle");
+  if (cct->n == 0) return GPA_OK;
+  if (!d_prof_hist || !d_prof_excl || !d_prof_incl) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  if (n_profiles > 65536) return fail(GPA_ERR_INVALID_ARG, "n_profiles %u > 65536", n_profiles);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  gpa_status r = cct_levels(cct);
+  if (r != GPA_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t P1 = n_profiles + 1;
+  CU(launch_cct_prof_excl(s, cct, d_prof_hist, P1, d_prof_excl, st));
+  for (size_t L = cct->level_start.size() - 1; L-- > 0;)
+    CU(launch_cct_prof_incl_level(cct, cct->level_start[L], cct->level_start[L + 1], P1, d_prof_excl, d_prof_incl, st));
   return GPA_OK;
 }
 

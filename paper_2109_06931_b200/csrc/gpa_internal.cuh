@@ -96,6 +96,12 @@ struct gpa_cct_s {
   uint64_t *w = nullptr, *W = nullptr, *S_f = nullptr;
   uint8_t *dag_active = nullptr, *func_active = nullptr;
   std::vector<uint64_t> level_start;  // contexts of BFS level L: [level_start[L], level_start[L+1])
+  // device level table of the one-kernel builds (read back lazily by gpa_cct_profiles):
+  // lev_fmt 1 = k_cct_small (lev[0] = levels, lev[1 + l] = first context of level l),
+  // lev_fmt 2 = k_cct_coop (lev[l] = first context of level l, up to lev_len entries)
+  uint32_t *d_lev = nullptr;
+  int lev_fmt = 0;
+  uint32_t lev_len = 0;
   std::vector<void *> allocs;
 };
 
@@ -133,6 +139,15 @@ cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_ins
                                       const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
                                       unsigned long long *d_ph, unsigned long long *d_pu, int sm_count,
                                       cudaStream_t st);
+cudaError_t launch_attribute_profiles_inst(const AttrTables &T, uint32_t n_inst, const gpa_sample *d_samples,
+                                           uint64_t n, uint32_t n_prof, unsigned long long *d_ph,
+                                           unsigned long long *d_pu, int sm_count, cudaStream_t st);
+cudaError_t launch_profile_stats_f64(const double *d_x, uint32_t n_prof, uint64_t rows, double *d_stats,
+                                     cudaStream_t st);
+cudaError_t launch_cct_prof_excl(const gpa_structure_s *s, const gpa_cct_s *c, const uint64_t *d_ph, uint32_t P1,
+                                 double *d_excl, cudaStream_t st);
+cudaError_t launch_cct_prof_incl_level(const gpa_cct_s *c, uint64_t a, uint64_t b, uint32_t P1, const double *d_excl,
+                                       double *d_incl, cudaStream_t st);
 cudaError_t launch_profile_stats(const uint64_t *d_ph, uint32_t n_prof, uint32_t rows, double *d_stats,
                                  cudaStream_t st);
 // GPU-idleness blame (k_blame.cu)

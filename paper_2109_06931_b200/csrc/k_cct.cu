@@ -274,6 +274,41 @@ __global__ void k_incl_level(uint64_t a, uint64_t b, const uint32_t *first_child
   }
 }
 
+// f1 at CCT level (R28): profile p's excl = frac * p's function histogram; incl level by level
+__global__ void k_cct_prof_excl(uint64_t n, uint32_t P1, uint32_t n_func, const uint8_t *__restrict__ kind,
+                                const uint32_t *__restrict__ node, const double *__restrict__ frac,
+                                const uint32_t *__restrict__ dmem_ptr, const uint32_t *__restrict__ dmem,
+                                const uint64_t *__restrict__ PH, double *__restrict__ excl) {
+  const uint64_t per = n * GPA_SLOTS;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < per * P1;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = x / per, y = x - p * per, c = y >> 4;
+    const int r = (int)(y & 15);
+    const uint8_t k = kind[c];
+    double v = 0.0;
+    if (k != GPA_CTX_SCC) {
+      const uint32_t g = k == GPA_CTX_SCC_MEMBER ? node[c] : dmem[dmem_ptr[node[c]]];
+      v = __dmul_rn(frac[c], __ull2double_rn(PH[(p * n_func + g) * GPA_SLOTS + r]));
+    }
+    excl[x] = v;
+  }
+}
+
+__global__ void k_cct_prof_incl_level(uint64_t n, uint64_t a, uint64_t b, uint32_t P1,
+                                      const uint32_t *__restrict__ first_child, const uint32_t *__restrict__ n_children,
+                                      const double *__restrict__ excl, double *__restrict__ incl) {
+  const uint64_t w = (b - a) * GPA_SLOTS;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < w * P1; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = x / w, y = a * GPA_SLOTS + (x - p * w), c = y >> 4;
+    const int r = (int)(y & 15);
+    const double *I = incl + p * n * GPA_SLOTS;
+    double v = excl[p * n * GPA_SLOTS + y];
+    const uint32_t d0 = first_child[c], nc = n_children[c];
+    for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, I[(uint64_t)d * GPA_SLOTS + r]);
+    incl[p * n * GPA_SLOTS + y] = v;
+  }
+}
+
 // Whole Step 4 in one CTA for small trees (the common case: C1, C2, C4, C5 have <= 2^15
 // contexts): roots, every BFS level (count -> block scan -> write), excl, and the reverse
 // incl fold, separated by __syncthreads instead of kernel launches and host syncs.
@@ -521,6 +556,23 @@ LevelArgs level_args(const gpa_structure_s *s, gpa_cct_s *c) {
 }
 
 }  // namespace
+
+cudaError_t launch_cct_prof_excl(const gpa_structure_s *s, const gpa_cct_s *c, const uint64_t *d_ph, uint32_t P1,
+                                 double *d_excl, cudaStream_t st) {
+  k_cct_prof_excl<<<grid_for(c->n * GPA_SLOTS * P1, 256), 256, 0, st>>>(
+      c->n, P1, s->info.n_func, c->kind, c->node, c->frac, s->d_dmem_ptr, s->d_dmem, d_ph, d_excl);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cct_prof_incl_level(const gpa_cct_s *c, uint64_t a, uint64_t b, uint32_t P1, const double *d_excl,
+                                       double *d_incl, cudaStream_t st) {
+  if (b <= a) return cudaSuccess;
+  k_cct_prof_incl_level<<<grid_for((b - a) * GPA_SLOTS * P1, 256), 256, 0, st>>>(c->n, a, b, P1, c->first_child,
+                                                                                  c->n_children, d_excl, d_incl);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist, uint64_t *d_w, cudaStream_t st) {
   uint32_t n = s->info.n_call;

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int u = 0; u < kUnroll; u++) {
       uint32_t i = lookup<MODE>(T, ((uint64_t)v[u].y << 32) | v[u].x);
-      f[u] = i == NONE ? NONE : __ldg(inst_func + i);
+      f[u] = i == NONE ? NONE : (inst_func ? __ldg(inst_func + i) : i);  // inst_func NULL: instruction rows
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; u++) {
@@ -234,7 +234,63 @@ __global__ void k_prof_stats(const uint64_t *__restrict__ PH, uint32_t n_prof, u
   }
 }
 
+// fp64 cube statistics (R28): left-fold sum, min, max, mean, two-pass population std, cv
+__global__ void k_prof_stats_f64(const double *__restrict__ X, uint32_t n_prof, uint64_t rows,
+                                 double *__restrict__ out) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < rows * GPA_SLOTS;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = x >> 4;
+    const int r = (int)(x & 15);
+    double sum = 0.0, mn = 0.0, mx = 0.0;
+    for (uint32_t p = 0; p < n_prof; p++) {
+      const double v = __ldg(X + ((uint64_t)p * rows + f) * GPA_SLOTS + r);
+      sum = __dadd_rn(sum, v);
+      if (p == 0 || v < mn) mn = v;
+      if (p == 0 || v > mx) mx = v;
+    }
+    const double mean = n_prof ? __ddiv_rn(sum, __uint2double_rn(n_prof)) : 0.0;
+    double ss = 0.0;
+    for (uint32_t p = 0; p < n_prof; p++) {
+      const double d = __dsub_rn(__ldg(X + ((uint64_t)p * rows + f) * GPA_SLOTS + r), mean);
+      ss = __dadd_rn(ss, __dmul_rn(d, d));
+    }
+    const double sd = n_prof ? __dsqrt_rn(__ddiv_rn(ss, __uint2double_rn(n_prof))) : 0.0;
+    double *o = out + f * 6 * GPA_SLOTS;
+    o[0 * GPA_SLOTS + r] = sum;
+    o[1 * GPA_SLOTS + r] = mn;
+    o[2 * GPA_SLOTS + r] = mean;
+    o[3 * GPA_SLOTS + r] = mx;
+    o[4 * GPA_SLOTS + r] = sd;
+    o[5 * GPA_SLOTS + r] = mean == 0.0 ? 0.0 : __ddiv_rn(sd, mean);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_attribute_profiles_inst(const AttrTables &T, uint32_t n_inst, const gpa_sample *d_samples,
+                                           uint64_t n, uint32_t n_prof, unsigned long long *d_ph,
+                                           unsigned long long *d_pu, int sm_count, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  uint64_t per_block = (uint64_t)kThreads * kUnroll;
+  uint64_t want = (n + per_block - 1) / per_block;
+  uint64_t cap = (uint64_t)sm_count * (2048 / kThreads);
+  unsigned blocks = (unsigned)(want < cap ? want : cap);
+  const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
+  if (T.mode == 0) k_attr_prof<0><<<blocks, kThreads, 0, st>>>(T, nullptr, n_inst, rec, n, n_prof, d_ph, d_pu);
+  else k_attr_prof<1><<<blocks, kThreads, 0, st>>>(T, nullptr, n_inst, rec, n, n_prof, d_ph, d_pu);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_profile_stats_f64(const double *d_x, uint32_t n_prof, uint64_t rows, double *d_stats,
+                                     cudaStream_t st) {
+  if (!rows) return cudaSuccess;
+  uint64_t blocks = (rows * GPA_SLOTS + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_prof_stats_f64<<<(unsigned)blocks, 256, 0, st>>>(d_x, n_prof, rows, d_stats);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, const uint32_t *d_gfunc,
                                       uint32_t n_func, const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,

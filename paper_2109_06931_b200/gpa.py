@@ -95,6 +95,10 @@ def _load():
         "gpa_sparse_build": ([_vp, _vp, _u32, ctypes.c_int, ctypes.POINTER(_vp), _vp], S),
         "gpa_get_sparse_view": ([_vp, ctypes.POINTER(SparseView)], S),
         "gpa_free_sparse": ([_vp], None),
+        "gpa_attribute_profiles_inst": ([_vp, _vp, _u64, _u32, _vp, _vp, _vp], S),
+        "gpa_profile_stats_rows": ([_u64, _vp, _u32, _vp, ctypes.c_int, _vp], S),
+        "gpa_cct_profiles": ([_vp, _vp, _vp, _u32, _vp, _vp, _vp], S),
+        "gpa_profile_stats_f64": ([_u64, _vp, _u32, _vp, ctypes.c_int, _vp], S),
         "gpa_idleness_blame": ([ctypes.POINTER(TraceDesc), _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp], S),
     }
     for name, (args, res) in sig.items():
@@ -255,6 +259,45 @@ def profile_stats(s: Structure, prof_hist, n_profiles: int, stats, stream=None) 
     _check(_lib.gpa_profile_stats(s.handle, _ptr(prof_hist, "prof_hist"), int(n_profiles),
                                   _ptr(stats, "stats", 8 * 6 * 16 * s.info["n_func"]),
                                   _stream_ptr(stream, stats.device)), "gpa_profile_stats")
+
+
+def attribute_profiles_inst(s: Structure, samples, n_profiles: int, prof_hist, prof_unattr, n: int | None = None,
+                            stream=None) -> None:
+    """f1: per-profile instruction histograms ((n_profiles+1) x n_inst x 16, see gpa.h)."""
+    nb = samples.numel() * samples.element_size()
+    n = nb // 16 if n is None else int(n)
+    rows = int(n_profiles) + 1
+    _check(_lib.gpa_attribute_profiles_inst(
+        s.handle, _ptr(samples, "samples", 16 * n), n, int(n_profiles),
+        _ptr(prof_hist, "prof_hist", 128 * rows * s.info["n_inst"]), _ptr(prof_unattr, "prof_unattr", 128 * rows),
+        _stream_ptr(stream, samples.device)), "gpa_attribute_profiles_inst")
+
+
+def profile_stats_rows(prof_hist, n_profiles: int, stats, stream=None) -> None:
+    """f1: statistics of any u64 cube [(n_profiles+1), rows, 16] -> stats [rows, 6, 16]."""
+    rows = prof_hist.shape[1]
+    _check(_lib.gpa_profile_stats_rows(rows, _ptr(prof_hist, "prof_hist", 128 * rows * (int(n_profiles) + 1)),
+                                       int(n_profiles), _ptr(stats, "stats", 8 * 6 * 16 * rows),
+                                       stats.device.index or 0, _stream_ptr(stream, stats.device)),
+           "gpa_profile_stats_rows")
+
+
+def cct_profiles(s: Structure, cct: "Cct", prof_hist, n_profiles: int, prof_excl, prof_incl, stream=None) -> None:
+    """f1 at CCT level (R28): per-profile excl / incl [(n_profiles+1), n, 16] f64 on the tree."""
+    need = 128 * (int(n_profiles) + 1) * cct.n
+    _check(_lib.gpa_cct_profiles(s.handle, cct.handle,
+                                 _ptr(prof_hist, "prof_hist", 128 * (int(n_profiles) + 1) * s.info["n_func"]),
+                                 int(n_profiles), _ptr(prof_excl, "prof_excl", need), _ptr(prof_incl, "prof_incl", need),
+                                 _stream_ptr(stream, prof_hist.device)), "gpa_cct_profiles")
+
+
+def profile_stats_f64(prof_vals, n_profiles: int, stats, stream=None) -> None:
+    """f1: statistics of an f64 cube [(n_profiles+1), rows, 16] -> stats [rows, 6, 16]."""
+    rows = prof_vals.shape[1]
+    _check(_lib.gpa_profile_stats_f64(rows, _ptr(prof_vals, "prof_vals", 128 * rows * (int(n_profiles) + 1)),
+                                      int(n_profiles), _ptr(stats, "stats", 8 * 6 * 16 * rows),
+                                      stats.device.index or 0, _stream_ptr(stream, stats.device)),
+           "gpa_profile_stats_f64")
 
 
 def block_counts(s: Structure, block_start, counts, inst_hist, stream=None) -> None:

@@ -400,3 +400,53 @@ def test_attribution_shared_counter_overflow_patterns(gpa, attr_kernel, kernel):
     H, U, _ = _attribute(gpa, s, torch.from_numpy(rec.view(np.int64).reshape(-1, 2)).to(DEV), rec_inst=False)
     Ho, Uo, _ = oracle.attribute(w.structure, rec)
     assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
+
+
+# ---- f1 at instruction and CCT level ------------------------------------------------------------
+@pytest.mark.parametrize("name,records,n_prof", [("C2", 2_000_000, 5), ("C4", 1_000_003, 64), ("C1", 1000, 0)])
+def test_profiles_inst_parity(gpa, name, records, n_prof):
+    w = gen.workload(name, records=records)
+    s = gpa.load_structure(w.structure, 0)
+    rec = _device_records(w)
+    ni = s.info["n_inst"]
+    PH = torch.zeros((n_prof + 1, ni, 16), dtype=torch.int64, device=DEV)
+    PU = torch.zeros((n_prof + 1, 16), dtype=torch.int64, device=DEV)
+    gpa.attribute_profiles_inst(s, rec, n_prof, PH, PU)
+    stats = torch.empty((ni, 6, 16), dtype=torch.float64, device=DEV)
+    gpa.profile_stats_rows(PH, n_prof, stats)
+    torch.cuda.synchronize()
+    Hp, Up = oracle.attribute_profiles_inst(w.structure, w.records_host(), n_prof)
+    assert np.array_equal(u64(PH), Hp) and np.array_equal(u64(PU), Up)
+    So = oracle.profile_stats(Hp, n_prof)
+    assert np.array_equal(stats.cpu().numpy().view(np.uint64), So.view(np.uint64))
+
+
+@pytest.mark.parametrize("name,records,n_prof", [("C4", 2_000_000, 48), ("C3", 3_000_000, 3), ("C2", 500_000, 1)])
+def test_cct_profiles_parity(gpa, name, records, n_prof):
+    w = gen.workload(name, records=records)
+    s = gpa.load_structure(w.structure, 0)
+    rec = _device_records(w)
+    H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device=DEV)
+    U = torch.zeros(16, dtype=torch.int64, device=DEV)
+    gpa.attribute_samples(s, rec, H, U)
+    nf = s.info["n_func"]
+    PH = torch.zeros((n_prof + 1, nf, 16), dtype=torch.int64, device=DEV)
+    PU = torch.zeros((n_prof + 1, 16), dtype=torch.int64, device=DEV)
+    gpa.attribute_profiles(s, rec, n_prof, PH, PU)
+    c = gpa.reconstruct_cct(s, H)
+    n = c.n
+    E = torch.empty((n_prof + 1, n, 16), dtype=torch.float64, device=DEV)
+    I = torch.empty_like(E)
+    gpa.cct_profiles(s, c, PH, n_prof, E, I)
+    stats = torch.empty((n, 6, 16), dtype=torch.float64, device=DEV)
+    gpa.profile_stats_f64(I, n_prof, stats)
+    torch.cuda.synchronize()
+    R = oracle.cct(w.structure, u64(H))
+    Eo, Io = oracle.cct_profiles(R, u64(PH))
+    assert np.array_equal(E.cpu().numpy().view(np.uint64), Eo.view(np.uint64))
+    assert np.array_equal(I.cpu().numpy().view(np.uint64), Io.view(np.uint64))
+    So = oracle.profile_stats_f64(Io, n_prof)
+    got = stats.cpu().numpy()
+    np.testing.assert_allclose(got, So, rtol=1e-9, atol=0)
+    assert np.array_equal(got.view(np.uint64), So.view(np.uint64))
+    c.free()
