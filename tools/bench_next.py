@@ -58,6 +58,32 @@ def f1():
                       "attr_ms": ms_attr, "records_per_s": n / ms_attr * 1e3, "GBps": gbs, "frac": gbs / PEAK,
                       "stats_ms": ms_stats}), flush=True)
     f3(s, PH, P)
+    # instruction level: (P+1) x n_inst x 16 u64 cube (9.9 GB at C4), all-L2 reductions
+    PI = torch.zeros((P + 1, s.info["n_inst"], 16), dtype=torch.int64, device="cuda")
+
+    def run_inst():
+        PI.zero_()
+        PU.zero_()
+        gpa.attribute_profiles_inst(s, rec, P, PI, PU)
+
+    ms_inst = timed(run_inst)
+    st_inst = torch.empty((s.info["n_inst"], 6, 16), dtype=torch.float64, device="cuda")
+    ms_inst_stats = timed(lambda: gpa.profile_stats_rows(PI, P, st_inst))
+    del PI
+    # CCT level over the aggregate tree
+    H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device="cuda")
+    U = torch.zeros(16, dtype=torch.int64, device="cuda")
+    gpa.attribute_samples(s, rec, H, U)
+    c = gpa.reconstruct_cct(s, H)
+    E = torch.empty((P + 1, c.n, 16), dtype=torch.float64, device="cuda")
+    I = torch.empty_like(E)
+    ms_cct = timed(lambda: gpa.cct_profiles(s, c, PH, P, E, I))
+    st_cct = torch.empty((c.n, 6, 16), dtype=torch.float64, device="cuda")
+    ms_cct_stats = timed(lambda: gpa.profile_stats_f64(I, P, st_cct))
+    print(json.dumps({"row": "f1-inst+cct", "workload": "C4", "profiles": P, "inst_attr_ms": ms_inst,
+                      "inst_records_per_s": n / ms_inst * 1e3, "inst_GBps": 16 * n / ms_inst / 1e6,
+                      "inst_stats_ms": ms_inst_stats, "contexts": c.n, "cct_profiles_ms": ms_cct,
+                      "cct_stats_ms": ms_cct_stats}), flush=True)
 
 
 def f3(s, PH, P):
