@@ -102,6 +102,10 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_prof_tma(AttrTables T, const uint32_t *__restrict__ gfunc, uint32_t n_func, const uint4 *__restrict__ rec,
                     uint64_t n, uint32_t n_prof, uint32_t K, unsigned long long *__restrict__ PH,
                     unsigned long long *__restrict__ PU) {
+  // K > 0: each CTA takes a contiguous range of tiles (it meets few profiles: the shared table
+  // pays).  K == 0 (instruction rows, everything to L2): tiles are dealt round-robin so all CTAs
+  // stay inside the same stretch of the stream (a profile or two) and the reduction targets stay
+  // L2-resident instead of spreading over 148 profiles' rows.
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = kProfLook + 1;
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
@@ -111,7 +115,10 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   const uint32_t tab_s = smem_u32(tab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t ntiles = (n + S - 1) / S;
-  const uint64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const bool rr = K == 0;
+  const uint64_t t0 = rr ? blockIdx.x : ntiles * blockIdx.x / gridDim.x;
+  const uint64_t t1 = rr ? ntiles : ntiles * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t step = rr ? gridDim.x : 1;
   const uint32_t nt = K * n_func * GPA_VALID_SLOTS;
   for (uint32_t x = threadIdx.x; x < nt; x += blockDim.x) tab[x] = 0;
   uint32_t pf = 0;
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, t0, 1, t1);
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, t0, step, t1);
     return;
   }
   uint4 v[D][R];
@@ -143,14 +150,14 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   };
 #pragma unroll
   for (int q = 0; q < kProfLook; q++)
-    if (t0 + q < t1) fetch(q, v[q], c[q]);
+    if (t0 + q * step < t1) fetch(q, v[q], c[q]);
   for (uint32_t it0 = 0;; it0 += D) {
 #pragma unroll
     for (int q = 0; q < D; q++) {
       const uint32_t it = it0 + q;
-      const uint64_t tile = t0 + it;
+      const uint64_t tile = t0 + it * step;
       if (tile >= t1) goto done;
-      if (tile + kProfLook < t1) fetch(it + kProfLook, v[(q + kProfLook) % D], c[(q + kProfLook) % D]);
+      if (tile + kProfLook * step < t1) fetch(it + kProfLook, v[(q + kProfLook) % D], c[(q + kProfLook) % D]);
       const uint64_t left = n - tile * S;
       const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
       uint32_t old[R], idx[R];
@@ -271,11 +278,22 @@ cudaError_t launch_attribute_profiles_inst(const AttrTables &T, uint32_t n_inst,
                                            uint64_t n, uint32_t n_prof, unsigned long long *d_ph,
                                            unsigned long long *d_pu, int sm_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
+  if (T.mode == 0 && n >= 4096) {  // TMA ring, granule -> instruction, one u64 L2 reduction per record
+    using RG = RingProf;
+    const size_t smem = RG::kBytes + 2 * RG::kStages * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_attr_prof_tma<RG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    uint64_t ntiles = (n + RG::kTile - 1) / RG::kTile;
+    unsigned blocks = (unsigned)(ntiles < (uint64_t)sm_count ? ntiles : (uint64_t)sm_count);
+    k_attr_prof_tma<RG><<<blocks, RG::kThreads, smem, st>>>(T, T.gmap, n_inst, rec, n, n_prof, 0, d_ph, d_pu);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   uint64_t per_block = (uint64_t)kThreads * kUnroll;
   uint64_t want = (n + per_block - 1) / per_block;
   uint64_t cap = (uint64_t)sm_count * (2048 / kThreads);
   unsigned blocks = (unsigned)(want < cap ? want : cap);
-  const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
   if (T.mode == 0) k_attr_prof<0><<<blocks, kThreads, 0, st>>>(T, nullptr, n_inst, rec, n, n_prof, d_ph, d_pu);
   else k_attr_prof<1><<<blocks, kThreads, 0, st>>>(T, nullptr, n_inst, rec, n, n_prof, d_ph, d_pu);
   count_launches(1);
