@@ -38,7 +38,7 @@ __global__ void k_weights(const uint32_t *__restrict__ call_inst, uint32_t n_cal
 }
 
 struct PropArgs {
-  uint32_t n_func, n_dag, n_lev, exact, do_count;
+  uint32_t n_func, n_dag, n_lev, exact, do_count, n_call;
   const uint64_t *S_f;
   const uint32_t *fin_ptr, *fin_e, *caller, *scc_of, *din_ptr, *din_e, *dmem_ptr, *dmem, *dlev_ptr, *dlev_node;
   const uint8_t *nontriv;
@@ -48,14 +48,30 @@ struct PropArgs {
 };
 
 // Single CTA: the call graph is small (<= a few thousand functions); rounds are separated
-// by __syncthreads, which also orders the global-memory updates inside the CTA.
+// by __syncthreads, which also orders the memory updates inside the CTA.  SM = true: the
+// mutable state (w, function / DAG activity, path counts) lives in shared memory for the
+// whole kernel (every fixpoint round then costs shared-memory, not L2, latency) and is
+// written back at the end; the read-only graph tables stay in global memory (L1-cached).
+template <bool SM>
 __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
   __shared__ int changed;
   __shared__ unsigned long long red[32];
+  extern __shared__ __align__(16) uint8_t psm[];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   volatile uint8_t *fact = A.fact;
   volatile uint8_t *dact = A.dact;
   volatile uint64_t *w = A.w;
+  volatile uint64_t *paths = A.paths;
+  if (SM) {
+    uint64_t *ws = reinterpret_cast<uint64_t *>(psm);
+    uint64_t *ps = ws + A.n_call;
+    uint8_t *fs = reinterpret_cast<uint8_t *>(ps + A.n_dag);
+    for (uint32_t e = t; e < A.n_call; e += nt) ws[e] = A.w[e];
+    w = ws;
+    paths = ps;
+    fact = fs;
+    dact = fs + A.n_func;
+  }
   for (uint32_t f = t; f < A.n_func; f += nt) {
     uint64_t s = 0;
     for (int r = 0; r < GPA_VALID_SLOTS; r++) s += A.S_f[(uint64_t)f * GPA_SLOTS + r];
@@ -115,16 +131,21 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
     if (!changed) break;
   }
   // W_X = total weight of the external calls into X
+  __syncthreads();
   for (uint32_t X = t; X < A.n_dag; X += nt) {
     uint64_t s = 0;
     for (uint32_t k = A.din_ptr[X]; k < A.din_ptr[X + 1]; k++) s += w[A.din_e[k]];
     A.W[X] = s;
   }
+  if (SM) {  // write the shared state back for the tree builders
+    for (uint32_t e = t; e < A.n_call; e += nt) A.w[e] = w[e];
+    for (uint32_t f = t; f < A.n_func; f += nt) A.fact[f] = fact[f];
+    for (uint32_t X = t; X < A.n_dag; X += nt) A.dact[X] = dact[X];
+  }
   // exact context count: paths from active roots through edges with w > 0, level by level
   // (skipped when the caller builds the tree into a static-bound allocation and reads the
   // size back afterwards)
   if (!A.do_count) return;
-  volatile uint64_t *paths = A.paths;
   for (uint32_t L = 0; L < A.n_lev; L++) {
     __syncthreads();
     for (uint32_t q = A.dlev_ptr[L] + t; q < A.dlev_ptr[L + 1]; q += nt) {
@@ -539,6 +560,41 @@ __global__ void __launch_bounds__(512) k_cct_fold(LevelArgs A, const uint32_t *_
   }
 }
 
+// The same excl + level-by-level incl fold on ONE thread-block cluster (8-16 SMs) with hardware
+// cluster barriers between levels instead of grid-wide barriers: small trees have tens of
+// levels with little work each, so the barrier latency dominates.  Values written by other
+// CTAs of the cluster are read through L2 (ld.cg) after the barrier's release/acquire.
+__global__ void __launch_bounds__(1024) k_cct_fold_cl(LevelArgs A, const uint32_t *__restrict__ lev,
+                                                    const uint64_t *__restrict__ S_f, double *excl, double *incl) {
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t L = lev[0];
+  const uint64_t n = lev[1 + L];
+  const uint64_t gt = (uint64_t)cl.block_rank() * blockDim.x + threadIdx.x, gs = (uint64_t)cl.num_blocks() * blockDim.x;
+  for (uint64_t x = gt; x < n * GPA_SLOTS; x += gs) {  // excl (R14)
+    uint64_t c = x >> 4;
+    int r = (int)(x & 15);
+    uint8_t k = A.kind[c];
+    double v = 0.0;
+    if (k != GPA_CTX_SCC) {
+      uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
+      v = __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
+    }
+    excl[x] = v;
+  }
+  cl.sync();
+  for (int l = (int)L - 1; l >= 0; l--) {  // incl: children in index order
+    for (uint64_t x = (uint64_t)lev[1 + l] * GPA_SLOTS + gt; x < (uint64_t)lev[2 + l] * GPA_SLOTS; x += gs) {
+      uint64_t c = x >> 4;
+      int r = (int)(x & 15);
+      double v = __ldcg(excl + x);
+      uint32_t d0 = A.first_child[c], nc = A.n_children[c];
+      for (uint32_t d = d0; d < d0 + nc; d++) v = __dadd_rn(v, __ldcg(incl + (uint64_t)d * GPA_SLOTS + r));
+      incl[x] = v;
+    }
+    cl.sync();
+  }
+}
+
 unsigned grid_for(uint64_t work, unsigned threads) {
   uint64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -582,6 +638,8 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
   return cudaGetLastError();
 }
 
+constexpr size_t kPropSmem = 200 * 1024;
+
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
                                  unsigned long long *d_count, bool exact, bool count, cudaStream_t st) {
@@ -596,7 +654,17 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
   A.scc_of = s->d_scc_of; A.din_ptr = s->d_din_ptr; A.din_e = s->d_din_e; A.dmem_ptr = s->d_dmem_ptr;
   A.dmem = s->d_dmem; A.dlev_ptr = s->d_dlev_ptr; A.dlev_node = s->d_dlev_node; A.nontriv = s->d_dag_nontrivial;
   A.w = d_w; A.W = d_W; A.paths = paths; A.fact = d_func_active; A.dact = d_dag_active; A.count = d_count;
-  k_propagate<<<1, 1024, 0, st>>>(A);
+  A.n_call = s->info.n_call;
+  const size_t sm = 8ull * (A.n_call + A.n_dag) + A.n_func + A.n_dag;
+  if (sm <= kPropSmem) {
+    if (sm > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(k_propagate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPropSmem)) !=
+            cudaSuccess)
+      return e;
+    k_propagate<true><<<1, 1024, sm, st>>>(A);
+  } else {
+    k_propagate<false><<<1, 1024, 0, st>>>(A);
+  }
   count_launches(1);
   e = cudaGetLastError();
   cudaError_t e2 = cudaFreeAsync(paths, st);
@@ -662,13 +730,43 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  const uint32_t *lev = d_lev;
+  const uint64_t *S_f = c->S_f;
+  double *excl = c->excl, *incl = c->incl;
+  static int cluster = -1;  // largest cluster the device accepts for k_cct_fold_cl (16, else 8), 0 = none
+  if (cluster < 0) {
+    cluster = 0;
+    if (cudaFuncSetAttribute(k_cct_fold_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+      cluster = 16;
+    else
+      cluster = 8;
+    cudaGetLastError();
+  }
+  for (int cs = cluster; cs >= 8; cs /= 2) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_cct_fold_cl, A, lev, S_f, excl, incl);
+    if (e == cudaSuccess) {
+      count_launches(1);
+      cluster = cs;
+      return cudaSuccess;
+    }
+    cudaGetLastError();
+  }
+  cluster = 0;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cct_fold, 512, 0);
   if (e != cudaSuccess) return e;
   unsigned blocks = (unsigned)(sm_count * (per_sm < 2 ? (per_sm < 1 ? 1 : per_sm) : 2));
-  const uint32_t *lev = d_lev;
-  const uint64_t *S_f = c->S_f;
-  double *excl = c->excl, *incl = c->incl;
   void *args[] = {&A, &lev, &S_f, &excl, &incl};
   e = cudaLaunchCooperativeKernel((void *)k_cct_fold, dim3(blocks), dim3(512), args, 0, st);
   count_launches(1);

@@ -10,7 +10,8 @@ import torch
 import gen
 from paper_2109_06931_b200 import gpa
 
-for kernel in (0, 1, 2, 3, 4):
+KERNELS = [int(k) for k in os.environ.get("SAN_KERNELS", "0,1,2,3,4").split(",")]
+for kernel in KERNELS:
     gpa.set_attr_kernel(kernel)
     for name, records in (("C1", 10_000), ("C2", 2_200_000)):
         w = gen.workload(name, records=records)
@@ -37,6 +38,29 @@ for kernel in (0, 1, 2, 3, 4):
         PU = torch.zeros((P + 1, 16), dtype=torch.int64, device="cuda")
         gpa.attribute_profiles(s, rec, P, PH, PU)
         gpa.profile_stats(s, PH, P, torch.empty((s.info["n_func"], 6, 16), dtype=torch.float64, device="cuda"))
+        for cms in (False, True):
+            gpa.sparse_build(s, PH, P, cms).free()
+        PI = torch.zeros((P + 1, s.info["n_inst"], 16), dtype=torch.int64, device="cuda")
+        gpa.attribute_profiles_inst(s, rec, P, PI, PU)
+        gpa.profile_stats_rows(PI, P, torch.empty((s.info["n_inst"], 6, 16), dtype=torch.float64, device="cuda"))
+        c = gpa.reconstruct_cct(s, H)
+        E = torch.empty((P + 1, max(1, c.n), 16), dtype=torch.float64, device="cuda")
+        I = torch.empty_like(E)
+        gpa.cct_profiles(s, c, PH, P, E, I)
+        gpa.profile_stats_f64(I, P, torch.empty((max(1, c.n), 6, 16), dtype=torch.float64, device="cuda"))
+        c.free()
         torch.cuda.synchronize()
         s.free()
+    if kernel != KERNELS[0]:
+        continue
+    from gen.trace import trace_set
+    for tname in ("B1", "B2"):
+        tr = trace_set(tname)
+        t = torch.from_numpy(tr["time"].view(np.int64)).cuda()
+        cx = torch.from_numpy(tr["ctx"].view(np.int32)).cuda()
+        S, R = tr["n_scopes"], tr["n_routines"]
+        gpa.idleness_blame(tr, t, cx, torch.empty((S, R), dtype=torch.float64, device="cuda"),
+                           torch.empty((S, R), dtype=torch.float64, device="cuda"),
+                           torch.empty(S, dtype=torch.int64, device="cuda"), torch.empty(S, dtype=torch.int64, device="cuda"))
+        torch.cuda.synchronize()
 print("sanitize run OK")
