@@ -215,23 +215,35 @@ def run_gpa(args):
             ev_a1.append(e1)
         reduce_histogram(HU, dst=0)
         if rank == 0:
-            return analyse()
+            return analyse(timed)
         return 0
 
     side = torch.cuda.Stream(dev)
 
-    def analyse():
+    ev_b0, ev_b1, ev_c1 = [], [], []
+
+    def analyse(timed: bool = False):
         """Roll-up + metrics of the five scopes on a side stream, concurrently with the CCT
         (both only read H)."""
-        ready = torch.cuda.Event()
+        ready = torch.cuda.Event(enable_timing=timed)
         ready.record(stream)
+        if timed:
+            ev_b0.append(ready)
         side.wait_event(ready)
         for sc in SCOPES:
             gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=side)
+        if timed:
+            sd = torch.cuda.Event(enable_timing=True)
+            sd.record(side)
+            ev_b1.append(sd)
         cct = gpa.reconstruct_cct(s, H, stream=stream)
         cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
         gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
         gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+        if timed:
+            ce = torch.cuda.Event(enable_timing=True)
+            ce.record(stream)
+            ev_c1.append(ce)
         stream.wait_stream(side)
         stream.synchronize()
         nctx = cct.n
@@ -326,6 +338,11 @@ def run_gpa(args):
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # phase times on rank 0 and the secondary sum-of-counts rate
+    phases = {"attr_ms": attr_ms,
+              "scopes_ms_side_stream": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_b1)) / max(1, len(ev_b1)),
+              "cct_and_cct_metrics_ms": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_c1)) / max(1, len(ev_c1))}
+    observations = int(HU.sum().item())  # sum of counts of the last step (two's complement = u64 here)
     line = {"metric": METRIC, "value": n_all / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
@@ -336,7 +353,8 @@ def run_gpa(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_attr_bins",
                          "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
-            "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
+            "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e, "phases_ms": phases,
+            "observations_per_s": observations / (ms / 1e3)}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
     print(json.dumps(line), flush=True)
