@@ -477,6 +477,7 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
   UP(s->d_scc_of, s->h_scc_of);
   UP(s->d_fout_ptr, fout_ptr);
   UP(s->d_fout_e, fout_e);
+  s->n_ext_calls = (uint32_t)fout_e.size();
   UP(s->d_din_ptr, din_ptr);
   UP(s->d_din_e, din_e);
   UP(s->d_dmem_ptr, dmem_ptr);

@@ -62,6 +62,7 @@ struct gpa_structure_s {
   // call graph (function level)
   uint32_t *d_call_inst = nullptr, *d_call_callee = nullptr, *d_call_caller = nullptr;
   uint32_t *d_fin_ptr = nullptr, *d_fin_e = nullptr;    // in-edges per function
+  uint32_t n_ext_calls = 0;                             // external (cross-DAG-node) call sites
   uint32_t *d_fout_ptr = nullptr, *d_fout_e = nullptr;  // external out-edges per function,
                                                         // ascending call instruction
   // condensed DAG

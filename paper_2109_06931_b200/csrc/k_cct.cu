@@ -414,6 +414,156 @@ __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag,
   if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
 }
 
+// k_cct_small with its working set in shared memory (used when it fits): per external call
+// site (in each caller's ascending call-instruction order) the child it creates — node, kind,
+// site and the ratio w_e / W_Y (R13; frac = parent's frac * ratio, the same two roundings as
+// write_children) — the number of weighted external calls of every function, and the kind /
+// node / frac of the current and next BFS level (up to kSmallCap contexts each; contexts
+// beyond that are read back from global memory).  Same numbering and results as k_cct_small.
+constexpr uint32_t kSmallCap = 3072;
+constexpr uint8_t kSkip = 0xFF;
+
+__host__ __device__ inline size_t small2_smem(uint32_t n_func, uint32_t m) {
+  return (size_t)m * 8 + (size_t)m * 4 * 2 + 2ull * kSmallCap * 8 + 2ull * kSmallCap * 4 + (size_t)n_func * 2 +
+         (size_t)m + 2ull * kSmallCap + 64;
+}
+
+__global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_func, uint32_t m, uint32_t n_dag,
+                                                     const uint32_t *din_ptr, const uint8_t *dact, uint32_t *lev_out,
+                                                     unsigned long long *built) {
+  extern __shared__ __align__(16) uint8_t sm2[];
+  __shared__ uint32_t lev[kSmallLevels + 1];
+  double *eratio = reinterpret_cast<double *>(sm2);
+  double *cfrac = eratio + m, *nfrac = cfrac + kSmallCap;
+  uint32_t *enode = reinterpret_cast<uint32_t *>(nfrac + kSmallCap);
+  uint32_t *esite = enode + m;
+  uint32_t *cnode = esite + m, *nnode = cnode + kSmallCap;
+  uint16_t *nzc = reinterpret_cast<uint16_t *>(nnode + kSmallCap);
+  uint8_t *ekind = reinterpret_cast<uint8_t *>(nzc + n_func);
+  uint8_t *ckind = ekind + m, *nkind = ckind + kSmallCap;
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  for (uint32_t q = t; q < m; q += nt) {  // the child each weighted external call creates
+    const uint32_t e = A.fout_e[q];
+    const uint64_t we = A.w[e];
+    const uint32_t Y = A.scc_of[A.callee[e]];
+    esite[q] = e;
+    enode[q] = Y;
+    ekind[q] = we ? (A.nontriv[Y] ? GPA_CTX_SCC : GPA_CTX_FUNC) : kSkip;
+    eratio[q] = we ? __ddiv_rn(__ull2double_rn(we), __ull2double_rn(A.W[Y])) : 0.0;  // R13
+  }
+  __syncthreads();
+  for (uint32_t g = t; g < n_func; g += nt) {
+    uint32_t c = 0;
+    for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) c += ekind[q] != kSkip;
+    nzc[g] = (uint16_t)c;
+  }
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < n_dag; base += nt) {  // roots in DAG order (R15)
+    uint32_t X = base + t;
+    uint32_t flag = X < n_dag && din_ptr[X] == din_ptr[X + 1] && dact[X];
+    uint32_t tot;
+    uint32_t pos = running + block_exscan(flag, &tot);
+    if (flag) {
+      const uint8_t k = A.nontriv[X] ? GPA_CTX_SCC : GPA_CTX_FUNC;
+      A.parent[pos] = NONE;
+      A.site[pos] = NONE;
+      A.node[pos] = X;
+      A.kind[pos] = k;
+      A.frac[pos] = 1.0;
+      if (pos < kSmallCap) {
+        ckind[pos] = k;
+        cnode[pos] = X;
+        cfrac[pos] = 1.0;
+      }
+    }
+    running += tot;
+  }
+  __syncthreads();
+  uint32_t a = 0, b = running, L = 0;
+  if (t == 0) lev[0] = 0;
+  while (b > a && L < kSmallLevels) {
+    if (t == 0) lev[L + 1] = b;
+    L++;
+    uint32_t next = b;
+    for (uint32_t base = a; base < b; base += nt) {
+      const uint32_t c = base + t;
+      uint8_t k = 0;
+      uint32_t nd = 0, cnt = 0, g = 0;
+      double f = 0.0;
+      if (c < b) {
+        if (c - a < kSmallCap) {
+          k = ckind[c - a];
+          nd = cnode[c - a];
+          f = cfrac[c - a];
+        } else {
+          k = A.kind[c];
+          nd = A.node[c];
+          f = A.frac[c];
+        }
+        if (k == GPA_CTX_SCC) {
+          cnt = A.dmem_ptr[nd + 1] - A.dmem_ptr[nd];
+        } else {
+          g = k == GPA_CTX_SCC_MEMBER ? nd : A.dmem[A.dmem_ptr[nd]];
+          cnt = nzc[g];
+        }
+      }
+      uint32_t tot;
+      const uint32_t o = next + block_exscan(cnt, &tot);
+      if (c < b) {
+        if (k == GPA_CTX_SCC) {  // members in ascending function id (R14)
+          uint32_t d = o;
+          for (uint32_t q = A.dmem_ptr[nd]; q < A.dmem_ptr[nd + 1]; q++, d++) {
+            const uint32_t mf = A.dmem[q];
+            A.parent[d] = c;
+            A.site[d] = NONE;
+            A.node[d] = mf;
+            A.kind[d] = GPA_CTX_SCC_MEMBER;
+            A.frac[d] = f;
+            if (d - b < kSmallCap) {
+              nkind[d - b] = GPA_CTX_SCC_MEMBER;
+              nnode[d - b] = mf;
+              nfrac[d - b] = f;
+            }
+          }
+        } else {  // weighted external calls, ascending call instruction (R15, R17)
+          uint32_t d = o;
+          for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) {
+            const uint8_t ek = ekind[q];
+            if (ek == kSkip) continue;
+            const double fr = __dmul_rn(f, eratio[q]);
+            A.parent[d] = c;
+            A.site[d] = esite[q];
+            A.node[d] = enode[q];
+            A.kind[d] = ek;
+            A.frac[d] = fr;
+            if (d - b < kSmallCap) {
+              nkind[d - b] = ek;
+              nnode[d - b] = enode[q];
+              nfrac[d - b] = fr;
+            }
+            d++;
+          }
+        }
+        A.first_child[c] = o;
+        A.n_children[c] = cnt;
+      }
+      next += tot;
+    }
+    __syncthreads();
+    {  // the next level becomes the current one
+      uint8_t *tk = ckind; ckind = nkind; nkind = tk;
+      uint32_t *tn = cnode; cnode = nnode; nnode = tn;
+      double *tf = cfrac; cfrac = nfrac; nfrac = tf;
+    }
+    a = b;
+    b = next;
+  }
+  __syncthreads();
+  for (uint32_t l = t; l <= L; l += nt) lev_out[l + 1] = lev[l];  // lev_out[0] = number of levels
+  if (t == 0) lev_out[0] = L;
+  if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
+}
+
 // Exact counts from instrumentation: block b's execution count goes to slot 0 of
 // every instruction of the block.  One thread per block; blocks are short and disjoint.
 __global__ void k_block_counts(uint32_t n_blocks, const uint32_t *__restrict__ start, const uint64_t *__restrict__ cnt,
@@ -726,9 +876,19 @@ cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_
 cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_lev, unsigned long long *d_built,
                              int sm_count, cudaStream_t st) {
   LevelArgs A = level_args(s, c);
-  k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built);
+  const uint32_t m_ext = s->n_ext_calls;
+  const size_t sm2 = small2_smem(s->info.n_func, m_ext);
+  cudaError_t e = cudaSuccess;
+  if (sm2 <= 200 * 1024 && s->info.n_func < 65536) {
+    e = cudaFuncSetAttribute(k_cct_small2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    if (e != cudaSuccess) return e;
+    k_cct_small2<<<1, 1024, sm2, st>>>(A, s->info.n_func, m_ext, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev,
+                                       d_built);
+  } else {
+    k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built);
+  }
   count_launches(1);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const uint32_t *lev = d_lev;
   const uint64_t *S_f = c->S_f;
