@@ -450,3 +450,29 @@ def test_cct_profiles_parity(gpa, name, records, n_prof):
     np.testing.assert_allclose(got, So, rtol=1e-9, atol=0)
     assert np.array_equal(got.view(np.uint64), So.view(np.uint64))
     c.free()
+
+
+def test_f1_invalid_args(gpa):
+    w = gen.workload("C2", records=1000)
+    s = gpa.load_structure(w.structure, 0)
+    rec = _device_records(w)
+    ni, nf = s.info["n_inst"], s.info["n_func"]
+    with pytest.raises(gpa.GpaError):                  # instruction cube too small
+        gpa.attribute_profiles_inst(s, rec, 4, torch.zeros((2, ni, 16), dtype=torch.int64, device=DEV),
+                                    torch.zeros((5, 16), dtype=torch.int64, device=DEV))
+    with pytest.raises(gpa.GpaError):                  # unaligned records
+        gpa.attribute_profiles_inst(s, rec.view(-1)[1:-1].view(torch.uint8)[4:-4].view(torch.int64), 1,
+                                    torch.zeros((2, ni, 16), dtype=torch.int64, device=DEV),
+                                    torch.zeros((2, 16), dtype=torch.int64, device=DEV), n=10)
+    H = torch.zeros((ni, 16), dtype=torch.int64, device=DEV)
+    U = torch.zeros(16, dtype=torch.int64, device=DEV)
+    gpa.attribute_samples(s, rec, H, U)
+    c = gpa.reconstruct_cct(s, H)
+    PH = torch.zeros((3, nf, 16), dtype=torch.int64, device=DEV)
+    with pytest.raises(gpa.GpaError):                  # outputs too small for the tree
+        gpa.cct_profiles(s, c, PH, 2, torch.empty((1, 1, 16), dtype=torch.float64, device=DEV),
+                         torch.empty((1, 1, 16), dtype=torch.float64, device=DEV))
+    c.free()
+    with pytest.raises(gpa.GpaError):
+        gpa.profile_stats_f64(torch.zeros((2, 4, 16), dtype=torch.float64, device=DEV), 3,
+                              torch.empty((4, 6, 16), dtype=torch.float64, device=DEV))

@@ -82,3 +82,16 @@ def test_sparse_single_function_row(gpa):
     Hp[4, 0, 0] = 2 ** 64 - 1
     for cms in (False, True):
         _check(gpa, s, Hp, cms)
+
+
+def test_sparse_invalid_args(gpa):
+    w = gen.workload("C1", records=1)
+    s = gpa.load_structure(w.structure, 0)
+    PH = torch.zeros((3, s.info["n_func"], 16), dtype=torch.int64, device=DEV)
+    with pytest.raises(gpa.GpaError):                  # buffer too small for 5 profiles
+        gpa.sparse_build(s, PH, 5, True)
+    import ctypes
+    from paper_2109_06931_b200.gpa import _lib
+    h = ctypes.c_void_p()
+    assert _lib.gpa_sparse_build(s.handle, PH.data_ptr(), 2, 7, ctypes.byref(h), None) != 0   # bad major
+    assert _lib.gpa_sparse_build(None, PH.data_ptr(), 2, 0, ctypes.byref(h), None) != 0       # NULL structure
