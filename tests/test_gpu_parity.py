@@ -461,7 +461,7 @@ def test_f1_invalid_args(gpa):
         gpa.attribute_profiles_inst(s, rec, 4, torch.zeros((2, ni, 16), dtype=torch.int64, device=DEV),
                                     torch.zeros((5, 16), dtype=torch.int64, device=DEV))
     with pytest.raises(gpa.GpaError):                  # unaligned records
-        gpa.attribute_profiles_inst(s, rec.view(-1)[1:-1].view(torch.uint8)[4:-4].view(torch.int64), 1,
+        gpa.attribute_profiles_inst(s, rec.view(-1)[1:-1], 1,
                                     torch.zeros((2, ni, 16), dtype=torch.int64, device=DEV),
                                     torch.zeros((2, 16), dtype=torch.int64, device=DEV), n=10)
     H = torch.zeros((ni, 16), dtype=torch.int64, device=DEV)
