@@ -1046,7 +1046,7 @@ gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, c
   CU(mem.get(&a.ovf, n * kmax / 256 + 1));
   CU(mem.get(&a.seg, n));
   CU(mem.get(&a.seg_n, n / 8192 + 1));
-  CU(mem.get(&a.bs, 65536)); CU(mem.get(&a.err, 4)); CU(mem.get(&a.tots, 4));
+  CU(mem.get(&a.bs, kScanScratchWords)); CU(mem.get(&a.err, 4)); CU(mem.get(&a.tots, 4));
   CU(mem.get(&a.acc, 2ull * S)); CU(mem.get(&a.num, nsr));
   uint64_t max_tiles = 0, *d_split = nullptr;
   for (size_t r = 0, cofs = 0; r < round_np.size(); cofs += round_np[r] + 1, r++)
@@ -1139,7 +1139,7 @@ gpa_status gpa_sparse_build(gpa_structure s, const uint64_t *d_prof_hist, uint32
   unsigned long long *tot = nullptr;
   SC(alloc((void **)&ov, cells * 4));
   SC(alloc((void **)&oi, cells * 4));
-  SC(alloc((void **)&bs, 65536 * 4));
+  SC(alloc((void **)&bs, kScanScratchWords * 4));
   SC(alloc((void **)&tot, 16));
   SC(alloc((void **)&sp->plane_off, (sp->n_planes + 1) * 8));
   SC(alloc((void **)&sp->index_off, (sp->n_planes + 1) * 8));

@@ -114,6 +114,9 @@ void set_attr_kernel(int which);
 // threshold = unlimited, so memory freed at one call is reused by the next without going
 // back to the driver; the process's default pool is left untouched).
 cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
+// scratch words a scan_u32 call (kern_common.cuh) needs: look-back state for up to 2^27
+// elements + the tile ticket
+constexpr size_t kScanScratchWords = 2 * 32768 + 4;
 }
 
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------

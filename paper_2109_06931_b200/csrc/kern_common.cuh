@@ -176,20 +176,98 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t *v, uint64_
   }
 }
 
+// single-pass exclusive scan of u32 values in place (decoupled look-back): each CTA takes the
+// next tile by ticket, publishes its aggregate, then warp 0 walks back over the predecessors'
+// published (aggregate | inclusive) words 32 at a time until it meets an inclusive prefix, and
+// publishes its own inclusive prefix.  One read and one write per element.
+constexpr int kLbThreads = 512, kLbItems = 8, kLbTile = kLbThreads * kLbItems;
+
+__global__ void __launch_bounds__(kLbThreads) k_scan_lb(uint32_t *__restrict__ v, uint64_t m,
+                                                       unsigned long long *state, uint32_t *ctr,
+                                                       unsigned long long *total) {
+  const unsigned long long kLbAgg = 1ull << 32, kLbInc = 2ull << 32;  // published: aggregate / inclusive
+  __shared__ uint32_t s_tile, s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t i0 = (uint64_t)tile * kLbTile + (uint64_t)threadIdx.x * kLbItems;
+  uint32_t x[kLbItems], sum = 0;
+  if (i0 + kLbItems <= m) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(v + i0), b = *reinterpret_cast<const uint4 *>(v + i0 + 4);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kLbItems; q++) x[q] = i0 + q < m ? v[i0 + q] : 0;
+  }
+#pragma unroll
+  for (int q = 0; q < kLbItems; q++) sum += x[q];
+  uint32_t agg;
+  uint32_t ex = block_exscan(sum, &agg);
+  volatile unsigned long long *vs = state;
+  if (threadIdx.x == 0) vs[tile] = (tile == 0 ? kLbInc : kLbAgg) | agg;
+  if (tile > 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t excl = 0;
+    int64_t p = (int64_t)tile - 1;
+    for (;;) {
+      const int64_t q = p - lane;
+      const unsigned long long w = q >= 0 ? vs[q] : kLbInc;  // before the first tile: prefix 0
+      const uint32_t flag = (uint32_t)(w >> 32);
+      if (__any_sync(kFull, flag == 0)) continue;           // a predecessor has not published yet
+      const unsigned inc = __ballot_sync(kFull, flag == 2);
+      const int stop = inc ? __ffs(inc) - 1 : 31;
+      uint32_t val = lane <= stop ? (uint32_t)w : 0u;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
+      excl += val;
+      if (inc) break;
+      p -= 32;
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      vs[tile] = kLbInc | (uint32_t)(excl + agg);
+    }
+  }
+  __syncthreads();
+  uint32_t run = (tile ? s_excl : 0u) + ex;
+  if (i0 + kLbItems <= m) {
+    uint32_t y[kLbItems];
+#pragma unroll
+    for (int q = 0; q < kLbItems; q++) {
+      y[q] = run;
+      run += x[q];
+    }
+    *reinterpret_cast<uint4 *>(v + i0) = make_uint4(y[0], y[1], y[2], y[3]);
+    *reinterpret_cast<uint4 *>(v + i0 + 4) = make_uint4(y[4], y[5], y[6], y[7]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kLbItems; q++)
+      if (i0 + q < m) {
+        v[i0 + q] = run;
+        run += x[q];
+      }
+  }
+  const uint64_t n_tiles = (m + kLbTile - 1) / kLbTile;
+  if (threadIdx.x == 0 && tile == (n_tiles ? n_tiles - 1 : 0)) total[0] = (uint32_t)((tile ? s_excl : 0u) + agg);
+}
+
 }  // namespace
 
 void count_launches(uint64_t k);
 
 namespace {
-// host side: exclusive scan of m u32 values in place on `st`; the total lands in *total (device)
-inline cudaError_t scan_u32(uint32_t *v, uint64_t m, uint32_t *bs, unsigned long long *total, cudaStream_t st) {
-  uint64_t nb = (m + kScanTile - 1) / kScanTile;
-  if (nb > 65536) return cudaErrorInvalidValue;
-  if (nb == 0) nb = 1;
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(v, m, bs);
-  k_scan_top<<<1, kScanThreads, 0, st>>>(bs, (uint32_t)nb, total);
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(v, m, bs);
-  count_launches(3);
+// host side: exclusive scan of m u32 values (m <= 2^27; v 16-B aligned) in place on `st`; the
+// total lands in *total (device); scratch = kScanScratchWords u32
+inline cudaError_t scan_u32(uint32_t *v, uint64_t m, uint32_t *scratch, unsigned long long *total, cudaStream_t st) {
+  uint64_t nt = (m + kLbTile - 1) / kLbTile;
+  if (nt > 32768) return cudaErrorInvalidValue;
+  if (nt == 0) nt = 1;
+  unsigned long long *state = reinterpret_cast<unsigned long long *>(scratch);
+  uint32_t *ctr = scratch + 2 * nt;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, (2 * nt + 1) * 4, st);
+  if (e != cudaSuccess) return e;
+  k_scan_lb<<<(unsigned)nt, kLbThreads, 0, st>>>(v, m, state, ctr, total);
+  count_launches(1);
   return cudaGetLastError();
 }
 }  // namespace
