@@ -1051,7 +1051,7 @@ gpa_status gpa_idleness_blame(const gpa_trace_desc *d, const uint64_t *d_time, c
   uint64_t max_tiles = 0, *d_split = nullptr;
   for (size_t r = 0, cofs = 0; r < round_np.size(); cofs += round_np[r] + 1, r++)
     max_tiles = std::max(max_tiles, chunks[cofs + round_np[r]]);
-  CU(mem.get(&d_split, max_tiles + 1));
+  CU(mem.get(&d_split, 2 * max_tiles + 2));  // split [tiles+1] then the tile -> pair map (u32)
   CU(cudaMemcpyAsync(d_off, d->line_off, (L + 1) * 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_kind, d->line_kind, L, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_scope, d->line_scope, L * 4, cudaMemcpyHostToDevice, st));

@@ -80,13 +80,15 @@ constexpr int kMergeThreads = 256, kMergeItems = kMergeChunk / kMergeThreads;
 
 // merge-path split of every tile start (thread per tile; all searches in flight at once)
 __global__ void k_merge_split(const MergePair *__restrict__ pairs, const uint64_t *__restrict__ tile_start,
-                              uint32_t np, const uint64_t *__restrict__ st, uint64_t *__restrict__ split) {
+                              uint32_t np, const uint64_t *__restrict__ st, uint64_t *__restrict__ split,
+                              uint32_t *__restrict__ tile_pair) {
   const uint64_t n_tiles = tile_start[np];
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= n_tiles;
        c += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t i = 0;
     if (c < n_tiles) {
       const uint32_t p = (uint32_t)(upper_bound_u64(tile_start, np + 1, c) - 1);
+      tile_pair[c] = p;
       const MergePair q = pairs[p];
       const uint64_t na = q.a1 - q.a0, nb = q.b1 - q.a1;
       const uint64_t d = (c - tile_start[p]) * kMergeChunk;
@@ -103,29 +105,69 @@ __global__ void k_merge_split(const MergePair *__restrict__ pairs, const uint64_
 }
 static_assert(kMergeItems * kMergeThreads == kMergeChunk, "tile");
 
+struct MergeTile {
+  uint64_t a0, a1, d0, i0, j0;
+  int la, m;
+};
+
+__device__ __forceinline__ MergeTile merge_tile(const MergePair *__restrict__ pairs,
+                                                const uint64_t *__restrict__ tile_start,
+                                                const uint32_t *__restrict__ tile_pair,
+                                                const uint64_t *__restrict__ split, uint64_t c) {
+  const uint32_t p = tile_pair[c];
+  const MergePair q = pairs[p];
+  const uint64_t na = q.a1 - q.a0, nb = q.b1 - q.a1;
+  const uint64_t d0 = (c - tile_start[p]) * kMergeChunk, d1 = min(d0 + kMergeChunk, na + nb);
+  const bool last = c + 1 == tile_start[p + 1];
+  const uint64_t i0 = split[c], i1 = last ? na : split[c + 1];
+  return MergeTile{q.a0, q.a1, d0, i0, d0 - i0, (int)(i1 - i0), (int)(d1 - d0)};
+}
+
+__device__ __forceinline__ void cp_async8(void *s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+
+// Tiles are double-buffered: while a CTA merges tile c from one buffer, the asynchronous copies
+// (cp.async, no registers) of its next tile land in the other.
 __global__ void __launch_bounds__(kMergeThreads) k_merge(const MergePair *__restrict__ pairs,
                                                        const uint64_t *__restrict__ tile_start, uint32_t np,
                                                        const uint64_t *__restrict__ st,
                                                        const uint32_t *__restrict__ si, uint64_t *__restrict__ dt,
                                                        uint32_t *__restrict__ di,
-                                                       const uint64_t *__restrict__ split) {
-  __shared__ uint64_t sk[kMergeChunk];
-  __shared__ uint32_t sv[kMergeChunk];
+                                                       const uint64_t *__restrict__ split,
+                                                       const uint32_t *__restrict__ tile_pair) {
+  __shared__ __align__(16) uint64_t skb[2][kMergeChunk];
+  __shared__ __align__(16) uint32_t svb[2][kMergeChunk];
   const uint64_t n_tiles = tile_start[np];
-  for (uint64_t c = blockIdx.x; c < n_tiles; c += gridDim.x) {
-    const uint32_t p = (uint32_t)(upper_bound_u64(tile_start, np + 1, c) - 1);
-    const MergePair q = pairs[p];
-    const uint64_t na = q.a1 - q.a0, nb = q.b1 - q.a1;
-    const uint64_t d0 = (c - tile_start[p]) * kMergeChunk, d1 = min(d0 + kMergeChunk, na + nb);
-    const bool last = c + 1 == tile_start[p + 1];
-    const uint64_t i0 = split[c], i1 = last ? na : split[c + 1], j0 = d0 - i0;
-    const int la = (int)(i1 - i0), m = (int)(d1 - d0), lb = m - la;
-    for (int x = threadIdx.x; x < m; x += kMergeThreads) {
-      const uint64_t src = x < la ? q.a0 + i0 + x : q.a1 + j0 + (x - la);
-      sk[x] = st[src];
-      sv[x] = si ? si[src] : (uint32_t)src;
+  auto issue = [&](uint64_t c, int buf) {
+    const MergeTile T = merge_tile(pairs, tile_start, tile_pair, split, c);
+#pragma unroll
+    for (int u = 0; u < kMergeItems; u++) {
+      const int x = (int)threadIdx.x + u * kMergeThreads;
+      if (x < T.m) {
+        const uint64_t src = x < T.la ? T.a0 + T.i0 + x : T.a1 + T.j0 + (x - T.la);
+        cp_async8(&skb[buf][x], st + src);
+        if (si) cp_async4(&svb[buf][x], si + src);
+        else svb[buf][x] = (uint32_t)src;
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  if (blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  for (uint64_t c = blockIdx.x; c < n_tiles; c += gridDim.x, buf ^= 1) {
+    if (c + gridDim.x < n_tiles) issue(c + gridDim.x, buf ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncthreads();
+    const MergeTile T = merge_tile(pairs, tile_start, tile_pair, split, c);
+    uint64_t *sk = skb[buf];
+    uint32_t *sv = svb[buf];
+    const int la = T.la, m = T.m, lb = m - la;
+    const uint64_t d0 = T.d0;
     const int dd = min((int)threadIdx.x * kMergeItems, m);
     int lo = dd > lb ? dd - lb : 0, hi = min(dd, la);
     while (lo < hi) {
@@ -161,9 +203,13 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const MergePair *__rest
         sv[x ^ ((x >> 3) & 31)] = rv[o];
       }
     __syncthreads();
-    for (int x = threadIdx.x; x < m; x += kMergeThreads) {
-      dt[q.a0 + d0 + x] = sk[x ^ ((x >> 3) & 15)];
-      di[q.a0 + d0 + x] = sv[x ^ ((x >> 3) & 31)];
+#pragma unroll
+    for (int u = 0; u < kMergeItems; u++) {
+      const int x = (int)threadIdx.x + u * kMergeThreads;
+      if (x < m) {
+        __stcs(dt + T.a0 + d0 + x, (unsigned long long)sk[x ^ ((x >> 3) & 15)]);
+        __stcs(di + T.a0 + d0 + x, sv[x ^ ((x >> 3) & 31)]);
+      }
     }
     __syncthreads();
   }
@@ -415,9 +461,10 @@ cudaError_t blame_prep(const BlameArgs &a, uint32_t n_lines, cudaStream_t st) {
 cudaError_t blame_merge(const MergePair *pairs, const uint64_t *chunk_start, uint32_t np, uint64_t n_chunks,
                         const uint64_t *st_in, const uint32_t *si, uint64_t *dt, uint32_t *di, uint64_t *split,
                         cudaStream_t st) {
-  k_merge_split<<<grid_for(n_chunks + 1), 256, 0, st>>>(pairs, chunk_start, np, st_in, split);
+  uint32_t *tile_pair = reinterpret_cast<uint32_t *>(split + n_chunks + 1);
+  k_merge_split<<<grid_for(n_chunks + 1), 256, 0, st>>>(pairs, chunk_start, np, st_in, split, tile_pair);
   k_merge<<<(unsigned)(n_chunks < 148 * 16 ? (n_chunks ? n_chunks : 1) : 148 * 16), kMergeThreads, 0, st>>>(
-      pairs, chunk_start, np, st_in, si, dt, di, split);
+      pairs, chunk_start, np, st_in, si, dt, di, split, tile_pair);
   count_launches(2);
   return cudaGetLastError();
 }
