@@ -24,6 +24,8 @@
 //  K_attr_tma (mid-size calls): the same TMA ring, warp-aggregated L2 reductions only.
 //  K_attr_stream (small calls, sparse address spaces via binary search): register streaming.
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -560,14 +562,15 @@ cudaError_t run_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned 
   return cudaGetLastError();
 }
 
-int g_attr_kernel = -1;  // gpa_set_attr_kernel; -1 = read GPA_ATTR_VARIANT once (0 if unset)
+std::atomic<int> g_attr_kernel{-1};  // gpa_set_attr_kernel; -1 = read GPA_ATTR_VARIANT once (0 if unset)
 
 int attr_variant() {  // 0 auto, 1 stream, 2 tma, 3 shared bins, 4 shared rows (when applicable)
-  if (g_attr_kernel < 0) {
+  if (g_attr_kernel.load(std::memory_order_relaxed) < 0) {
     const char *e = getenv("GPA_ATTR_VARIANT");
-    g_attr_kernel = e ? atoi(e) : 0;
+    int expect = -1;
+    g_attr_kernel.compare_exchange_strong(expect, e ? atoi(e) : 0);
   }
-  return g_attr_kernel;
+  return g_attr_kernel.load(std::memory_order_relaxed);
 }
 
 cudaError_t launch_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
@@ -622,7 +625,7 @@ cudaError_t launch_stream(const AttrTables &T, const uint4 *rec, uint64_t n, uns
 
 }  // namespace
 
-void set_attr_kernel(int which) { g_attr_kernel = which; }
+void set_attr_kernel(int which) { g_attr_kernel.store(which, std::memory_order_relaxed); }
 
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr, uint32_t *d_rec_inst,

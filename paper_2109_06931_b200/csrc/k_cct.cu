@@ -15,6 +15,8 @@
 // Every fp64 operation is one correctly rounded __d*_rn call in the oracle's order.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include "gpa_internal.cuh"
@@ -893,16 +895,14 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
   const uint32_t *lev = d_lev;
   const uint64_t *S_f = c->S_f;
   double *excl = c->excl, *incl = c->incl;
-  static int cluster = -1;  // largest cluster the device accepts for k_cct_fold_cl (16, else 8), 0 = none
-  if (cluster < 0) {
-    cluster = 0;
-    if (cudaFuncSetAttribute(k_cct_fold_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
-      cluster = 16;
-    else
-      cluster = 8;
+  // largest cluster the device accepts for k_cct_fold_cl (16, else 8); 0 = none (cooperative grid)
+  static std::atomic<int> cluster{-1};
+  int cs0 = cluster.load(std::memory_order_relaxed);
+  if (cs0 < 0) {
+    cs0 = cudaFuncSetAttribute(k_cct_fold_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess ? 16 : 8;
     cudaGetLastError();
   }
-  for (int cs = cluster; cs >= 8; cs /= 2) {
+  for (int cs = cs0; cs >= 8; cs /= 2) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -917,12 +917,12 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
     e = cudaLaunchKernelEx(&cfg, k_cct_fold_cl, A, lev, S_f, excl, incl);
     if (e == cudaSuccess) {
       count_launches(1);
-      cluster = cs;
+      cluster.store(cs, std::memory_order_relaxed);
       return cudaSuccess;
     }
     cudaGetLastError();
   }
-  cluster = 0;
+  cluster.store(0, std::memory_order_relaxed);
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cct_fold, 512, 0);
   if (e != cudaSuccess) return e;
