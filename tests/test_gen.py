@@ -78,3 +78,27 @@ def test_c4_streams():
         s = w.records_host(k0, 10_000)["stream"]
         assert (np.diff(s.astype(np.int64)) >= 0).all() and s.max() < 384
     assert w.records_host(49_999_999, 1)["stream"][0] == 383
+
+
+def test_trace_sets_are_seeded_and_well_formed():
+    """f4 inputs (gen/trace.py): deterministic per seed, every line non-decreasing in time, ranks
+    grouped, every rank has GPU and CPU lines, routine ids in range, mostly idle-terminated."""
+    from gen.trace import TRACE_CONFIGS, trace_set
+    for name in ("B1", "B2"):
+        a, b = trace_set(name), trace_set(name)
+        for k in ("line_off", "line_kind", "line_scope", "time", "ctx"):
+            assert np.array_equal(a[k], b[k]), k
+        cfg = TRACE_CONFIGS[name]
+        lo = a["line_off"].astype(np.int64)
+        assert lo[0] == 0 and lo[-1] == len(a["time"]) and (np.diff(lo) > 0).all()
+        assert (np.diff(a["line_scope"].astype(np.int64)) >= 0).all() and a["line_scope"][-1] == cfg.scopes - 1
+        for l in range(len(lo) - 1):
+            t = a["time"][lo[l]:lo[l + 1]]
+            assert (np.diff(t.astype(np.int64)) >= 0).all()
+            c = a["ctx"][lo[l]:lo[l + 1]]
+            if a["line_kind"][l] == 1:
+                live = c[c != 0xFFFFFFFF]
+                assert (live < cfg.n_routines).all()
+        for s in range(cfg.scopes):
+            kinds = a["line_kind"][a["line_scope"] == s]
+            assert (kinds == 0).sum() == cfg.gpu_lines and (kinds == 1).sum() == cfg.cpu_lines
