@@ -58,7 +58,7 @@ def test_worked_examples(gpa):
     assert got["blame"][three, 0] == 95 / 6 and got["total"][three] == 30
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("GPA_FUZZ_SEEDS", "30"))))
 def test_random_tiny(gpa, seed):
     rng = np.random.default_rng(1000 + seed)
     _compare(gpa, random_trace(rng, int(rng.integers(1, 6))))

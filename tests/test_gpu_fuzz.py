@@ -74,7 +74,7 @@ def random_records(rng, st, n):
     return rec
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("GPA_FUZZ_SEEDS", "24"))))
 def test_fuzz_whole_path(gpa, seed):
     rng = np.random.default_rng(777 + seed)
     n_func = int(rng.integers(1, 60))
