@@ -12,7 +12,8 @@ frac = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
 data = data[int(len(data) * (1 - frac)):]
 agg = collections.OrderedDict()
 for r in data:
-    n = r[ki].split("(")[0].split("<")[0].replace("(anonymous namespace)::", "")
+    n = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "")
+    n = n.split("(")[0].split("<")[0]
     agg.setdefault(n, [0, 0.0])
     agg[n][0] += 1
     agg[n][1] += float(r[vi].replace(",", ""))
