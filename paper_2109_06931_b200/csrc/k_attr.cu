@@ -376,7 +376,11 @@ done:
 #define GPA_HOT_BINS 32768
 #endif
 constexpr int kHotBins = GPA_HOT_BINS;               // x 4 B = 128 KiB (the rest of the SM's 256 KiB is L1 for the code-map gathers)
-using RingBins = Ring<16, 2, 4>;
+// 31 consumer warps x 1 record per lane (tile = 992 records, 4 x 15.5 KiB stages) + the producer
+// = 1024 threads, 3 tiles of lookahead: C5 15.6 -> 15.4 ms, C4 3.71 -> 3.48 ms against 16 x 2 with
+// lookahead 2 (DESIGN.md §7 geometry sweep)
+using RingBins = Ring<31, 1, 4>;
+constexpr int kLookBins = 3;
 
 __global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
   const uint64_t total = (uint64_t)kSampleChunks * kSampleChunk;
@@ -427,14 +431,14 @@ __device__ __forceinline__ void repay(unsigned long long *H, const uint32_t *bin
   if (b != NONE) red_add_u64(H + b, v);
 }
 
-template <class RG, int NB, bool REC>
+template <class RG, int NB, bool REC, int LOOK = kLook>
 __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_bins(uint64_t base, uint64_t n_gran, uint32_t gshift, const unsigned long long *__restrict__ code,
                 const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
                 unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
                 const uint32_t *__restrict__ bin_of, const uint32_t *__restrict__ thr) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = kLook + 1;
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = LOOK + 1;
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
   uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NB * 4);
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     }
   };
 #pragma unroll
-  for (int q = 0; q < kLook; q++)
+  for (int q = 0; q < LOOK; q++)
     if (blockIdx.x + q * G < ntiles) fetch(q, v[q], c[q]);
   for (uint32_t it0 = 0;; it0 += D) {
 #pragma unroll
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
       const uint32_t it = it0 + q;
       const uint64_t tile = blockIdx.x + it * G;
       if (tile >= ntiles) goto done;
-      if (tile + kLook * G < ntiles) fetch(it + kLook, v[(q + kLook) % D], c[(q + kLook) % D]);
+      if (tile + LOOK * G < ntiles) fetch(it + LOOK, v[(q + LOOK) % D], c[(q + LOOK) % D]);
       const uint64_t left = n - tile * S;
       const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
       uint32_t old[R], idx[R];
@@ -538,7 +542,7 @@ cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsig
   k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of);
   k_codemap_bins<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, code);
   using RG = RingBins;
-  auto kern = ri ? k_attr_bins<RG, kHotBins, true> : k_attr_bins<RG, kHotBins, false>;
+  auto kern = ri ? k_attr_bins<RG, kHotBins, true, kLookBins> : k_attr_bins<RG, kHotBins, false, kLookBins>;
   const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
