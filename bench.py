@@ -180,8 +180,12 @@ def run_gpa(args):
     from paper_2109_06931_b200.parallel import reduce_histogram, shard_range
 
     rank, world, local = _dist_env()
+    local = local % max(1, torch.cuda.device_count())  # (a host-logic check may run 2 ranks on 1 GPU)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = gen.workload(args.config, records=args.records)
@@ -192,11 +196,16 @@ def run_gpa(args):
     ni = s.info["n_inst"]
     stream = torch.cuda.current_stream(dev)
 
-    rec = torch.empty((max(n, 1), 2), dtype=torch.int64, device=dev)
     CH = 1 << 28
-    for k in range(0, n, CH):
-        w.records_device(rec[k:k + CH], a + k, min(CH, n - k))
-    torch.cuda.synchronize()
+
+    def make_shard(a, n):
+        r = torch.empty((max(n, 1), 2), dtype=torch.int64, device=dev)
+        for k in range(0, n, CH):
+            w.records_device(r[k:k + CH], a + k, min(CH, n - k))
+        torch.cuda.synchronize()
+        return r
+
+    rec = make_shard(a, n)
     HU = torch.zeros(ni * 16 + 16, dtype=torch.int64, device=dev)   # H_inst || U, one buffer
     H, U = HU[:ni * 16].view(ni, 16), HU[ni * 16:]
     rows = {sc: max(1, gpa.scope_row_count(s, sc)) for sc in SCOPES}
@@ -253,6 +262,39 @@ def run_gpa(args):
     for _ in range(args.warmup):
         nctx = step(False)
     torch.cuda.synchronize()
+    root_less = 0
+    if world > 1 and not args.no_balance:
+        # Load balance (untimed): rank 0 also runs the analysis after the reduce, so it takes
+        # D fewer records, D = its analysis time / its attribution time per record (measured
+        # here); the shards are regenerated and re-warmed before the timed region.
+        cal = []
+        for _ in range(2):
+            HU.zero_()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(stream)
+            gpa.attribute_samples(s, rec, H, U, n=n, stream=stream)
+            ev[1].record(stream)
+            reduce_histogram(HU, dst=0)
+            ev[2].record(stream)
+            if rank == 0:
+                analyse(False)
+            ev[3].record(stream)
+            torch.cuda.synchronize()
+            cal.append((ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])))
+        t_at, t_an = cal[-1]
+        d = int(t_an / max(t_at, 1e-6) * n) if rank == 0 else 0
+        t = torch.tensor([max(0, d)], dtype=torch.int64, device=dev)
+        dist.broadcast(t, 0)
+        root_less = int(t.item())
+        a2, b2 = shard_range(n_all, rank, world, root_less)
+        if (a2, b2) != (a, b):
+            del rec
+            torch.cuda.empty_cache()
+            a, b, n = a2, b2, b2 - a2
+            rec = make_shard(a, n)
+        for _ in range(args.warmup):
+            nctx = step(False)
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     l0 = gpa.kernel_launches()
@@ -272,10 +314,14 @@ def run_gpa(args):
     launches = gpa.kernel_launches() - l0
     ms = t0.elapsed_time(t1) / args.steps
     attr_ms = sum(x.elapsed_time(y) for x, y in zip(ev_a0, ev_a1)) / len(ev_a0)
+    algo_bytes = 16 * n                              # this rank's K_attr launch
     if world > 1:
         t = torch.tensor([ms, attr_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, attr_ms = t.tolist()
+        nb = torch.tensor([algo_bytes], dtype=torch.int64, device=dev)
+        dist.all_reduce(nb)
+        algo_bytes = int(nb.item())                  # all ranks; divided by N below
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
         dist.all_reduce(lt)
         launches = int(lt.item())
@@ -329,8 +375,7 @@ def run_gpa(args):
             dist.destroy_process_group()
         return
     peak, peak_src = _peaks()
-    algo_bytes = 16 * n                              # per K_attr launch
-    achieved = algo_bytes / (attr_ms / 1e3) / 1e9
+    achieved = algo_bytes / world / (attr_ms / 1e3) / 1e9   # per GPU: mean bytes / slowest launch
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"k_attr_traffic_{w.cfg.name}.json")
     if os.path.exists(tp):
@@ -347,6 +392,7 @@ def run_gpa(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
             "config": {"workload": w.cfg.name, "records": n_all, "records_per_gpu": n, "n_inst": ni,
+                       "root_shard_less": root_less,
                        "n_func": s.info["n_func"], "n_call": s.info["n_call"], "cct_contexts": int(nctx),
                        "parallelism": f"record shards x{world}, NCCL reduce of H||U",
                        "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
@@ -371,6 +417,8 @@ def main():
     ap.add_argument("--records", type=int, default=None, help="override the config's record count")
     ap.add_argument("--impl", default="gpa", choices=["gpa", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="N > 1 process group (gloo: a host-logic check only)")
+    ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

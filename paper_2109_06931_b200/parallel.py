@@ -9,11 +9,23 @@ is associative, so the result is bit-identical for every rank count and shard sp
 from __future__ import annotations
 
 
-def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
-    """Records [floor(r*n/N), floor((r+1)*n/N)) of rank r of N (balanced by records)."""
+def shard_range(n: int, rank: int, world: int, root_less: int = 0) -> tuple[int, int]:
+    """Records [floor(r*n/N), floor((r+1)*n/N)) of rank r of N (balanced by records).
+
+    root_less = D > 0: rank 0 also runs the roll-up / CCT / metrics after the reduce, so it
+    takes D records fewer than each other rank (D = that analysis time in records of
+    attribution time, measured by bench.py): n0 = max(0, floor((n - (N-1) D) / N)) records
+    [0, n0) for rank 0, the rest [n0, n) split evenly over ranks 1..N-1.  Any split gives the
+    same reduced histogram (integer sums)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"rank {rank} of {world}")
-    return (n * rank) // world, (n * (rank + 1)) // world
+    if root_less <= 0 or world == 1:
+        return (n * rank) // world, (n * (rank + 1)) // world
+    n0 = max(0, (n - (world - 1) * root_less) // world)
+    if rank == 0:
+        return 0, n0
+    m, k, o = n - n0, rank - 1, world - 1
+    return n0 + (m * k) // o, n0 + (m * (k + 1)) // o
 
 
 def reduce_histogram(hist, dst: int = 0, group=None) -> None:

@@ -25,12 +25,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, records, out_path):
+def _worker(rank, world, port, name, records, out_path, root_less=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         w = gen.workload(name, records=records)
-        a, b = shard_range(w.cfg.records, rank, world)
+        a, b = shard_range(w.cfg.records, rank, world, root_less)
         rec = w.records_host(a, b - a)
         H, U, _ = oracle.attribute(w.structure, rec)
         HU = torch.from_numpy(np.concatenate([H.reshape(-1), U]).view(np.int64).copy())
@@ -41,10 +41,14 @@ def _worker(rank, world, port, name, records, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,records,world", [("C2", 100_003, 2), ("C4", 60_001, 2), ("C1", 1, 2), ("C1", 0, 2)])
-def test_sharded_reduce_equals_single_process(tmp_path, name, records, world):
+@pytest.mark.parametrize("name,records,world,root_less", [("C2", 100_003, 2, 0), ("C4", 60_001, 2, 0), ("C1", 1, 2, 0),
+                                                       ("C1", 0, 2, 0), ("C2", 100_003, 3, 20_000),
+                                                       ("C4", 60_001, 2, 10 ** 9)])
+def test_sharded_reduce_equals_single_process(tmp_path, name, records, world, root_less):
+    """Equal shards, and bench.py's load-balanced split (rank 0 lighter by root_less records,
+    down to an empty rank-0 shard), reduce to the single-process histogram."""
     out = str(tmp_path / "hu.npy")
-    mp.start_processes(_worker, args=(world, _free_port(), name, records, out), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), name, records, out, root_less), nprocs=world, join=True,
                        start_method="spawn")
     got = np.load(out).view(np.uint64)
     w = gen.workload(name, records=records)
@@ -62,6 +66,23 @@ def test_shard_range_partitions():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def test_shard_range_root_less_partitions():
+    """Load-balanced split: a partition of [0, n); rank 0 holds root_less records fewer than
+    the others (up to rounding), or none when root_less is too large."""
+    for n in [0, 5, 1000, 4_000_000_000]:
+        for world in [2, 3, 8]:
+            for d in [1, 17, 143_000_000, 10 ** 12]:
+                parts = [shard_range(n, r, world, d) for r in range(world)]
+                assert parts[0][0] == 0 and parts[-1][1] == n
+                assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+                sizes = [b - a for a, b in parts]
+                assert max(sizes[1:]) - min(sizes[1:]) <= 1
+                if (world - 1) * d <= n:
+                    assert abs((sizes[1] - sizes[0]) - d) <= world
+                else:
+                    assert sizes[0] == 0
 
 
 def _blame_worker(rank, world, port, out_path):
