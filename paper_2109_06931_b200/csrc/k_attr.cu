@@ -376,11 +376,12 @@ done:
 #define GPA_HOT_BINS 32768
 #endif
 constexpr int kHotBins = GPA_HOT_BINS;               // x 4 B = 128 KiB (the rest of the SM's 256 KiB is L1 for the code-map gathers)
-// 31 consumer warps x 1 record per lane (tile = 992 records, 4 x 15.5 KiB stages) + the producer
-// = 1024 threads, 3 tiles of lookahead: C5 15.6 -> 15.4 ms, C4 3.71 -> 3.48 ms against 16 x 2 with
-// lookahead 2 (DESIGN.md §7 geometry sweep)
-using RingBins = Ring<31, 1, 4>;
-constexpr int kLookBins = 3;
+// 31 consumer warps x 2 records per lane (tile = 1984 records, 2 x 31 KiB stages) + the producer
+// = 1024 threads, 1 tile of lookahead: C5 15.6 -> 14.9 ms, C4 3.71 -> 3.21 ms against 16 x 2 x 4
+// stages with lookahead 2 (DESIGN.md §7 geometry sweep; fewer stage releases per record, each of
+// which costs a proxy fence that waits for the warp's outstanding memory operations)
+using RingBins = Ring<31, 2, 2>;
+constexpr int kLookBins = 1;
 
 __global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
   const uint64_t total = (uint64_t)kSampleChunks * kSampleChunk;
