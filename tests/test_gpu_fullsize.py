@@ -1,8 +1,9 @@
-"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (one
-gpa_attribute_samples call over the whole device-resident stream): the complete histogram
-H || U bit-exact against the oracle run chunk by chunk on the host (16 threads), sampled
-per-record attributions, the > 2^32 planted bin (C5), and CCT / metrics on the full
-histogram.  Slow (about a minute each)."""
+"""Parity at BASELINE.json's full sizes (all five configs), in the launch configuration
+bench.py times (one gpa_attribute_samples call over the whole device-resident stream): the
+complete histogram H || U bit-exact against the oracle run chunk by chunk on the host (all
+host threads), sampled per-record attributions, the > 2^32 planted bin (C5), the CCT
+(topology exact, fp64 within 1e-9) with its EXCL/INCL metrics, and every scope's roll-up and
+metrics on the full histogram.  Slow (about a minute for C4 / C5)."""
 import os
 
 import numpy as np
@@ -39,7 +40,7 @@ def _oracle_full(w, chunk=1 << 27):
     return H, U
 
 
-@pytest.mark.parametrize("name", ["C4", "C5"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
 def test_full_size_histogram_bit_exact(gpa, name):
     w = gen.workload(name)
     n = w.cfg.records
@@ -52,12 +53,13 @@ def test_full_size_histogram_bit_exact(gpa, name):
     gpa.attribute_samples(s, rec, H, U)
     # per-record attributions on sampled windows (a second call over slices, rec_inst on)
     rng = np.random.default_rng(11)
-    for k0 in [0, n - 100_000] + [int(x) for x in rng.integers(0, n - 100_000, 3)]:
-        ri = torch.empty(100_000, dtype=torch.int32, device="cuda")
+    win = min(100_000, n)
+    for k0 in [0, n - win] + [int(x) for x in rng.integers(0, n - win + 1, 3)]:
+        ri = torch.empty(win, dtype=torch.int32, device="cuda")
         H2 = torch.zeros_like(H)
         U2 = torch.zeros_like(U)
-        gpa.attribute_samples(s, rec[k0:k0 + 100_000], H2, U2, ri)
-        _, _, rio = oracle.attribute(w.structure, w.records_host(k0, 100_000), rec_inst=True)
+        gpa.attribute_samples(s, rec[k0:k0 + win], H2, U2, ri)
+        _, _, rio = oracle.attribute(w.structure, w.records_host(k0, win), rec_inst=True)
         assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
     torch.cuda.synchronize()
     Hg = H.cpu().numpy().view(np.uint64)
@@ -75,8 +77,21 @@ def test_full_size_histogram_bit_exact(gpa, name):
     g = c.to_numpy()
     assert g["n"] == R["n"] and np.array_equal(g["parent"], R["parent"]) and np.array_equal(g["site"], R["site"])
     assert np.allclose(g["incl"], R["incl"], rtol=1e-9, atol=0)
-    fm = torch.empty((s.info["n_func"], 33), dtype=torch.float64, device="cuda")
-    gpa.derive_metrics(s, "FUNC", H, metrics=fm)
-    hist, mix = oracle.scope_hist(w.structure, Ho, "FUNC")
-    assert np.array_equal(fm.cpu().numpy().view(np.uint64), oracle.derive_u64(hist, mix).view(np.uint64))
+    assert np.allclose(g["excl"], R["excl"], rtol=1e-9, atol=0) and np.allclose(g["frac"], R["frac"], rtol=1e-9, atol=0)
+    for scope, V in [("CCT_EXCL", R["excl"]), ("CCT_INCL", R["incl"])]:
+        met = torch.empty((max(R["n"], 1), 33), dtype=torch.float64, device="cuda")
+        gpa.derive_metrics(s, scope, cct=c, metrics=met)
+        assert np.allclose(met.cpu().numpy()[:R["n"]], oracle.derive_f64(V), rtol=1e-9, atol=0, equal_nan=True), scope
     c.free()
+    # every scope's roll-up (u64, bit-exact) and derived metrics (closed forms on u64: bit-exact)
+    for scope in ["INST", "LINE", "LOOP", "INLINE", "FUNC"]:
+        rows = max(1, gpa.scope_row_count(s, scope))
+        sh = torch.empty((rows, 16), dtype=torch.int64, device="cuda")
+        sm = torch.empty((rows, 16), dtype=torch.int64, device="cuda")
+        fm = torch.empty((rows, 33), dtype=torch.float64, device="cuda")
+        gpa.derive_metrics(s, scope, H, scope_hist=sh, scope_mix=sm, metrics=fm)
+        hist, mix = oracle.scope_hist(w.structure, Ho, scope)
+        k = len(hist)
+        assert np.array_equal(sh.cpu().numpy().view(np.uint64)[:k], hist), scope
+        assert np.array_equal(sm.cpu().numpy().view(np.uint64)[:k], mix), scope
+        assert np.array_equal(fm.cpu().numpy()[:k].view(np.uint64), oracle.derive_u64(hist, mix).view(np.uint64)), scope
