@@ -9,7 +9,7 @@
 //     spread addresses (each RED lane costs ~1.3 SM cycles of LSU issue), far below the
 //     ~4.3e11 records/s the HBM roofline allows; shared-memory u32 atomics sustain ~1.3e12/s.
 //     So the rows of the hottest instructions are privatised per CTA in shared memory:
-//       1. k_sample       instruction hits in 64 evenly spaced chunks (2^21 records)
+//       1. k_sample       instruction hits in 16 384 evenly spaced runs of 128 records (2^21)
 //       2. k_vhist/k_pick/k_assign   choose up to kHotRows instructions with the most hits
 //       3. k_codemap      per-call code map: cold instruction i -> i<<4, hot row r -> r<<4|1,
 //                         unmapped -> ~0 (one gather resolves a record, one OR forms the index)
@@ -162,7 +162,10 @@ constexpr int kHotSlots = GPA_VALID_SLOTS;
 constexpr int kHotRows = 3328;                     // 3328 x 12 x 4 B = 156 KiB
 using RingHot = Ring<16, 2, 4>;                    // 4 x 16 KiB stages
 constexpr int kLook = 2;                           // tiles of records + codes in flight ahead
-constexpr int kSampleChunks = 64, kSampleChunk = 1 << 15;
+#ifndef GPA_SAMPLE_CHUNK_LOG
+#define GPA_SAMPLE_CHUNK_LOG 7  // 16 384 runs of 128 records: the sample spans ~16 k launch bursts (tools/sample_sweep.sh)
+#endif
+constexpr int kSampleChunk = 1 << GPA_SAMPLE_CHUNK_LOG, kSampleChunks = (1 << 21) / kSampleChunk;
 constexpr uint64_t kHotMinRecords = (uint64_t)kSampleChunks * kSampleChunk;
 constexpr int kVBins = 4096;
 
