@@ -642,9 +642,15 @@ cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, u
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
   const int var = attr_variant();
   const bool hot_ok = T.mode == 0 && n >= kHotMinRecords && T.n_inst >= 1024;
-  if ((var == 0 || var == 3) && hot_ok) return launch_bins(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+  // automatic choice: the bins kernel's per-call pre-pass (sample, value histogram, code map:
+  // ~40-90 us, growing with n_inst) pays off from ~6e6 records and 40 records per instruction
+  // on (measured crossovers: C2 ~5e6, C5 ~2e7 records; tools/attr_variants.py); below that the
+  // register-streaming kernel is fastest
+  const bool bins_auto = hot_ok && n >= 6000000ull && n >= 40ull * T.n_inst;
+  if ((var == 0 && bins_auto) || (var == 3 && hot_ok))
+    return launch_bins(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
   if (var == 4 && hot_ok) return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
-  if (var == 1 || n < 4096) {
+  if (var == 1 || n < 4096 || (var == 0 && T.mode == 0)) {
     return T.mode == 0 ? launch_stream<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
                        : launch_stream<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
   }
