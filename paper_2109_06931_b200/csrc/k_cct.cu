@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <stdint.h>
 
@@ -47,7 +48,16 @@ struct PropArgs {
   uint64_t *w, *W, *paths;
   uint8_t *fact, *dact;
   unsigned long long *count;
+  uint32_t *q0, *q1;  // worklists, max(n_func, n_dag) entries each
 };
+
+// set byte flag[i] to 1; true if it was 0 (byte flags live in 32-bit words: atomicOr)
+__device__ __forceinline__ bool set_flag(volatile uint8_t *flag, uint32_t i) {
+  uintptr_t a = (uintptr_t)(flag + i);
+  unsigned *word = (unsigned *)(a & ~(uintptr_t)3);
+  const unsigned sh = 8u * (unsigned)(a & 3);
+  return ((atomicOr(word, 1u << sh) >> sh) & 0xFFu) == 0;
+}
 
 // Single CTA: the call graph is small (<= a few thousand functions); rounds are separated
 // by __syncthreads, which also orders the memory updates inside the CTA.  SM = true: the
@@ -81,29 +91,45 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
   }
   // Step 2: "if a function has samples and none of its incoming call edges has a non-zero
   // weight, we assign each of its incoming call edges a weight of one; we repeat this
-  // propagation through callers".  Each function's in-edges are written only by
-  // the thread that owns the function, so a round's result is race-free.  Exact counts skip
-  // it ("For call graphs based on samples", R24).
-  for (; !A.exact;) {
+  // propagation through callers".  A function's in-edges are written only when that
+  // function is processed, so each active function needs processing exactly once: a worklist
+  // of the initially active functions, then of the callers each round activates (the least
+  // fixpoint of R11, O(F + E) work; rounds = length of the longest zero-weight chain).
+  // Exact counts skip it ("For call graphs based on samples", R24).
+  __shared__ uint32_t qn[2];
+  auto run_worklist = [&](uint32_t n_items, volatile uint8_t *act, const uint32_t *in_ptr, const uint32_t *in_e,
+                          bool dag) {
     __syncthreads();
-    if (t == 0) changed = 0;
+    if (t == 0) qn[0] = 0;
     __syncthreads();
-    for (uint32_t f = t; f < A.n_func; f += nt) {
-      uint32_t a = A.fin_ptr[f], b = A.fin_ptr[f + 1];
-      if (!fact[f] || a == b) continue;
-      bool zero = true;
-      for (uint32_t k = a; k < b; k++) zero &= w[A.fin_e[k]] == 0;
-      if (!zero) continue;
-      for (uint32_t k = a; k < b; k++) {
-        uint32_t e = A.fin_e[k];
-        w[e] = 1;
-        fact[A.caller[e]] = 1;
+    for (uint32_t x = t; x < n_items; x += nt)
+      if (act[x]) A.q0[atomicAdd(&qn[0], 1u)] = x;
+    uint32_t cur = 0;
+    for (;;) {
+      __syncthreads();
+      const uint32_t m = qn[cur];
+      if (m == 0) break;
+      if (t == 0) qn[cur ^ 1] = 0;
+      __syncthreads();
+      uint32_t *qc = cur ? A.q1 : A.q0, *qx = cur ? A.q0 : A.q1;
+      for (uint32_t i = t; i < m; i += nt) {
+        const uint32_t x = qc[i], a = in_ptr[x], b = in_ptr[x + 1];
+        if (a == b) continue;
+        bool zero = true;
+        for (uint32_t k = a; k < b; k++) zero &= w[in_e[k]] == 0;
+        if (!zero) continue;
+        for (uint32_t k = a; k < b; k++) {
+          const uint32_t e = in_e[k];
+          w[e] = 1;
+          const uint32_t u = dag ? A.scc_of[A.caller[e]] : A.caller[e];
+          if (set_flag(act, u)) qx[atomicAdd(&qn[cur ^ 1], 1u)] = u;
+        }
       }
-      changed = 1;
+      __threadfence_block();
+      cur ^= 1;
     }
-    __syncthreads();
-    if (!changed) break;
-  }
+  };
+  if (!A.exact) run_worklist(A.n_func, fact, A.fin_ptr, A.fin_e, false);
   // DAG activity, then the guard (R12): the same rule on external in-edges of DAG nodes
   // (samples mode only, like Step 2)
   __syncthreads();
@@ -112,26 +138,7 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
     for (uint32_t k = A.dmem_ptr[X]; k < A.dmem_ptr[X + 1]; k++) act |= fact[A.dmem[k]];
     dact[X] = act;
   }
-  for (; !A.exact;) {
-    __syncthreads();
-    if (t == 0) changed = 0;
-    __syncthreads();
-    for (uint32_t X = t; X < A.n_dag; X += nt) {
-      uint32_t a = A.din_ptr[X], b = A.din_ptr[X + 1];
-      if (!dact[X] || a == b) continue;
-      bool zero = true;
-      for (uint32_t k = a; k < b; k++) zero &= w[A.din_e[k]] == 0;
-      if (!zero) continue;
-      for (uint32_t k = a; k < b; k++) {
-        uint32_t e = A.din_e[k];
-        w[e] = 1;
-        dact[A.scc_of[A.caller[e]]] = 1;
-      }
-      changed = 1;
-    }
-    __syncthreads();
-    if (!changed) break;
-  }
+  if (!A.exact) run_worklist(A.n_dag, dact, A.din_ptr, A.din_e, true);
   // W_X = total weight of the external calls into X
   __syncthreads();
   for (uint32_t X = t; X < A.n_dag; X += nt) {
@@ -798,7 +805,8 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
   // paths[] scratch lives behind W in the caller's allocation? keep it separate and simple:
   static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
   uint64_t *paths = nullptr;
-  cudaError_t e = pool_alloc((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1), st);
+  const size_t nq = std::max<size_t>(s->info.n_func, s->info.n_dag) + 1;
+  cudaError_t e = pool_alloc((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1) + 8 * nq, st);
   if (e != cudaSuccess) return e;
   PropArgs A;
   A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels; A.exact = exact ? 1 : 0; A.do_count = count ? 1 : 0;
@@ -807,7 +815,9 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
   A.dmem = s->d_dmem; A.dlev_ptr = s->d_dlev_ptr; A.dlev_node = s->d_dlev_node; A.nontriv = s->d_dag_nontrivial;
   A.w = d_w; A.W = d_W; A.paths = paths; A.fact = d_func_active; A.dact = d_dag_active; A.count = d_count;
   A.n_call = s->info.n_call;
-  const size_t sm = 8ull * (A.n_call + A.n_dag) + A.n_func + A.n_dag;
+  A.q0 = reinterpret_cast<uint32_t *>(paths + s->info.n_dag + 1);
+  A.q1 = A.q0 + nq;
+  const size_t sm = 8ull * (A.n_call + A.n_dag) + A.n_func + A.n_dag + 8;
   if (sm <= kPropSmem) {
     if (sm > 48 * 1024 &&
         (e = cudaFuncSetAttribute(k_propagate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPropSmem)) !=
