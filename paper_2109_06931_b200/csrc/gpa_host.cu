@@ -32,6 +32,9 @@ cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    return cudaMallocAsync(p, bytes, st);  // inside a CUDA-graph capture: a graph memory node
   if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, st);
   {
     std::lock_guard<std::mutex> lock(mu);
