@@ -2,26 +2,31 @@
 // stall-reason histogram (§4.2 P:365-374 "an instruction address, a stall reason,
 // and a count"; §4.5 P:475-479 raw metric = sum; §5 P:614-617 disjoint relocated ranges).
 //
-// Three kernels, chosen by launch_attribute (DESIGN.md §7 has the measurements behind them):
+// Four kernels; launch_attribute picks K_attr_bins for large calls (granule map, from
+// max(6e6, 40 x n_inst) records) and K_attr_stream below (DESIGN.md §7 has the measurements).
 //
-//  K_attr_hot (default for large calls, granule map present)
-//     Measured on B200 (tools/microbench.cu): u64 reductions into L2 sustain ~1.9e11/s at
-//     spread addresses (each RED lane costs ~1.3 SM cycles of LSU issue), far below the
-//     ~4.3e11 records/s the HBM roofline allows; shared-memory u32 atomics sustain ~1.3e12/s.
-//     So the rows of the hottest instructions are privatised per CTA in shared memory:
-//       1. k_sample       instruction hits in 16 384 evenly spaced runs of 128 records (2^21)
-//       2. k_vhist/k_pick/k_assign   choose up to kHotRows instructions with the most hits
-//       3. k_codemap      per-call code map: cold instruction i -> i<<4, hot row r -> r<<4|1,
-//                         unmapped -> ~0 (one gather resolves a record, one OR forms the index)
-//       4. k_attr_hot     persistent CTA per SM.  A producer warp streams record tiles
-//                         HBM -> shared memory with 1-D bulk copies (cp.async.bulk = TMA engine,
-//                         L2 evict-first) into a 4-stage mbarrier ring; 16 consumer warps copy
-//                         their records to registers, free the stage, gather the codes of the
-//                         tile two ahead, and accumulate: hot valid-slot records -> u32 shared
-//                         atomics (a u32 wrap, old + cnt < old, is repaid as +2^32 in L2, so
-//                         any count is exact), others -> u64 L2 reductions.  Each CTA flushes
-//                         its rows once.  The hot set only moves where a count lands first.
-//  K_attr_tma (mid-size calls): the same TMA ring, warp-aggregated L2 reductions only.
+// Why privatise: measured on B200 (tools/microbench.cu), u64 reductions into L2 sustain
+// ~1.9e11/s at spread addresses (each RED lane costs ~1.3 SM cycles of LSU issue), far below
+// the ~4.3e11 records/s the HBM roofline allows; shared-memory u32 atomics sustain ~1.3e12/s.
+//
+//  K_attr_bins (default for large calls): the ~32 k most-sampled (instruction, slot) BINS live
+//     in shared memory, per CTA.  Per call:
+//       1. k_sample_bins  bin hits of 2^21 sampled records (16 384 evenly spaced runs of 128)
+//       2. k_vhist/k_pick/k_assign_bins   choose the hottest bins; each instruction gets a
+//                         12-bit hot-slot mask and a base index into the shared table
+//       3. k_codemap_bins per-call 64-bit code per granule (instruction, hot mask, base): one
+//                         gather resolves a record
+//       4. k_attr_bins    persistent CTA per SM (1024 threads).  One producer lane streams
+//                         record tiles HBM -> shared memory with 1-D bulk copies (cp.async.bulk
+//                         = TMA engine, L2 evict-first) into a 2-stage mbarrier ring; 31 consumer
+//                         warps copy their 2 records per lane to registers, free the stage (proxy
+//                         fence + arrive), gather the codes of the next tile, and accumulate: hot
+//                         records -> u32 shared atomics (a u32 wrap, old + cnt < old, is repaid as
+//                         +2^32 in L2, so any count is exact), others -> u64 L2 reductions.  Each
+//                         CTA flushes its bins once.  The hot set only moves where a count lands.
+//  K_attr_hot: the same with whole 12-slot rows of the hottest instructions (k_sample, k_assign,
+//     k_codemap; 16 consumer warps, 4 stages).
+//  K_attr_tma: the TMA ring with warp-aggregated L2 reductions only.
 //  K_attr_stream (small calls, sparse address spaces via binary search): register streaming.
 #include <cuda_runtime.h>
 
@@ -368,8 +373,8 @@ done:
 
 // ---- K_attr_bins: heavy-hitter BINS in shared memory (default) ---------------------------------
 // Same pipeline as K_attr_hot, but the shared table holds individual (instruction, slot) bins
-// rather than whole 12-slot rows: with the same 160 KiB it covers the ~40 k most-sampled bins
-// (C5: 75 % of records vs 67 % for 3 328 rows), so fewer records fall back to L2 reductions.
+// rather than whole 12-slot rows: 128 KiB cover the 32 768 most-sampled bins (C5: ~70 % of
+// records vs 67 % for 3 328 rows in 156 KiB), so fewer records fall back to L2 reductions.
 // Per call: k_sample_bins counts sampled records per bin; the top kHotBins bins are chosen by
 // the same value histogram / threshold; k_assign_bins gives each instruction a 12-bit mask of
 // its hot slots and a base index (atomic cursor) and records bin_of[idx] = inst<<4 | slot;
