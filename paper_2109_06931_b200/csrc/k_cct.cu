@@ -49,6 +49,8 @@ struct PropArgs {
   uint8_t *fact, *dact;
   unsigned long long *count;
   uint32_t *q0, *q1;  // worklists, max(n_func, n_dag) entries each
+  uint32_t n_ext;     // external call sites (din_e entries)
+  uint32_t stage_dp;  // SM only: the DP's static tables fit behind the mutable state
 };
 
 // set byte flag[i] to 1; true if it was 0 (byte flags live in 32-bit words: atomicOr)
@@ -155,21 +157,59 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
   // (skipped when the caller builds the tree into a static-bound allocation and reads the
   // size back afterwards)
   if (!A.do_count) return;
-  for (uint32_t L = 0; L < A.n_lev; L++) {
+  if (SM && A.stage_dp) {
+    // The level loop is a chain of dependent reads; with the weights final, stage per
+    // external in-edge its source DAG node (or NONE when w = 0) and per level slot the node
+    // and its in-edge range in shared memory in one coalesced pass, so each of the
+    // dag_levels rounds costs shared-memory latency only.
+    uint32_t *src = reinterpret_cast<uint32_t *>(psm + 8ull * (A.n_call + A.n_dag) + ((A.n_func + A.n_dag + 7) & ~7u));
+    uint32_t *lx = src + A.n_ext, *la = lx + A.n_dag, *lb = la + A.n_dag;
     __syncthreads();
-    for (uint32_t q = A.dlev_ptr[L] + t; q < A.dlev_ptr[L + 1]; q += nt) {
-      uint32_t X = A.dlev_node[q];
-      uint32_t a = A.din_ptr[X], b = A.din_ptr[X + 1];
-      unsigned long long p = 0;
-      if (a == b) {
-        p = dact[X] ? 1 : 0;
-      } else {
-        for (uint32_t k = a; k < b; k++) {
-          uint32_t e = A.din_e[k];
-          if (w[e]) p = min(SAT, p + paths[A.scc_of[A.caller[e]]]);
+    for (uint32_t k = t; k < A.n_ext; k += nt) {
+      const uint32_t e = A.din_e[k];
+      src[k] = w[e] ? A.scc_of[A.caller[e]] : 0xFFFFFFFFu;
+    }
+    for (uint32_t q = t; q < A.n_dag; q += nt) {
+      const uint32_t X = A.dlev_node[q];
+      lx[q] = X;
+      la[q] = A.din_ptr[X];
+      lb[q] = A.din_ptr[X + 1];
+    }
+    __syncthreads();
+    uint32_t q0 = 0;
+    for (uint32_t L = 0; L < A.n_lev; L++) {
+      const uint32_t q1 = A.dlev_ptr[L + 1];
+      for (uint32_t q = q0 + t; q < q1; q += nt) {
+        const uint32_t X = lx[q], a = la[q], b = lb[q];
+        unsigned long long p = 0;
+        if (a == b) {
+          p = dact[X] ? 1 : 0;
+        } else {
+          for (uint32_t k = a; k < b; k++)
+            if (src[k] != 0xFFFFFFFFu) p = min(SAT, p + paths[src[k]]);
         }
+        paths[X] = p;
       }
-      paths[X] = p;
+      q0 = q1;
+      __syncthreads();
+    }
+  } else {
+    for (uint32_t L = 0; L < A.n_lev; L++) {
+      __syncthreads();
+      for (uint32_t q = A.dlev_ptr[L] + t; q < A.dlev_ptr[L + 1]; q += nt) {
+        uint32_t X = A.dlev_node[q];
+        uint32_t a = A.din_ptr[X], b = A.din_ptr[X + 1];
+        unsigned long long p = 0;
+        if (a == b) {
+          p = dact[X] ? 1 : 0;
+        } else {
+          for (uint32_t k = a; k < b; k++) {
+            uint32_t e = A.din_e[k];
+            if (w[e]) p = min(SAT, p + paths[A.scc_of[A.caller[e]]]);
+          }
+        }
+        paths[X] = p;
+      }
     }
   }
   __syncthreads();
@@ -817,7 +857,12 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
   A.n_call = s->info.n_call;
   A.q0 = reinterpret_cast<uint32_t *>(paths + s->info.n_dag + 1);
   A.q1 = A.q0 + nq;
-  const size_t sm = 8ull * (A.n_call + A.n_dag) + A.n_func + A.n_dag + 8;
+  A.n_ext = s->n_ext_calls;
+  size_t sm = 8ull * (A.n_call + A.n_dag) + A.n_func + A.n_dag + 8;
+  const size_t sm_dp = 8ull * (A.n_call + A.n_dag) + ((A.n_func + A.n_dag + 7) & ~7ull) + 4ull * A.n_ext +
+                       12ull * A.n_dag;
+  A.stage_dp = count && sm_dp <= kPropSmem ? 1u : 0u;
+  if (A.stage_dp) sm = std::max(sm, sm_dp);
   if (sm <= kPropSmem) {
     if (sm > 48 * 1024 &&
         (e = cudaFuncSetAttribute(k_propagate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPropSmem)) !=
