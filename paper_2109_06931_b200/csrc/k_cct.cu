@@ -479,7 +479,7 @@ __host__ __device__ inline size_t small2_smem(uint32_t n_func, uint32_t m) {
 
 __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_func, uint32_t m, uint32_t n_dag,
                                                      const uint32_t *din_ptr, const uint8_t *dact, uint32_t *lev_out,
-                                                     unsigned long long *built) {
+                                                     unsigned long long *built, uint32_t stage) {
   extern __shared__ __align__(16) uint8_t sm2[];
   __shared__ uint32_t lev[kSmallLevels + 1];
   double *eratio = reinterpret_cast<double *>(sm2);
@@ -491,6 +491,20 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
   uint8_t *ekind = reinterpret_cast<uint8_t *>(nzc + n_func);
   uint8_t *ckind = ekind + m, *nkind = ckind + kSmallCap;
   const uint32_t t = threadIdx.x, nt = blockDim.x;
+  // stage = 1: the static tables every level reads (DAG members, external calls per function)
+  // are copied to shared memory once, so a level costs shared-memory latency only
+  const uint32_t *dmem_ptr = A.dmem_ptr, *dmem = A.dmem, *fout_ptr = A.fout_ptr;
+  if (stage) {
+    uint32_t *sp = reinterpret_cast<uint32_t *>(sm2 + ((small2_smem(n_func, m) + 15) & ~(size_t)15));
+    uint32_t *sdp = sp, *sdm = sdp + n_dag + 1, *sfp = sdm + n_func;
+    for (uint32_t x = t; x <= n_dag; x += nt) sdp[x] = A.dmem_ptr[x];
+    for (uint32_t x = t; x < n_func; x += nt) sdm[x] = A.dmem[x];
+    for (uint32_t x = t; x <= n_func; x += nt) sfp[x] = A.fout_ptr[x];
+    dmem_ptr = sdp;
+    dmem = sdm;
+    fout_ptr = sfp;
+    __syncthreads();
+  }
   for (uint32_t q = t; q < m; q += nt) {  // the child each weighted external call creates
     const uint32_t e = A.fout_e[q];
     const uint64_t we = A.w[e];
@@ -503,7 +517,7 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
   __syncthreads();
   for (uint32_t g = t; g < n_func; g += nt) {
     uint32_t c = 0;
-    for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) c += ekind[q] != kSkip;
+    for (uint32_t q = fout_ptr[g]; q < fout_ptr[g + 1]; q++) c += ekind[q] != kSkip;
     nzc[g] = (uint16_t)c;
   }
   uint32_t running = 0;
@@ -550,9 +564,9 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
           f = A.frac[c];
         }
         if (k == GPA_CTX_SCC) {
-          cnt = A.dmem_ptr[nd + 1] - A.dmem_ptr[nd];
+          cnt = dmem_ptr[nd + 1] - dmem_ptr[nd];
         } else {
-          g = k == GPA_CTX_SCC_MEMBER ? nd : A.dmem[A.dmem_ptr[nd]];
+          g = k == GPA_CTX_SCC_MEMBER ? nd : dmem[dmem_ptr[nd]];
           cnt = nzc[g];
         }
       }
@@ -561,8 +575,8 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
       if (c < b) {
         if (k == GPA_CTX_SCC) {  // members in ascending function id (R14)
           uint32_t d = o;
-          for (uint32_t q = A.dmem_ptr[nd]; q < A.dmem_ptr[nd + 1]; q++, d++) {
-            const uint32_t mf = A.dmem[q];
+          for (uint32_t q = dmem_ptr[nd]; q < dmem_ptr[nd + 1]; q++, d++) {
+            const uint32_t mf = dmem[q];
             A.parent[d] = c;
             A.site[d] = NONE;
             A.node[d] = mf;
@@ -576,7 +590,7 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
           }
         } else {  // weighted external calls, ascending call instruction (R15, R17)
           uint32_t d = o;
-          for (uint32_t q = A.fout_ptr[g]; q < A.fout_ptr[g + 1]; q++) {
+          for (uint32_t q = fout_ptr[g]; q < fout_ptr[g + 1]; q++) {
             const uint8_t ek = ekind[q];
             if (ek == kSkip) continue;
             const double fr = __dmul_rn(f, eratio[q]);
@@ -935,12 +949,15 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
   LevelArgs A = level_args(s, c);
   const uint32_t m_ext = s->n_ext_calls;
   const size_t sm2 = small2_smem(s->info.n_func, m_ext);
+  const size_t sm2s = ((sm2 + 15) & ~(size_t)15) + 4ull * (s->info.n_dag + 1 + 2ull * s->info.n_func + 1);
+  const uint32_t stage = sm2s <= 200 * 1024 ? 1u : 0u;
   cudaError_t e = cudaSuccess;
   if (sm2 <= 200 * 1024 && s->info.n_func < 65536) {
-    e = cudaFuncSetAttribute(k_cct_small2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    const size_t smx = stage ? sm2s : sm2;
+    e = cudaFuncSetAttribute(k_cct_small2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smx);
     if (e != cudaSuccess) return e;
-    k_cct_small2<<<1, 1024, sm2, st>>>(A, s->info.n_func, m_ext, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev,
-                                       d_built);
+    k_cct_small2<<<1, 1024, smx, st>>>(A, s->info.n_func, m_ext, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev,
+                                       d_built, stage);
   } else {
     k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built);
   }
