@@ -13,7 +13,7 @@ from paper_2109_06931_b200 import gpa
 KERNELS = [int(k) for k in os.environ.get("SAN_KERNELS", "0,1,2,3,4").split(",")]
 for kernel in KERNELS:
     gpa.set_attr_kernel(kernel)
-    for name, records in (("C1", 10_000), ("C2", 2_200_000)):
+    for name, records in (("C1", 10_000), ("C2", 2_200_000), ("C3", 300_000)):
         w = gen.workload(name, records=records)
         s = gpa.load_structure(w.structure, 0)
         rec = torch.empty((records, 2), dtype=torch.int64, device="cuda")
