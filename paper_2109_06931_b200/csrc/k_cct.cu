@@ -86,10 +86,21 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
     fact = fs;
     dact = fs + A.n_func;
   }
-  for (uint32_t f = t; f < A.n_func; f += nt) {
-    uint64_t s = 0;
-    for (int r = 0; r < GPA_VALID_SLOTS; r++) s += A.S_f[(uint64_t)f * GPA_SLOTS + r];
-    fact[f] = s > 0;
+  // a function is active if any valid slot of S_f is non-zero: six independent 16-B loads per
+  // function row (a dependent 12-load loop behind volatile stores serialised on L2 latency)
+  {
+    uint8_t *fw = const_cast<uint8_t *>(fact);
+#pragma unroll 2
+    for (uint32_t f = t; f < A.n_func; f += nt) {
+      const ulonglong2 *row = reinterpret_cast<const ulonglong2 *>(A.S_f + (uint64_t)f * GPA_SLOTS);
+      ulonglong2 v[GPA_VALID_SLOTS / 2];
+#pragma unroll
+      for (int q = 0; q < GPA_VALID_SLOTS / 2; q++) v[q] = __ldg(row + q);
+      unsigned long long o = 0;
+#pragma unroll
+      for (int q = 0; q < GPA_VALID_SLOTS / 2; q++) o |= v[q].x | v[q].y;
+      fw[f] = o != 0;
+    }
   }
   // Step 2: "if a function has samples and none of its incoming call edges has a non-zero
   // weight, we assign each of its incoming call edges a weight of one; we repeat this
@@ -135,11 +146,10 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
   // DAG activity, then the guard (R12): the same rule on external in-edges of DAG nodes
   // (samples mode only, like Step 2)
   __syncthreads();
-  for (uint32_t X = t; X < A.n_dag; X += nt) {
-    uint8_t act = 0;
-    for (uint32_t k = A.dmem_ptr[X]; k < A.dmem_ptr[X + 1]; k++) act |= fact[A.dmem[k]];
-    dact[X] = act;
-  }
+  for (uint32_t X = t; X < A.n_dag; X += nt) dact[X] = 0;
+  __syncthreads();
+  for (uint32_t f = t; f < A.n_func; f += nt)  // a DAG node is active if any member is
+    if (fact[f]) dact[A.scc_of[f]] = 1;
   if (!A.exact) run_worklist(A.n_dag, dact, A.din_ptr, A.din_e, true);
   // W_X = total weight of the external calls into X
   __syncthreads();
