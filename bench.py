@@ -194,7 +194,12 @@ def run_gpa(args):
     n = b - a
     s = gpa.load_structure(w.structure, local)
     ni = s.info["n_inst"]
-    stream = torch.cuda.current_stream(dev)
+    # the attribution and the latency-bound CCT chain run on a high-priority stream: when the
+    # attribution ends, the CCT's single-CTA kernels are scheduled ahead of the side stream's
+    # roll-up CTAs (which only have to finish by the end of the step)
+    lo_pri, hi_pri = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+    stream = torch.cuda.Stream(dev, priority=min(lo_pri, hi_pri)) if not args.no_priority else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(stream)
 
     CH = 1 << 28
 
@@ -417,6 +422,7 @@ def main():
     ap.add_argument("--records", type=int, default=None, help="override the config's record count")
     ap.add_argument("--impl", default="gpa", choices=["gpa", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-priority", action="store_true", help="attribution + CCT on the default-priority stream")
     ap.add_argument("--dist-backend", default="nccl", help="N > 1 process group (gloo: a host-logic check only)")
     ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
     ap.add_argument("--e2e-steps", type=int, default=0)
