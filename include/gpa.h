@@ -189,7 +189,7 @@ GPA_API uint64_t gpa_kernel_launches(void);
  * 0 automatic (default), 1 register streaming, 2 TMA ring with L2 reductions, 3 TMA ring with
  * shared-memory heavy-hitter bins, 4 TMA ring with shared-memory heavy-hitter rows (3 and 4 only
  * where applicable: granule map, >= 2^21 records, >= 1024 instructions; otherwise automatic).
- * Automatic = 3 from max(6e6, 40 x n_inst) records on (granule map), else 1 (2 for binary-search
+ * Automatic = 3 from max(4e6, 8 x n_inst) records on (granule map), else 1 (2 for binary-search
  * structures above 4096 records).  Also settable by the environment
  * variable GPA_ATTR_VARIANT before the first call.  DESIGN.md §7 describes the kernels. */
 GPA_API gpa_status gpa_set_attr_kernel(int which);

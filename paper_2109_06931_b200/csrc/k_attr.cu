@@ -30,6 +30,7 @@
 //  K_attr_stream (small calls, sparse address spaces via binary search): register streaming.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <stdint.h>
 #include <stdlib.h>
@@ -172,6 +173,12 @@ constexpr int kLook = 2;                           // tiles of records + codes i
 #endif
 constexpr int kSampleChunk = 1 << GPA_SAMPLE_CHUNK_LOG, kSampleChunks = (1 << 21) / kSampleChunk;
 constexpr uint64_t kHotMinRecords = (uint64_t)kSampleChunks * kSampleChunk;
+#ifndef GPA_SAMPLE_DIV
+#define GPA_SAMPLE_DIV 256
+#endif
+#ifndef GPA_SAMPLE_MAX_LOG
+#define GPA_SAMPLE_MAX_LOG 21
+#endif
 constexpr int kVBins = 4096;
 
 __global__ void k_sample(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
@@ -391,11 +398,13 @@ constexpr int kHotBins = GPA_HOT_BINS;               // x 4 B = 128 KiB (the res
 using RingBins = Ring<31, 2, 2>;
 constexpr int kLookBins = 1;
 
-__global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ scnt) {
-  const uint64_t total = (uint64_t)kSampleChunks * kSampleChunk;
+// `chunks` runs of kSampleChunk records, evenly spaced over the call's records
+__global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t chunks,
+                              uint32_t *__restrict__ scnt) {
+  const uint64_t total = (uint64_t)chunks * kSampleChunk;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t c = x / kSampleChunk, o = x % kSampleChunk;
-    uint64_t k = c * (n - kSampleChunk) / (kSampleChunks - 1) + o;
+    uint64_t k = c * (n - kSampleChunk) / (chunks - 1) + o;
     uint4 v = ld_stream(rec + k);
     uint32_t i = lookup<0>(T, ((uint64_t)v.y << 32) | v.x);
     uint32_t stall = v.w & 0xFFFFu;
@@ -545,7 +554,12 @@ cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsig
   cudaMemsetAsync(scnt, 0, nbins * 4, st);
   cudaMemsetAsync(V, 0, kVBins * 4, st);
   cudaMemsetAsync(bin_of, 0xFF, kHotBins * 4, st);  // unassigned table entries map to NONE
-  k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, scnt);
+  // sample 2^21 records, or n/8 for smaller calls (at least 2^18): the pre-pass then stays a
+  // small fraction of a mid-size call (C2, 1e7 records)
+  const uint64_t ns = std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
+                                         std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, ns / kSampleChunk);
+  k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, scnt);
   k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)nbins, V);
   k_pick<<<1, 1024, 0, st>>>(V, thr, kHotBins);
   k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of);
@@ -647,11 +661,11 @@ cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, u
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
   const int var = attr_variant();
   const bool hot_ok = T.mode == 0 && n >= kHotMinRecords && T.n_inst >= 1024;
-  // automatic choice: the bins kernel's per-call pre-pass (sample, value histogram, code map:
-  // ~40-90 us, growing with n_inst) pays off from ~6e6 records and 40 records per instruction
-  // on (measured crossovers: C2 ~5e6, C5 ~2e7 records; tools/attr_variants.py); below that the
-  // register-streaming kernel is fastest
-  const bool bins_auto = hot_ok && n >= 6000000ull && n >= 40ull * T.n_inst;
+  // automatic choice: the bins kernel's per-call pre-pass (sample, value histogram, code map;
+  // growing with n_inst) pays off from ~4e6 records and 8 records per instruction on
+  // (measured crossovers: C2 ~2e6, C3 ~4e6, C5 ~5e6 records; tools/attr_variants.py); below
+  // that the register-streaming kernel is fastest
+  const bool bins_auto = hot_ok && n >= 4000000ull && n >= 8ull * T.n_inst;
   if ((var == 0 && bins_auto) || (var == 3 && hot_ok))
     return launch_bins(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
   if (var == 4 && hot_ok) return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
