@@ -373,6 +373,21 @@ def run_gpa(args):
         e2e = {"value": n_all / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * n_all,
                "d2h_bytes_per_step": (res_h.numel() * 8 + fm_h.numel() * 8) if rank == 0 else 0,
                "ms_per_step": ems, "steps": e_k}
+        # the link's pinned H2D ceiling, for context: copy (up to) 4 GiB of this rank's host
+        # records over their identical device copy
+        m = min(n, 1 << 28)
+        if m > 0:
+            src, dst = host[:m], rec[:m]
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            dst.copy_(src, non_blocking=True)
+            h1.record(stream)
+            torch.cuda.synchronize()
+            link = 16 * m / (h0.elapsed_time(h1) / 1e3) / 1e9
+            e2e["h2d_link_gbs"] = link
+            e2e["h2d_link_frac"] = 16 * n / (ems / 1e3) / 1e9 / link
         del host
 
     if rank != 0:
