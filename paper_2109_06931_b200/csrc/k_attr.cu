@@ -449,6 +449,16 @@ __device__ __forceinline__ void repay(unsigned long long *H, const uint32_t *bin
   if (b != NONE) red_add_u64(H + b, v);
 }
 
+__device__ __forceinline__ unsigned long long ldg_keep(const unsigned long long *p, uint64_t pol) {
+  unsigned long long v;
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ void red_add_u64_keep(unsigned long long *p, unsigned long long v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
 template <class RG, int NB, bool REC, int LOOK = kLook>
 __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_bins(uint64_t base, uint64_t n_gran, uint32_t gshift, const unsigned long long *__restrict__ code,
@@ -475,6 +485,8 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   uint4 v[D][R];
   unsigned long long c[D][R];
   const uint64_t G = gridDim.x;
+  uint64_t keep;  // L2 evict-last for the code map (the record stream is evict-first)
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
   auto fetch = [&](uint32_t it, uint4 *vv, unsigned long long *cc) {
     uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
 #pragma unroll
     for (int u = 0; u < R; u++) {
       uint64_t g = ((((uint64_t)vv[u].y << 32) | vv[u].x) - base) >> gshift;
-      cc[u] = g < n_gran ? __ldg(code + g) : 0xFFFFFFFFull;  // unmapped: low word ~0, no hot mask
+      cc[u] = g < n_gran ? ldg_keep(code + g, keep) : 0xFFFFFFFFull;  // unmapped: low word ~0, no hot mask
     }
   };
 #pragma unroll
@@ -518,7 +530,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
           if (hot) {
             old[u] = atoms_add(tab_s + idx[u] * 4, cnt);
           } else {
-            red_add_u64(lo == 0xFFFFFFFFu ? U + slot : H + (lo | slot), cnt);
+            red_add_u64_keep(lo == 0xFFFFFFFFu ? U + slot : H + (lo | slot), cnt, keep);
             idx[u] = NONE;
           }
         } else {
