@@ -417,7 +417,8 @@ def run_gpa(args):
                        "parallelism": f"record shards x{world}, NCCL reduce of H||U",
                        "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_attr_bins",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": gpa.ATTR_KERNEL_NAMES.get(gpa.attr_kernel_choice(s, n), "?"),
                          "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
             "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e, "phases_ms": phases,
             "observations_per_s": observations / (ms / 1e3)}

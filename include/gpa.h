@@ -187,12 +187,19 @@ GPA_API const char *gpa_last_error(void);
 GPA_API uint64_t gpa_kernel_launches(void);
 /* Force the attribution kernel process-wide (testing / benchmarking; results are identical):
  * 0 automatic (default), 1 register streaming, 2 TMA ring with L2 reductions, 3 TMA ring with
- * shared-memory heavy-hitter bins, 4 TMA ring with shared-memory heavy-hitter rows (3 and 4 only
- * where applicable: granule map, >= 2^21 records, >= 1024 instructions; otherwise automatic).
- * Automatic = 3 from max(4e6, 8 x n_inst) records on (granule map), else 1 (2 for binary-search
- * structures above 4096 records).  Also settable by the environment
- * variable GPA_ATTR_VARIANT before the first call.  DESIGN.md §7 describes the kernels. */
+ * shared-memory heavy-hitter bins (u32), 4 ... heavy-hitter rows, 5 / 6 ... bins packed four /
+ * two per 32-bit word (carries repaid exactly), 7 TMA ring with a shared-memory probe table of
+ * granule rows (no per-record gather), 8 byte-packed bins found through a 32-bit code map with
+ * a granule-indexed scratch for the rest (3-8 only where applicable: granule map, >= 2^21
+ * records, >= 1024 instructions; 7 and 8 also need the module inside one aligned 4 GiB window;
+ * otherwise automatic).  Automatic = 7 (structures up to 2^18 granules) or 8 from
+ * max(4e6, 8 x n_inst) records on (granule map), else 1 (2 for binary-search structures above
+ * 4096 records).  Also settable by the environment variable GPA_ATTR_VARIANT before the first
+ * call.  DESIGN.md §7 describes the kernels. */
 GPA_API gpa_status gpa_set_attr_kernel(int which);
+/* The kernel (1..8, numbering above) gpa_attribute_samples runs for a call of n records on s
+ * under the current setting.  Host-only; *which is written on GPA_OK. */
+GPA_API gpa_status gpa_attr_kernel_choice(gpa_structure s, uint64_t n, int *which);
 /* Validate a structure description on the host only (no device touched).  Same checks and
  * status as gpa_load_structure. */
 GPA_API gpa_status gpa_validate_structure(const gpa_structure_desc *desc);

@@ -552,8 +552,14 @@ const char *gpa_last_error(void) { return g_err.c_str(); }
 uint64_t gpa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 gpa_status gpa_set_attr_kernel(int which) {
-  if (which < 0 || which > 4) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-4)", which);
+  if (which < 0 || which > 8) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-8)", which);
   gpa::set_attr_kernel(which);
+  return GPA_OK;
+}
+
+gpa_status gpa_attr_kernel_choice(gpa_structure s, uint64_t n, int *which) {
+  if (!s || !which) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  *which = attr_choice(s->attr, n);
   return GPA_OK;
 }
 

@@ -121,6 +121,7 @@ constexpr size_t kScanScratchWords = 2 * 32768 + 4;
 
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------
 namespace gpa {
+int attr_choice(const AttrTables &T, uint64_t n);  // kernel a call of n records runs (gpa_attr_kernel_choice)
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr,
                              uint32_t *d_rec_inst, int sm_count, cudaStream_t st);

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(RingTma::kThreads, 1)
   const uint64_t ntiles = (n + S - 1) / S;
   uint32_t it = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
     uint64_t left = n - tile * S;
     uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   uint32_t c[D][R];
   const uint64_t G = gridDim.x;
   auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *cc) {
-    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
     const uint4 *src = ring + (size_t)st * S + warp * 32 + lane;
 #pragma unroll
@@ -413,7 +413,7 @@ __global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint6
 }
 
 __global__ void k_assign_bins(const uint32_t *__restrict__ scnt, uint32_t n_inst, uint32_t *__restrict__ thr,
-                              uint32_t *__restrict__ hot_info, uint32_t *__restrict__ bin_of) {
+                              uint32_t *__restrict__ hot_info, uint32_t *__restrict__ bin_of, uint32_t K) {
   const uint32_t t = thr[0];
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += gridDim.x * blockDim.x) {
     uint32_t mask = 0;
@@ -426,7 +426,7 @@ __global__ void k_assign_bins(const uint32_t *__restrict__ scnt, uint32_t n_inst
     if (mask) {
       uint32_t k = __popc(mask);
       uint32_t base = atomicAdd(thr + 1, k);
-      if (base + k <= (uint32_t)kHotBins) {
+      if (base + k <= K) {
         info = base << 12 | mask;
         for (uint32_t m = mask, q = base; m; m &= m - 1, q++) bin_of[q] = i << 4 | (__ffs(m) - 1);
       }
@@ -449,6 +449,12 @@ __device__ __forceinline__ void repay(unsigned long long *H, const uint32_t *bin
   if (b != NONE) red_add_u64(H + b, v);
 }
 
+__device__ __forceinline__ uint32_t ldg_keep_u32(const uint32_t *p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ unsigned long long ldg_keep(const unsigned long long *p, uint64_t pol) {
   unsigned long long v;
   asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
@@ -459,23 +465,71 @@ __device__ __forceinline__ void red_add_u64_keep(unsigned long long *p, unsigned
   asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
-template <class RG, int NB, bool REC, int LOOK = kLook>
+// Bins packed into 32-bit shared words: BITS = 32 (one bin per word), 16 or 8 (two / four bins
+// per word).  Bin idx lives in word idx & (NW-1), part idx / NW (interleaved, so the consecutive
+// bins of one instruction fall in different banks).  A packed add of cnt < 2^BITS into part k can
+// carry across the part boundaries above it; every carry is visible in the atomic's old value:
+// a carry out of part j (< P-1) leaves part j short by 2^BITS and part j+1 one too high, so the
+// adder repays R_j += 2^BITS and R_{j+1} -= 1 in L2 (u64, modular), and a carry out of the word
+// repays R_{P-1} += 2^BITS.  Final H = L2 repayments + the flushed parts: exact for any count.
+template <int BITS>
+struct Pack {
+  static constexpr int P = 32 / BITS;
+  static constexpr uint32_t kBoundary = BITS == 8 ? 0x01010100u : (BITS == 16 ? 0x00010000u : 0u);
+  static constexpr uint32_t kPartMask = BITS == 32 ? 0xFFFFFFFFu : ((1u << BITS) - 1u);
+};
+
+// repayments go to acc[idx] (u64, one per bin, L2-resident): fire-and-forget reductions with no
+// dependent load of the bin's (instruction, slot); k_fold_acc adds acc into H once per call
+template <int BITS, int NW>
+__device__ __forceinline__ void repay_carries(unsigned long long *acc, uint32_t w, uint32_t old, uint32_t delta,
+                                              uint64_t pol) {
+  constexpr int P = Pack<BITS>::P;
+  const unsigned long long s = (unsigned long long)old + delta;
+  const uint32_t cin = old ^ delta ^ (uint32_t)s;  // carry into each bit position
+#pragma unroll
+  for (int j = 0; j < P; j++) {
+    const bool cross = j < P - 1 ? ((cin >> (BITS * (j + 1))) & 1u) : (uint32_t)(s >> 32);
+    if (cross) {
+      red_add_u64_keep(acc + (uint32_t)j * NW + w, 1ull << BITS, pol);
+      if (j < P - 1) red_add_u64_keep(acc + (uint32_t)(j + 1) * NW + w, ~0ull, pol);  // -1 (mod 2^64)
+    }
+  }
+}
+
+// H[bin_of[b]] += acc[b] for every assigned bin
+__global__ void k_fold_acc(const unsigned long long *__restrict__ acc, const uint32_t *__restrict__ bin_of,
+                           const uint32_t *__restrict__ thr, uint32_t K, unsigned long long *__restrict__ H) {
+  const uint32_t nb = min(thr[1], K);
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const unsigned long long v = acc[b];
+    const uint32_t t = bin_of[b];
+    if (v && t != NONE) red_add_u64(H + t, v);  // other streams may add into H concurrently
+  }
+}
+
+template <class RG, int NW, int BITS, bool REC, int LOOK = kLook>
 __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_bins(uint64_t base, uint64_t n_gran, uint32_t gshift, const unsigned long long *__restrict__ code,
                 const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ H,
                 unsigned long long *__restrict__ U, uint32_t *__restrict__ rec_inst,
-                const uint32_t *__restrict__ bin_of, const uint32_t *__restrict__ thr) {
+                unsigned long long *__restrict__ acc, const uint32_t *__restrict__ thr) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = LOOK + 1;
+  constexpr int P = Pack<BITS>::P;
+  static_assert((NW & (NW - 1)) == 0, "NW must be a power of two");
+  static_assert((uint64_t)NW * P <= (1u << 20), "bin index must fit the code map's 20-bit base field");
+  constexpr uint32_t kLogNW = __builtin_ctz(NW);
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
   uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NB * 4);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NW * 4);
   uint64_t *empty = full + NST;
   const uint32_t tab_s = smem_u32(tab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t ntiles = (n + S - 1) / S;
-  const uint32_t nb = min(thr[1], (uint32_t)NB);
-  for (uint32_t x = threadIdx.x; x < nb; x += blockDim.x) tab[x] = 0;
+  const uint32_t nb = min(thr[1], (uint32_t)NW * P);
+  const uint32_t nw = min(nb, (uint32_t)NW);
+  for (uint32_t x = threadIdx.x; x < nw; x += blockDim.x) tab[x] = 0;
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
@@ -488,7 +542,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   uint64_t keep;  // L2 evict-last for the code map (the record stream is evict-first)
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
   auto fetch = [&](uint32_t it, uint4 *vv, unsigned long long *cc) {
-    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
     const uint4 *src = ring + (size_t)st * S + warp * 32 + lane;
 #pragma unroll
@@ -513,7 +567,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
       if (tile + LOOK * G < ntiles) fetch(it + LOOK, v[(q + LOOK) % D], c[(q + LOOK) % D]);
       const uint64_t left = n - tile * S;
       const uint32_t m = (uint32_t)(left < (uint64_t)S ? left : (uint64_t)S);
-      uint32_t old[R], idx[R];
+      uint32_t old[R], idx[R], delta[R];
 #pragma unroll
       for (int u = 0; u < R; u++) {
         const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
@@ -523,12 +577,14 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
         const bool live = j < m;
         if (REC && live) rec_inst[tile * S + j] = lo == 0xFFFFFFFFu ? NONE : lo >> 4;
         const uint32_t mask = hi & 0xFFFu;
-        const bool hot = slot < (uint32_t)kHotSlots && ((mask >> slot) & 1u);
+        const bool hot = slot < (uint32_t)kHotSlots && ((mask >> slot) & 1u) && (BITS == 32 || cnt <= Pack<BITS>::kPartMask);
         idx[u] = (hi >> 12) + __popc(mask & ((1u << slot) - 1u));
         old[u] = 0;
+        delta[u] = 0;
         if (live) {
           if (hot) {
-            old[u] = atoms_add(tab_s + idx[u] * 4, cnt);
+            delta[u] = BITS == 32 ? cnt : cnt << (BITS * (idx[u] >> kLogNW));
+            old[u] = atoms_add(tab_s + (idx[u] & (NW - 1)) * 4, delta[u]);
           } else {
             red_add_u64_keep(lo == 0xFFFFFFFFu ? U + slot : H + (lo | slot), cnt, keep);
             idx[u] = NONE;
@@ -539,52 +595,459 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
       }
 #pragma unroll
       for (int u = 0; u < R; u++) {
-        // old + cnt wrapped the u32 shared counter: repay 2^32 in L2
-        if (idx[u] != NONE && old[u] + v[q][u].z < old[u]) repay(H, bin_of, idx[u], 1ull << 32);
+        // a carry across a part boundary or out of the word: repay in L2
+        const unsigned long long s = (unsigned long long)old[u] + delta[u];
+        const uint32_t crossed = ((old[u] ^ delta[u] ^ (uint32_t)s) & Pack<BITS>::kBoundary) | (uint32_t)(s >> 32);
+        if (idx[u] != NONE && crossed) repay_carries<BITS, NW>(acc, idx[u] & (NW - 1), old[u], delta[u], keep);
       }
     }
   }
 done:
   asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
-  for (uint32_t x = threadIdx.x; x < nb; x += NC * 32) {
-    uint32_t val = tab[x];
-    if (val) repay(H, bin_of, x, val);
+  for (uint32_t x = threadIdx.x; x < nw; x += NC * 32) {
+    const uint32_t word = tab[x];
+#pragma unroll
+    for (int p = 0; p < P; p++) {
+      const uint32_t val = (word >> (BITS * p)) & Pack<BITS>::kPartMask;
+      if (val && (uint32_t)p * NW + x < nb) red_add_u64_keep(acc + (uint32_t)p * NW + x, val, keep);  // coalesced
+    }
   }
 }
 
+template <int BITS>
 cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
                         unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  constexpr int NW = kHotBins;                       // shared 32-bit words (128 KiB)
+  constexpr uint32_t K = (uint32_t)NW * (32 / BITS);  // bins
   // stream-ordered scratch: scnt[n_inst*12] | hot_info[n_inst] | bin_of[K] | V[4096] | thr[4] | code[n_gran] (u64)
+  // | acc[K] (u64)
   const size_t ni = T.n_inst, nbins = ni * kHotSlots;
-  size_t words = nbins + ni + kHotBins + kVBins + 4;
+  size_t words = nbins + ni + K + kVBins + 4;
   words = (words + 1) & ~(size_t)1;  // 8-B align the code map
   uint32_t *w = nullptr;
-  cudaError_t e = pool_alloc((void **)&w, words * 4 + T.n_gran * 8, st);
+  cudaError_t e = pool_alloc((void **)&w, words * 4 + T.n_gran * 8 + (size_t)K * 8, st);
   if (e != cudaSuccess) return e;
-  uint32_t *scnt = w, *hot_info = w + nbins, *bin_of = hot_info + ni, *V = bin_of + kHotBins, *thr = V + kVBins;
+  uint32_t *scnt = w, *hot_info = w + nbins, *bin_of = hot_info + ni, *V = bin_of + K, *thr = V + kVBins;
   unsigned long long *code = reinterpret_cast<unsigned long long *>(w + words);
+  unsigned long long *acc = code + T.n_gran;
+  cudaMemsetAsync(acc, 0, (size_t)K * 8, st);
   cudaMemsetAsync(scnt, 0, nbins * 4, st);
   cudaMemsetAsync(V, 0, kVBins * 4, st);
-  cudaMemsetAsync(bin_of, 0xFF, kHotBins * 4, st);  // unassigned table entries map to NONE
-  // sample 2^21 records, or n/8 for smaller calls (at least 2^18): the pre-pass then stays a
-  // small fraction of a mid-size call (C2, 1e7 records)
+  cudaMemsetAsync(bin_of, 0xFF, (size_t)K * 4, st);  // unassigned table entries map to NONE
+  // sample min(2^21, max(2^18, n/256)) records: the pre-pass then stays a small fraction of a
+  // mid-size call (C2, 1e7 records)
   const uint64_t ns = std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
                                          std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
   const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, ns / kSampleChunk);
   k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, scnt);
   k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)nbins, V);
-  k_pick<<<1, 1024, 0, st>>>(V, thr, kHotBins);
-  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of);
+  k_pick<<<1, 1024, 0, st>>>(V, thr, K);
+  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of, K);
   k_codemap_bins<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, code);
   using RG = RingBins;
-  auto kern = ri ? k_attr_bins<RG, kHotBins, true, kLookBins> : k_attr_bins<RG, kHotBins, false, kLookBins>;
-  const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8;
+  auto kern = ri ? k_attr_bins<RG, NW, BITS, true, kLookBins> : k_attr_bins<RG, NW, BITS, false, kLookBins>;
+  const size_t smem = RG::kBytes + (size_t)NW * 4 + 2 * RG::kStages * 8;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
-    kern<<<sm_count, RG::kThreads, smem, st>>>(T.base, T.n_gran, T.gshift, code, rec, n, H, U, ri, bin_of, thr);
+    kern<<<sm_count, RG::kThreads, smem, st>>>(T.base, T.n_gran, T.gshift, code, rec, n, H, U, ri, acc, thr);
     e = cudaGetLastError();
   }
-  count_launches(6);
+  if (e == cudaSuccess) {
+    k_fold_acc<<<(K + 255) / 256, 256, 0, st>>>(acc, bin_of, thr, K, H);
+    e = cudaGetLastError();
+  }
+  count_launches(7);
+  cudaError_t e2 = cudaFreeAsync(w, st);
+  return e != cudaSuccess ? e : e2;
+}
+
+// ---- K_attr_probe: granule-keyed rows of byte counters, no global load in the record loop ---------
+// Each CTA holds a 2-way set-associative table of kProbeM granules (the key is the granule index
+// itself; set = (g ^ g >> 12) mod 4096, one 64-bit shared load returns both ways) and, per entry,
+// a row of 12 byte-wide counters (one per valid stall slot).  A hit with count < 256 is added to
+// its byte counter with a shared atomic; a carry across a byte boundary or out of the word is
+// visible in the atomic's old value and repaid through acc (as for the packed bins above).  Every
+// other record is reduced into a granule-indexed scratch histogram Hg[g][slot] in L2 (records
+// outside the module into the extra row Hg[n_gran], which folds into U).  So the per-record path
+// reads the record from the TMA ring, probes the table and issues one shared atomic or one L2
+// reduction: no gather, no wait on global memory; the kernel is issue-bound, so the record path
+// is written for a small instruction count.  k_fold_probe / k_fold_gran then add acc and Hg into
+// H (instruction = gmap[g]; gap granules -> U).  The table is chosen per call from a sample:
+// each set keeps its two most-sampled granules.
+constexpr int kProbeSetsLog = 12, kProbeSets = 1 << kProbeSetsLog;  // 4096 sets x 2 ways
+constexpr int kProbeM = 2 * kProbeSets;                               // entries: 32 KiB keys + 96 KiB rows
+constexpr int kProbeRowBytes = GPA_VALID_SLOTS;                       // byte counter of (e, slot) at 12 e + slot
+constexpr int kProbeWords = kProbeM * kProbeRowBytes / 4;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+#ifndef GPA_PROBE_NC
+#define GPA_PROBE_NC 31
+#endif
+#ifndef GPA_PROBE_R
+#define GPA_PROBE_R 3
+#endif
+#ifndef GPA_PROBE_NST
+#define GPA_PROBE_NST 2
+#endif
+using RingProbe = Ring<GPA_PROBE_NC, GPA_PROBE_R, GPA_PROBE_NST>;
+
+__host__ __device__ __forceinline__ uint32_t probe_set(uint32_t g) { return (g ^ (g >> kProbeSetsLog)) & (kProbeSets - 1); }
+
+// sampled records per mapped granule
+__global__ void k_sample_gran(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t chunks,
+                              uint32_t *__restrict__ gcnt) {
+  const uint64_t total = (uint64_t)chunks * kSampleChunk;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = x / kSampleChunk, o = x % kSampleChunk;
+    uint64_t k = c * (n - kSampleChunk) / (chunks - 1) + o;
+    uint4 v = ld_stream(rec + k);
+    uint64_t g = ((((uint64_t)v.y << 32) | v.x) - T.base) >> T.gshift;
+    if (g < T.n_gran && (v.w & 0xFFFFu) < GPA_VALID_SLOTS && __ldg(T.gmap + g) != NONE) atomicAdd(gcnt + g, 1u);
+  }
+}
+
+// way 0 of each set keeps its most-sampled granule, way 1 the next one (ties: the smaller granule);
+// best[] holds (count << 32 | ~g), 0 = empty
+__global__ void k_place(const uint32_t *__restrict__ gcnt, uint64_t n_gran, int way, unsigned long long *__restrict__ best) {
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_gran; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = gcnt[g];
+    if (!c) continue;
+    const uint32_t st = probe_set((uint32_t)g);
+    const unsigned long long v = (unsigned long long)c << 32 | (0xFFFFFFFFu - (uint32_t)g);
+    if (way == 1 && best[2 * st] == v) continue;  // the way-0 winner
+    atomicMax(best + 2 * st + way, v);
+  }
+}
+
+__device__ __forceinline__ uint32_t best_gran(unsigned long long b) { return b ? 0xFFFFFFFFu - (uint32_t)b : kEmpty; }
+
+struct ProbeArgs {
+  uint32_t base_lo, base_hi, span, gshift, n_gran;  // span = n_gran << gshift, one 4 GiB window (probe_ok)
+};
+
+// one record: granule (n_gran when outside the module), 2-way probe, shared byte add or L2 reduction.
+// The module lies in one aligned 4 GiB window (probe_ok), so pc is in the module iff its high word
+// is base_hi and its low word minus base_lo is below span.
+template <bool REC>
+__device__ __forceinline__ void probe_record(const ProbeArgs &A, uint4 v, bool live, uint32_t key_s, uint32_t cnt_s,
+                                             unsigned long long *Hg, unsigned long long *acc, uint64_t keep,
+                                             uint32_t *ri, const uint32_t *gmap) {
+  const uint32_t dlo = v.x - A.base_lo;
+  const uint32_t g = (v.y == A.base_hi && dlo < A.span) ? dlo >> A.gshift : A.n_gran;
+  const uint32_t set = probe_set(g);
+  const uint2 kk = ld_shared_v2(key_s + set * 8);
+  const uint32_t cnt = v.z, st16 = v.w & 0xFFFFu;
+  if (REC && live) *ri = g == A.n_gran ? NONE : __ldg(gmap + g);
+  const bool w1 = kk.y == g;
+  const bool hot = live && (kk.x == g || w1) && st16 < (uint32_t)GPA_VALID_SLOTS && cnt < 256u;
+  const uint32_t baddr = set * (2 * kProbeRowBytes) + (w1 ? (uint32_t)kProbeRowBytes : 0u) + st16;
+  const uint32_t sh = (baddr << 3) & 24u;
+  const uint32_t delta = cnt << sh;
+  if (hot) {
+    const uint32_t old = atoms_add(cnt_s + (baddr & ~3u), delta);
+    // the byte's old value + cnt > 255: a carry left the byte (maybe further): repay through acc
+    if (((old >> sh) & 0xFFu) + cnt > 255u) {
+      const unsigned long long sum = (unsigned long long)old + delta;
+      const uint32_t cin = old ^ delta ^ (uint32_t)sum;
+      unsigned long long *a = acc + (baddr & ~3u);  // acc index = 12 e + slot; this word's first slot
+#pragma unroll
+      for (int jb = 0; jb < 4; jb++) {
+        const bool cross = jb < 3 ? ((cin >> (8 * (jb + 1))) & 1u) : (uint32_t)(sum >> 32);
+        if (cross) {
+          red_add_u64_keep(a + jb, 256ull, keep);
+          if (jb < 3) red_add_u64_keep(a + jb + 1, ~0ull, keep);  // -1 (mod 2^64)
+        }
+      }
+    }
+  } else if (live) {
+    const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
+    red_add_u64(Hg + ((uint64_t)g * GPA_SLOTS + slot), cnt);
+  }
+}
+
+template <class RG, bool REC>
+__global__ void __launch_bounds__(RG::kThreads, 1)
+    k_attr_probe(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint4 *__restrict__ rec, uint64_t n,
+                 unsigned long long *__restrict__ Hg, uint32_t *__restrict__ rec_inst,
+                 const unsigned long long *__restrict__ best, unsigned long long *__restrict__ acc) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  uint2 *keys = reinterpret_cast<uint2 *>(smem + RG::kBytes);  // [set]: (way0 granule, way1 granule)
+  uint32_t *cnt8 = reinterpret_cast<uint32_t *>(keys + kProbeSets);
+  uint64_t *full = reinterpret_cast<uint64_t *>(cnt8 + kProbeWords);
+  uint64_t *empty = full + NST;
+  const uint32_t key_s = smem_u32(keys), cnt_s = smem_u32(cnt8), full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + S - 1) / S;
+  for (uint32_t x = threadIdx.x; x < kProbeSets; x += blockDim.x)
+    keys[x] = make_uint2(best_gran(best[2 * x]), best_gran(best[2 * x + 1]));
+  for (uint32_t x = threadIdx.x; x < kProbeWords; x += blockDim.x) cnt8[x] = 0;
+  ring_init(full, empty, NST, NC);
+  __syncthreads();
+  if (warp == NC) {
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles);
+    return;
+  }
+  uint64_t keep;  // L2 evict-last for Hg / acc (the record stream is evict-first)
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  const uint32_t ring_s = smem_u32(ring) + (warp * 32 + lane) * 16;
+  const uint32_t ntiles_me = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+  const bool has_last = ntiles_me && blockIdx.x + (uint64_t)(ntiles_me - 1) * gridDim.x == ntiles - 1;
+  const uint32_t last_m = (uint32_t)(n - (ntiles - 1) * S);  // records in the stream's last tile
+  const uint32_t full_tiles = has_last && last_m < (uint32_t)S ? ntiles_me - 1 : ntiles_me;
+  uint32_t *ri = nullptr;
+  for (uint32_t it = 0; it < ntiles_me; ++it) {
+    const uint32_t st = it % NST, ph = (it / NST) & 1;
+    mbar_wait_s(full_s + st * 8, ph);
+    uint4 v[R];
+#pragma unroll
+    for (int u = 0; u < R; u++) v[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the tile end: masked
+    __syncwarp();
+    if (lane == 0) ring_release_s(empty_s + st * 8);
+    if (it < full_tiles) {
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        if (REC) ri = rec_inst + (blockIdx.x + (uint64_t)it * gridDim.x) * S + (u * NC + warp) * 32 + lane;
+        probe_record<REC>(A, v[u], true, key_s, cnt_s, Hg, acc, keep, ri, gmap);
+      }
+    } else {  // the stream's partial last tile
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+        if (REC) ri = rec_inst + (blockIdx.x + (uint64_t)it * gridDim.x) * S + j;
+        probe_record<REC>(A, v[u], j < last_m, key_s, cnt_s, Hg, acc, keep, ri, gmap);
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+  for (uint32_t x = threadIdx.x; x < kProbeWords; x += NC * 32) {  // word x: bytes 4x .. 4x+3 = acc[4x ..]
+    const uint32_t word = cnt8[x];
+    if (!word) continue;
+#pragma unroll
+    for (int jb = 0; jb < 4; jb++) {
+      const uint32_t val = (word >> (8 * jb)) & 0xFFu;
+      if (val) red_add_u64_keep(acc + 4 * x + jb, val, keep);
+    }
+  }
+}
+
+// acc (per table entry x slot) -> H via the entry's granule and its instruction
+__global__ void k_fold_probe(const unsigned long long *__restrict__ acc, const unsigned long long *__restrict__ best,
+                             const uint32_t *__restrict__ gmap, unsigned long long *__restrict__ H) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (uint32_t)kProbeM * GPA_VALID_SLOTS) return;
+  const uint32_t e = t / GPA_VALID_SLOTS, s = t - e * GPA_VALID_SLOTS;
+  const unsigned long long v = acc[t];
+  const uint32_t g = best_gran(best[e]);
+  if (!v || g == kEmpty) return;
+  const uint32_t i = gmap[g];  // placed granules are mapped (k_sample_gran)
+  red_add_u64(H + ((uint64_t)i << 4 | s), v);
+}
+
+// Hg (granule x slot) -> H (gap granules and the out-of-module row n_gran -> U); 16 lanes per row
+__global__ void k_fold_gran(const unsigned long long *__restrict__ Hg, uint64_t n_gran, const uint32_t *__restrict__ gmap,
+                            unsigned long long *__restrict__ H, unsigned long long *__restrict__ U) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (n_gran + 1) * 16; t += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = Hg[t];
+    if (!v) continue;
+    const uint64_t g = t >> 4;
+    const uint32_t s = (uint32_t)(t & 15), i = g < n_gran ? __ldg(gmap + g) : NONE;
+    red_add_u64(i == NONE ? U + s : H + ((uint64_t)i << 4 | s), v);
+  }
+}
+
+// module span < 2^32 inside one aligned 4 GiB window (32-bit granule arithmetic)
+bool probe_ok(const AttrTables &T) {
+  const uint64_t span = T.n_gran << T.gshift;
+  return T.mode == 0 && T.n_gran < (1ull << 31) && span < (1ull << 32) && (T.base >> 32) == ((T.base + span - 1) >> 32);
+}
+
+cudaError_t launch_probe(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
+                         unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  // stream-ordered scratch, zeroed by one memset: best[M] (u64) | acc[M*12] (u64) | Hg[n_gran*16] (u64) | gcnt[n_gran] (u32)
+  const size_t nb = (size_t)kProbeM * 8, na = (size_t)kProbeM * GPA_VALID_SLOTS * 8, nh = (size_t)(T.n_gran + 1) * 128,
+               nc = (size_t)T.n_gran * 4;
+  uint8_t *w = nullptr;
+  cudaError_t e = pool_alloc((void **)&w, nb + na + nh + nc, st);
+  if (e != cudaSuccess) return e;
+  unsigned long long *best = (unsigned long long *)w, *acc = (unsigned long long *)(w + nb),
+                     *Hg = (unsigned long long *)(w + nb + na);
+  uint32_t *gcnt = (uint32_t *)(w + nb + na + nh);
+  cudaMemsetAsync(w, 0, nb + na + nh + nc, st);
+  const uint64_t ns = std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
+                                         std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, ns / kSampleChunk);
+  const unsigned gb = (unsigned)std::min<uint64_t>((T.n_gran + 255) / 256, (uint64_t)sm_count * 8);
+  k_sample_gran<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, gcnt);
+  k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 0, best);
+  k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 1, best);
+  using RG = RingProbe;
+  auto kern = ri ? k_attr_probe<RG, true> : k_attr_probe<RG, false>;
+  const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) {
+    ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift, (uint32_t)T.n_gran};
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, Hg, ri, best, acc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    k_fold_probe<<<(kProbeM * GPA_VALID_SLOTS + 255) / 256, 256, 0, st>>>(acc, best, T.gmap, H);
+    const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
+    k_fold_gran<<<(unsigned)b2, 256, 0, st>>>(Hg, T.n_gran, T.gmap, H, U);
+    e = cudaGetLastError();
+  }
+  count_launches(7);
+  cudaError_t e2 = cudaFreeAsync(w, st);
+  return e != cudaSuccess ? e : e2;
+}
+
+// ---- K_attr_code32: packed bins located through a 32-bit per-granule code ------------------------
+// The byte-packed bins of K_attr_bins<8> (131 072 bins in 128 KiB), but the per-call code map holds
+// only the hot information of the granule's instruction (base << 12 | 12-bit hot-slot mask; 0 =
+// no hot slot / unmapped): 4 B per granule, so twice as many codes per L1 line as the 64-bit map.
+// Records that are not hot (cold slots, cold or unmapped granules, counts >= 256) are reduced
+// into the granule-indexed scratch Hg of K_attr_probe (no instruction index needed), folded into
+// H / U after the kernel.
+__global__ void k_codemap32(const uint32_t *__restrict__ gmap, uint64_t n_gran, const uint32_t *__restrict__ hot_info,
+                            uint32_t *__restrict__ code) {
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_gran; g += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t m = gmap[g];
+    code[g] = m == NONE ? 0u : hot_info[m];
+  }
+}
+
+template <class RG, int NW, bool REC, int LOOK = 1>
+__global__ void __launch_bounds__(RG::kThreads, 1)
+    k_attr_code32(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint32_t *__restrict__ code,
+                  const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ Hg,
+                  uint32_t *__restrict__ rec_inst, unsigned long long *__restrict__ acc, const uint32_t *__restrict__ thr) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = LOOK + 1;
+  constexpr uint32_t kLogNW = __builtin_ctz(NW);
+  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NW * 4);
+  uint64_t *empty = full + NST;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  const uint32_t tab_s = smem_u32(tab), full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + S - 1) / S;
+  const uint32_t nb = min(thr[1], (uint32_t)NW * 4);
+  const uint32_t nw = min(nb, (uint32_t)NW);
+  for (uint32_t x = threadIdx.x; x < nw; x += blockDim.x) tab[x] = 0;
+  ring_init(full, empty, NST, NC);
+  __syncthreads();
+  if (warp == NC) {
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles);
+    return;
+  }
+  uint64_t keep;  // L2 evict-last for the code map and the reductions (the record stream is evict-first)
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  const uint32_t ring_s = smem_u32(ring) + (warp * 32 + lane) * 16;
+  const uint32_t ntiles_me = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+  const uint32_t last_m = (uint32_t)(n - (ntiles - 1) * S);
+  uint4 v[D][R];
+  uint32_t g[D][R], c[D][R];
+  auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *gg, uint32_t *cc) {
+    const uint32_t st = it % NST, ph = (it / NST) & 1;
+    mbar_wait_s(full_s + st * 8, ph);
+#pragma unroll
+    for (int u = 0; u < R; u++) vv[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the end: masked
+    __syncwarp();
+    if (lane == 0) ring_release_s(empty_s + st * 8);
+#pragma unroll
+    for (int u = 0; u < R; u++) {
+      const uint32_t dlo = vv[u].x - A.base_lo;
+      gg[u] = (vv[u].y == A.base_hi && dlo < A.span) ? dlo >> A.gshift : A.n_gran;
+      cc[u] = gg[u] < A.n_gran ? ldg_keep_u32(code + gg[u], keep) : 0u;
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < LOOK; q++)
+    if ((uint32_t)q < ntiles_me) fetch(q, v[q], g[q], c[q]);
+  for (uint32_t it0 = 0;; it0 += D) {
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      const uint32_t it = it0 + q;
+      if (it >= ntiles_me) goto done;
+      if (it + LOOK < ntiles_me) fetch(it + LOOK, v[(q + LOOK) % D], g[(q + LOOK) % D], c[(q + LOOK) % D]);
+      const bool last = blockIdx.x + (uint64_t)it * gridDim.x == ntiles - 1;
+#pragma unroll
+      for (int u = 0; u < R; u++) {
+        const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+        const bool live = !last || j < last_m;
+        const uint32_t cnt = v[q][u].z, st16 = v[q][u].w & 0xFFFFu, cd = c[q][u], gq = g[q][u];
+        if (REC && live)
+          rec_inst[(blockIdx.x + (uint64_t)it * gridDim.x) * S + j] = gq == A.n_gran ? NONE : __ldg(gmap + gq);
+        const uint32_t mask = cd & 0xFFFu;
+        const bool hot = live && st16 < (uint32_t)GPA_VALID_SLOTS && ((mask >> st16) & 1u) && cnt < 256u;
+        const uint32_t idx = (cd >> 12) + __popc(mask & ((1u << st16) - 1u));
+        const uint32_t sh = (idx >> kLogNW) << 3;
+        const uint32_t delta = cnt << sh;
+        if (hot) {
+          const uint32_t old = atoms_add(tab_s + (idx & (NW - 1)) * 4, delta);
+          if (((old >> sh) & 0xFFu) + cnt > 255u) repay_carries<8, NW>(acc, idx & (NW - 1), old, delta, keep);
+        } else if (live) {
+          const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
+          red_add_u64(Hg + ((uint64_t)gq * GPA_SLOTS + slot), cnt);
+        }
+      }
+    }
+  }
+done:
+  asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+  for (uint32_t x = threadIdx.x; x < nw; x += NC * 32) {
+    const uint32_t word = tab[x];
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      const uint32_t val = (word >> (8 * p)) & 0xFFu;
+      if (val && (uint32_t)p * NW + x < nb) red_add_u64_keep(acc + (uint32_t)p * NW + x, val, keep);  // coalesced
+    }
+  }
+}
+
+cudaError_t launch_code32(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
+                          unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  constexpr int NW = kHotBins;                 // shared 32-bit words (128 KiB) = 4 NW byte bins
+  constexpr uint32_t K = (uint32_t)NW * 4;
+  // stream-ordered scratch: scnt[n_inst*12] | hot_info[n_inst] | bin_of[K] | V[4096] | thr[4] | code[n_gran] (u32)
+  // | (8-B aligned) acc[K] (u64) | Hg[(n_gran+1)*16] (u64)
+  const size_t ni = T.n_inst, nbins = ni * kHotSlots;
+  size_t words = nbins + ni + K + kVBins + 4 + T.n_gran;
+  words = (words + 1) & ~(size_t)1;
+  const size_t nh = (size_t)(T.n_gran + 1) * 128;
+  uint32_t *w = nullptr;
+  cudaError_t e = pool_alloc((void **)&w, words * 4 + (size_t)K * 8 + nh, st);
+  if (e != cudaSuccess) return e;
+  uint32_t *scnt = w, *hot_info = w + nbins, *bin_of = hot_info + ni, *V = bin_of + K, *thr = V + kVBins, *code = thr + 4;
+  unsigned long long *acc = reinterpret_cast<unsigned long long *>(w + words), *Hg = acc + K;
+  cudaMemsetAsync(acc, 0, (size_t)K * 8 + nh, st);
+  cudaMemsetAsync(scnt, 0, nbins * 4, st);
+  cudaMemsetAsync(V, 0, kVBins * 4, st);
+  cudaMemsetAsync(bin_of, 0xFF, (size_t)K * 4, st);
+  const uint64_t ns = std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
+                                         std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, ns / kSampleChunk);
+  k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, scnt);
+  k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)nbins, V);
+  k_pick<<<1, 1024, 0, st>>>(V, thr, K);
+  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of, K);
+  k_codemap32<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, code);
+  using RG = RingBins;
+  auto kern = ri ? k_attr_code32<RG, NW, true> : k_attr_code32<RG, NW, false>;
+  const size_t smem = RG::kBytes + (size_t)NW * 4 + 2 * RG::kStages * 8;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) {
+    ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift, (uint32_t)T.n_gran};
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, code, rec, n, Hg, ri, acc, thr);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    k_fold_acc<<<(K + 255) / 256, 256, 0, st>>>(acc, bin_of, thr, K, H);
+    const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
+    k_fold_gran<<<(unsigned)b2, 256, 0, st>>>(Hg, T.n_gran, T.gmap, H, U);
+    e = cudaGetLastError();
+  }
+  count_launches(8);
   cudaError_t e2 = cudaFreeAsync(w, st);
   return e != cudaSuccess ? e : e2;
 }
@@ -666,27 +1129,43 @@ cudaError_t launch_stream(const AttrTables &T, const uint4 *rec, uint64_t n, uns
 
 void set_attr_kernel(int which) { g_attr_kernel.store(which, std::memory_order_relaxed); }
 
+// the kernel a call of n records runs (1..8, gpa_set_attr_kernel numbering)
+int attr_choice(const AttrTables &T, uint64_t n) {
+  const int var = attr_variant();
+  const bool hot_ok = T.mode == 0 && n >= kHotMinRecords && T.n_inst >= 1024;
+  // automatic choice: the large-call kernels' per-call pre-pass (sample, table / code map; growing
+  // with the structure) pays off from ~4e6 records and 8 records per instruction on (measured
+  // crossovers: C2 ~2e6, C3 ~4e6, C5 ~5e6 records; tools/attr_variants.py); below that the
+  // register-streaming kernel is fastest.  Among the large-call kernels: the probe table (8192
+  // granules in shared memory, no gather) while the structure is small enough for it to hold most
+  // sampled records (C3, C4: ~0.92), else the byte bins found through the 32-bit code map (C5)
+  //
+  const bool bins_auto = hot_ok && n >= 4000000ull && n >= 8ull * T.n_inst;
+  if (var == 0 && bins_auto) return probe_ok(T) ? (T.n_gran <= (1ull << 18) ? 7 : 8) : 3;
+  if (var >= 3 && var <= 6 && hot_ok) return var;
+  if (var >= 7 && hot_ok && probe_ok(T)) return var;
+  return (var == 1 || n < 4096 || (var == 0 && T.mode == 0)) ? 1 : 2;
+}
+
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr, uint32_t *d_rec_inst,
                              int sm_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
-  const int var = attr_variant();
-  const bool hot_ok = T.mode == 0 && n >= kHotMinRecords && T.n_inst >= 1024;
-  // automatic choice: the bins kernel's per-call pre-pass (sample, value histogram, code map;
-  // growing with n_inst) pays off from ~4e6 records and 8 records per instruction on
-  // (measured crossovers: C2 ~2e6, C3 ~4e6, C5 ~5e6 records; tools/attr_variants.py); below
-  // that the register-streaming kernel is fastest
-  const bool bins_auto = hot_ok && n >= 4000000ull && n >= 8ull * T.n_inst;
-  if ((var == 0 && bins_auto) || (var == 3 && hot_ok))
-    return launch_bins(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
-  if (var == 4 && hot_ok) return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
-  if (var == 1 || n < 4096 || (var == 0 && T.mode == 0)) {
-    return T.mode == 0 ? launch_stream<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
-                       : launch_stream<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+  switch (attr_choice(T, n)) {
+    case 8: return launch_code32(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 7: return launch_probe(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 6: return launch_bins<16>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 5: return launch_bins<8>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 4: return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 3: return launch_bins<32>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 2:
+      return T.mode == 0 ? launch_tma<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
+                         : launch_tma<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    default:
+      return T.mode == 0 ? launch_stream<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
+                         : launch_stream<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
   }
-  return T.mode == 0 ? launch_tma<0>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st)
-                     : launch_tma<1>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
 }
 
 }  // namespace gpa

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   uint4 v[D][R];
   uint32_t c[D][R];
   auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *cc) {
-    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait(full + st, ph);
     const uint4 *src = ring + (size_t)st * S + warp * 32 + lane;
 #pragma unroll

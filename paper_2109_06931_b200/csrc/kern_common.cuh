@@ -28,6 +28,18 @@ __device__ __forceinline__ uint32_t atoms_add(uint32_t saddr, uint32_t v) {
   return old;
 }
 
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t saddr) {
+  uint2 v;
+  asm volatile("ld.shared::cta.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(saddr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
@@ -48,6 +60,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+// same, on a 32-bit shared address
+__device__ __forceinline__ void mbar_wait_s(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(b),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void ring_release_s(uint32_t empty_bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty_bar) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 r;
+  asm volatile("ld.shared::cta.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(saddr) : "memory");
+  return r;
+}
+// predicated shared atomic add (returns old, or `dflt` when !p)
+__device__ __forceinline__ uint32_t atoms_add_if(bool p, uint32_t saddr, uint32_t v, uint32_t dflt) {
+  uint32_t old = dflt;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q atom.shared::cta.add.u32 %0, [%1], %3;\n\t}"
+               : "+r"(old) : "r"(saddr), "r"((uint32_t)p), "r"(v) : "memory");
+  return old;
+}
+// predicated L2 reduction with a cache policy
+__device__ __forceinline__ void red_add_u64_if(bool p, unsigned long long *a, unsigned long long v, uint64_t pol) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q red.global.add.L2::cache_hint.u64 [%1], %2, %3;\n\t}"
+               ::"r"((uint32_t)p), "l"(a), "l"(v), "l"(pol) : "memory");
+}
+
 // consumer side of a ring stage: order this warp's generic-proxy reads of the stage before the
 // producer's next async-proxy (TMA) write into it, then count the warp as done
 __device__ __forceinline__ void ring_release(uint64_t *empty_bar) {
@@ -70,7 +116,6 @@ struct Ring {
   static constexpr int kTile = NC * 32 * R;  // records per stage
   static constexpr size_t kBytes = (size_t)NST * kTile * 16;
   static constexpr int kThreads = (NC + 1) * 32;
-  static_assert((NST & (NST - 1)) == 0, "stages must be a power of two");
 };
 
 // producer warp body: one elected lane drives the bulk-copy engine over this CTA's tiles
@@ -83,7 +128,7 @@ __device__ __forceinline__ void ring_produce(uint4 *ring, uint64_t *full, uint64
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   uint32_t it = 0;
   for (uint64_t tile = t0; tile < t1; tile += step, ++it) {
-    uint32_t st = it & (NST - 1), ph = (it / NST) & 1;
+    uint32_t st = it % NST, ph = (it / NST) & 1;
     if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
     uint64_t left = n - tile * S;
     uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);

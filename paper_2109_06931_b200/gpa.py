@@ -92,6 +92,7 @@ def _load():
         "gpa_attribute_profiles": ([_vp, _vp, _u64, _u32, _vp, _vp, _vp], S),
         "gpa_profile_stats": ([_vp, _vp, _u32, _vp, _vp], S),
         "gpa_set_attr_kernel": ([ctypes.c_int], S),
+        "gpa_attr_kernel_choice": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int)], S),
         "gpa_sparse_build": ([_vp, _vp, _u32, ctypes.c_int, ctypes.POINTER(_vp), _vp], S),
         "gpa_get_sparse_view": ([_vp, ctypes.POINTER(SparseView)], S),
         "gpa_free_sparse": ([_vp], None),
@@ -119,8 +120,20 @@ def kernel_launches() -> int:
 
 def set_attr_kernel(which: int) -> None:
     """0 automatic, 1 register streaming, 2 TMA + L2 reductions, 3 TMA + shared-memory bins,
-    4 TMA + shared-memory rows."""
+    4 TMA + shared-memory rows, 5 / 6 byte / half-word packed bins, 7 shared-memory probe table of
+    granule rows, 8 byte bins through a 32-bit code map (include/gpa.h)."""
     _check(_lib.gpa_set_attr_kernel(int(which)), "gpa_set_attr_kernel")
+
+
+ATTR_KERNEL_NAMES = {1: "k_attr_stream", 2: "k_attr_tma", 3: "k_attr_bins", 4: "k_attr_hot", 5: "k_attr_bins",
+                     6: "k_attr_bins", 7: "k_attr_probe", 8: "k_attr_code32"}
+
+
+def attr_kernel_choice(s, n: int) -> int:
+    """The attribution kernel (1..8) a call of n records on structure s runs."""
+    w = ctypes.c_int(0)
+    _check(_lib.gpa_attr_kernel_choice(s._h, int(n), ctypes.byref(w)), "gpa_attr_kernel_choice")
+    return int(w.value)
 
 
 def version() -> str:

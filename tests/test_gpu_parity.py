@@ -321,7 +321,7 @@ def attr_kernel(gpa):
     gpa.set_attr_kernel(0)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("name,records", [("C3", 4_000_003), ("C5", 3_000_001)])
 def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
     attr_kernel(kernel)
@@ -333,7 +333,7 @@ def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
     assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_attribution_huge_counts_exact(gpa, attr_kernel, kernel):
     """Counts near 2^32 make every shared u32 add wrap: the repaid 2^32 keeps H exact."""
     attr_kernel(kernel)
@@ -385,7 +385,7 @@ def test_profile_stats_huge_values(gpa):
     assert (So[0, 4] == 0).all()
 
 
-@pytest.mark.parametrize("kernel", [3, 4])
+@pytest.mark.parametrize("kernel", [3, 4, 5, 6, 7, 8])
 def test_attribution_shared_counter_overflow_patterns(gpa, attr_kernel, kernel):
     """Hot bins receive counts that drive 16- and 32-bit shared counters through many
     overflows (incl. carries between packed halves, counts of exactly 0xFFFF / 0x10000)."""
