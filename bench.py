@@ -3,12 +3,14 @@
 attributed/sec and % of HBM roofline, vs the CPU oracle).
 
 One step = one pass of the whole hot path over one batch (DESIGN.md §1 rows a-1..a-10):
-zero H||U, attribute this rank's shard of the record stream (K_attr), NCCL-reduce H||U to
-rank 0 (N > 1), then on rank 0 roll up + derive metrics for INST/LINE/LOOP/INLINE/FUNC,
-reconstruct the CCT and derive its EXCL/INCL metrics.  Inputs are generated on the device
+zero H||U, attribute this rank's shard of the record stream (K_attr); at N = 1 roll up +
+derive metrics for INST/LINE/LOOP/INLINE/FUNC, reconstruct the CCT and derive its EXCL/INCL
+metrics; at N > 1 reduce-scatter H||U over NCCL at function-aligned bounds, every rank derives
+the rows of its own functions, and rank 0 reconstructs the CCT from the summed S_f||w.  Inputs are generated on the device
 (untimed) and are 64 GB at C5, far larger than the 126 MB L2, so no L2 flush is needed.
 
-    python bench.py [--gpus N --steps K --warmup W --config C5]        (torchrun for N > 1)
+    python bench.py [--gpus N --steps K --warmup W --config C5]        (N > 1: starts N ranks itself,
+                                                                       or runs under torchrun)
     python bench.py --impl reference ...                              (the CPU oracle arm)
 """
 from __future__ import annotations
@@ -177,7 +179,7 @@ def run_gpa(args):
 
     import gen
     from paper_2109_06931_b200 import gpa
-    from paper_2109_06931_b200.parallel import reduce_histogram, shard_range
+    from paper_2109_06931_b200.parallel import reduce_histogram, reduce_scatter_histogram, shard_range
 
     rank, world, local = _dist_env()
     local = local % max(1, torch.cuda.device_count())  # (a host-logic check may run 2 ranks on 1 GPU)
@@ -217,6 +219,18 @@ def run_gpa(args):
     met = {sc: torch.empty((rows[sc], gpa.NUM_DERIVED), dtype=torch.float64, device=dev) for sc in SCOPES}
     ev_a0, ev_a1 = [], []
 
+    # N > 1: the reduced histogram is scattered at function-aligned
+    # instruction bounds and every rank derives the rows of its own functions; the CCT's Step-1
+    # inputs (S_f, w: 0.7 MB at C5) are summed to rank 0, which reconstructs the tree
+    scatter = world > 1 and args.combine == "scatter"
+    if scatter:
+        bounds = [int(x) for x in gpa.partition_structure(w.structure, world)]
+        lo, hi = bounds[rank], bounds[rank + 1]
+        nf, nc = s.info["n_func"], s.info["n_call"]
+        SW = torch.zeros(nf * 16 + nc, dtype=torch.int64, device=dev)   # S_f || w
+        SF, CW = SW[:nf * 16].view(nf, 16), SW[nf * 16:]
+    ev_a0, ev_a1 = [], []
+
     def step(timed: bool):
         HU.zero_()
         if timed:
@@ -227,10 +241,43 @@ def run_gpa(args):
             e1.record(stream)
             ev_a0.append(e0)
             ev_a1.append(e1)
-        reduce_histogram(HU, dst=0)
+        return combine_analyse(timed)
+
+    def combine_analyse(timed: bool = False):
+        if not scatter:
+            reduce_histogram(HU, dst=0)
+            return analyse(timed) if rank == 0 else 0
+        reduce_scatter_histogram(HU, bounds, ni)
+        ready = torch.cuda.Event(enable_timing=timed)
+        ready.record(stream)
+        if timed:
+            ev_b0.append(ready)
+        side.wait_event(ready)
+        for sc in SCOPES:
+            gpa.derive_metrics_range(s, sc, H, lo, hi, metrics=met[sc], stream=side)
+        if timed:
+            sd = torch.cuda.Event(enable_timing=True)
+            sd.record(side)
+            ev_b1.append(sd)
+        SW.zero_()
+        gpa.cct_inputs(s, H, lo, hi, SF, CW, stream=stream)
+        dist.reduce(SW, dst=0)
+        nctx = 0
         if rank == 0:
-            return analyse(timed)
-        return 0
+            cct = gpa.reconstruct_cct_inputs(s, SF, CW, stream=stream)
+            cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+            gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
+            gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+            if timed:
+                ce = torch.cuda.Event(enable_timing=True)
+                ce.record(stream)
+                ev_c1.append(ce)
+            nctx = cct.n
+        stream.wait_stream(side)
+        stream.synchronize()
+        if rank == 0:
+            cct.free()
+        return nctx
 
     side = torch.cuda.Stream(dev)
 
@@ -269,9 +316,10 @@ def run_gpa(args):
     torch.cuda.synchronize()
     root_less = 0
     if world > 1 and not args.no_balance:
-        # Load balance (untimed): rank 0 also runs the analysis after the reduce, so it takes
-        # D fewer records, D = its analysis time / its attribution time per record (measured
-        # here); the shards are regenerated and re-warmed before the timed region.
+        # Load balance (untimed): rank 0 also runs the CCT (and, with --combine reduce, every
+        # roll-up) after the combine, so it takes D fewer records, D = (its combine + analysis
+        # time - the slowest other rank's) / its attribution time per record (measured here);
+        # the shards are regenerated and re-warmed before the timed region.
         cal = []
         for _ in range(2):
             HU.zero_()
@@ -279,15 +327,15 @@ def run_gpa(args):
             ev[0].record(stream)
             gpa.attribute_samples(s, rec, H, U, n=n, stream=stream)
             ev[1].record(stream)
-            reduce_histogram(HU, dst=0)
             ev[2].record(stream)
-            if rank == 0:
-                analyse(False)
+            combine_analyse(False)
             ev[3].record(stream)
             torch.cuda.synchronize()
             cal.append((ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])))
         t_at, t_an = cal[-1]
-        d = int(t_an / max(t_at, 1e-6) * n) if rank == 0 else 0
+        tt = torch.tensor([t_an if rank else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)          # the other ranks' combine + analysis
+        d = int(max(0.0, t_an - tt.item()) / max(t_at, 1e-6) * n) if rank == 0 else 0
         t = torch.tensor([max(0, d)], dtype=torch.int64, device=dev)
         dist.broadcast(t, 0)
         root_less = int(t.item())
@@ -344,9 +392,8 @@ def run_gpa(args):
         def e2e_step():
             HU.zero_()
             gpa.attribute_samples_host(s, host, H, U, stream=stream)
-            reduce_histogram(HU, dst=0)
+            combine_analyse()
             if rank == 0:
-                analyse()
                 res_h.copy_(HU, non_blocking=True)
                 fm_h.copy_(met["FUNC"], non_blocking=True)
                 stream.synchronize()
@@ -414,7 +461,10 @@ def run_gpa(args):
             "config": {"workload": w.cfg.name, "records": n_all, "records_per_gpu": n, "n_inst": ni,
                        "root_shard_less": root_less,
                        "n_func": s.info["n_func"], "n_call": s.info["n_call"], "cct_contexts": int(nctx),
-                       "parallelism": f"record shards x{world}, NCCL reduce of H||U",
+                       "parallelism": (f"record shards x{world}, " + (
+                           f"{args.dist_backend} reduce-scatter of H||U at function-aligned bounds, rows derived "
+                           f"per rank, S_f||w reduced to rank 0 for the CCT" if scatter else
+                           f"{args.dist_backend} reduce of H||U to rank 0") if world > 1 else "single GPU"),
                        "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -422,11 +472,24 @@ def run_gpa(args):
                          "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
             "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e, "phases_ms": phases,
             "observations_per_s": observations / (ms / 1e3)}
-    if world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:   # rank 0 at every N (the other ranks have finished their GPU work)
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start N ranks of this same command with
+    torch.distributed.run on this node (rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -440,12 +503,26 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-priority", action="store_true", help="attribution + CCT on the default-priority stream")
     ap.add_argument("--dist-backend", default="nccl", help="N > 1 process group (gloo: a host-logic check only)")
+    ap.add_argument("--combine", default="scatter", choices=["scatter", "reduce"],
+                    help="N > 1: reduce-scatter + per-rank roll-ups (default) or reduce to rank 0")
     ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-sample", type=int, default=1 << 28)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args))
+    rank, world, _ = _dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.impl == "gpa" and world > 1 and args.dist_backend == "nccl":
+        import torch
+        if torch.cuda.device_count() < world:
+            print(f"bench.py: {world} NCCL ranks need {world} GPUs, this node has {torch.cuda.device_count()}",
+                  file=sys.stderr)
+            sys.exit(2)
     if args.warmup < 3 and args.impl == "gpa":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

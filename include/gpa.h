@@ -378,6 +378,71 @@ GPA_API gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const ui
                               gpa_cct cct, uint64_t *d_scope_hist, uint64_t *d_scope_mix,
                               double *d_metrics, gpa_stream_t stream);
 
+/* ---- reusable attribution plans -----------------------------------------------------------------
+ * The large-call attribution kernels (gpa_set_attr_kernel 7 / 8) first choose, from a sample of
+ * the call's records, which granules / (instruction, slot) bins are counted in shared memory (a
+ * "plan"; the rest go to L2).  gpa_attribute_samples builds a plan per call.  A plan built once
+ * from representative records (e.g. the first batch of a profile stream: records of one
+ * application are alike) can be reused for any number of later calls, removing the
+ * per-call pre-pass; results are identical for every plan (exact counting), only speed differs.
+ *
+ * gpa_attr_plan_create: samples d_samples[0..n) (DEVICE, 16-byte aligned; n >= 4096 for a plan)
+ *   and synchronizes `stream`.  Structures without a large-call kernel (binary-search lookup,
+ *   module across a 4 GiB boundary) and small samples get an empty plan (variant 0): planned calls
+ *   then behave as gpa_attribute_samples.  The plan holds device memory until gpa_attr_plan_free
+ *   and must not outlive its structure.  Errors as gpa_attribute_samples. */
+typedef struct gpa_attr_plan_s *gpa_attr_plan;
+GPA_API gpa_status gpa_attr_plan_create(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+                                        gpa_attr_plan *out, gpa_stream_t stream);
+/* The kernel a plan runs (7 or 8, 0 = none). */
+GPA_API gpa_status gpa_attr_plan_variant(gpa_attr_plan p, int *which);
+/* gpa_attribute_samples with a prepared plan: same arguments, semantics (accumulates into
+ * d_inst_hist / d_unattributed) and errors; enqueue-only.  Plans are read-only: one plan may serve
+ * concurrent calls on different streams. */
+GPA_API gpa_status gpa_attribute_samples_planned(gpa_structure s, gpa_attr_plan p, const gpa_sample *d_samples,
+                                                 uint64_t n, uint64_t *d_inst_hist, uint64_t *d_unattributed,
+                                                 uint32_t *d_rec_inst, gpa_stream_t stream);
+GPA_API void gpa_attr_plan_free(gpa_attr_plan p);
+
+/* ---- a-4 / a-5 across GPUs: statistics over function-aligned instruction ranges -------------
+ * The paper generates statistics "in parallel" after the profiles are aggregated by a second
+ * reduction (reading R29 in DESIGN.md): every scope row (LINE, LOOP, INLINE, FUNC)
+ * lies inside one function, so when each function's instructions are contiguous, rank r of N can
+ * receive the reduced histogram rows [b_r, b_{r+1}) of a function-aligned split (one
+ * reduce-scatter instead of a reduce to one rank) and derive the rows of its own functions.
+ *
+ * gpa_partition_structure: HOST only (no device touched).  Writes h_inst_bounds[0..n_parts]:
+ *   0 = b_0 <= b_1 <= ... <= b_n_parts = n_inst, each inner bound the first instruction of a
+ *   function (the one nearest to r*n_inst/n_parts; empty parts possible).  Same checks as
+ *   gpa_validate_structure; GPA_ERR_STRUCTURE when some function's instructions are not
+ *   contiguous (then reduce to one rank and use gpa_derive_metrics). */
+GPA_API gpa_status gpa_partition_structure(const gpa_structure_desc *desc, uint32_t n_parts,
+                                           uint32_t *h_inst_bounds);
+/* gpa_derive_metrics restricted to the rows of the functions whose instructions lie in
+ * [inst_lo, inst_hi) (INST scope: rows inst_lo .. inst_hi-1).  Both ends must be 0, n_inst or
+ * the first instruction of a function (GPA_ERR_INVALID_ARG otherwise; GPA_ERR_STRUCTURE when
+ * functions are not contiguous); inst_hi == n_inst also takes functions without instructions.
+ * Reads d_inst_hist rows of the range only; writes only the range's rows of the full-size
+ * outputs (row numbering as gpa_derive_metrics).  No CCT scopes.  Enqueue-only. */
+GPA_API gpa_status gpa_derive_metrics_range(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist,
+                                            uint32_t inst_lo, uint32_t inst_hi, uint64_t *d_scope_hist,
+                                            uint64_t *d_scope_mix, double *d_metrics, gpa_stream_t stream);
+/* CCT Step 1 on a range: S_f (d_func_hist[f*16 + r], u64) for the functions of
+ * [inst_lo, inst_hi) and w_e (d_call_weight[e] = sum_{r<12} H[call_inst[e]][r], R10) for the call
+ * sites whose call instruction lies in it; other entries are left untouched (zero them, then
+ * the element-wise sum over a partition's ranks is the whole input).  Range rules as above;
+ * d_inst_hist / d_func_hist 16-byte aligned.  Enqueue-only. */
+GPA_API gpa_status gpa_cct_inputs(gpa_structure s, const uint64_t *d_inst_hist, uint32_t inst_lo,
+                                  uint32_t inst_hi, uint64_t *d_func_hist, uint64_t *d_call_weight,
+                                  gpa_stream_t stream);
+/* gpa_reconstruct_cct from Step-1 inputs (S_f = d_func_hist [n_func*16], w = d_call_weight
+ * [n_call], DEVICE, read only) instead of the instruction histogram: Steps 2-4
+ * and the result are those of gpa_reconstruct_cct on a histogram with these S_f and w. */
+GPA_API gpa_status gpa_reconstruct_cct_inputs(gpa_structure s, const uint64_t *d_func_hist,
+                                              const uint64_t *d_call_weight, gpa_weight_mode mode,
+                                              uint64_t max_contexts, gpa_cct *out, uint64_t *n_contexts,
+                                              gpa_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -360,22 +360,61 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
         lst[k][fill[k][row_of[x]]++] = i;
       }
   }
+  // function layout (P:711-714 distributed statistics, gpa_derive_metrics_range): first / last
+  // instruction of every function and whether each function is one contiguous run
+  {
+    std::vector<uint32_t> lo(nf, ni), hi(nf, 0), cnt(nf, 0);
+    for (uint32_t i = 0; i < ni; i++) {
+      const uint32_t f = dv.inst_func[i];
+      lo[f] = std::min(lo[f], i);
+      hi[f] = std::max(hi[f], i);
+      cnt[f]++;
+    }
+    bool contig = true;
+    for (uint32_t f = 0; f < nf; f++) contig = contig && (cnt[f] == 0 || hi[f] - lo[f] + 1 == cnt[f]);
+    s->h_func_lo = lo;
+    s->funcs_contiguous = contig;
+    s->h_func_starts.clear();
+    for (uint32_t f = 0; f < nf; f++)
+      if (cnt[f]) s->h_func_starts.push_back(lo[f]);
+    std::sort(s->h_func_starts.begin(), s->h_func_starts.end());
+  }
+  // function of every row of every kind (LINE / LOOP / INLINE: the scope's FUNCTION ancestor)
+  std::vector<std::vector<uint32_t>> row_func(ROLL_KINDS);
+  for (int k = 0; k < ROLL_KINDS; k++) row_func[k].assign(R[k].rows, 0);
+  for (uint32_t x = 0; x < ns; x++) {
+    const int k = set_of(x);
+    if (k == ROLL_FUNC) continue;
+    uint32_t y = x;
+    while (d->scope_parent[y] != NONE) y = d->scope_parent[y];
+    row_func[k][row_of[x]] = dv.func_of_scope[y];
+  }
+  for (uint32_t f = 0; f < nf; f++) row_func[ROLL_FUNC][f] = f;
   for (int k = 0; k < ROLL_KINDS; k++) {
     UP(R[k].d_ptr, ptr[k]);
     UP(R[k].d_inst, lst[k]);
-    // chunks of <= kRollChunk instructions; rows with several chunks get a scratch slot
+    // chunks of <= kRollChunk instructions; rows with several chunks get a scratch slot.  Rows
+    // are visited in their function's instruction order (key = the function's first instruction)
+    std::vector<uint32_t> rord(R[k].rows);
+    std::iota(rord.begin(), rord.end(), 0u);
+    auto key = [&](uint32_t r) { return s->h_func_lo[row_func[k][r]]; };
+    std::stable_sort(rord.begin(), rord.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
     std::vector<uint32_t> chunk, mslot(R[k].rows, NONE), mrows;
-    for (uint32_t r = 0; r < R[k].rows; r++) {
+    R[k].h_chunk_key.clear();
+    R[k].h_multi_key.clear();
+    for (uint32_t r : rord) {
       uint32_t b = ptr[k][r], e = ptr[k][r + 1];
       if (e - b > kRollChunk) {
         mslot[r] = (uint32_t)mrows.size();
         mrows.push_back(r);
+        R[k].h_multi_key.push_back(key(r));
       }
-      if (b == e) { chunk.push_back(r); chunk.push_back(b); chunk.push_back(e); }
+      if (b == e) { chunk.push_back(r); chunk.push_back(b); chunk.push_back(e); R[k].h_chunk_key.push_back(key(r)); }
       for (uint32_t x = b; x < e; x += kRollChunk) {
         chunk.push_back(r);
         chunk.push_back(x);
         chunk.push_back(std::min(e, x + kRollChunk));
+        R[k].h_chunk_key.push_back(key(r));
       }
     }
     R[k].n_chunks = (uint32_t)(chunk.size() / 3);
@@ -661,7 +700,9 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
   cudaEvent_t copied[NBUF] = {}, consumed[NBUF] = {};
   gpa_sample *buf[NBUF] = {};
   gpa_status ret = GPA_OK;
+  void *plan_mem_err = nullptr;  // set below; released by cleanup() on an error path
   auto cleanup = [&]() {
+    if (plan_mem_err) cudaFreeAsync(plan_mem_err, st);
     if (cp) cudaStreamSynchronize(cp);
     for (int b = 0; b < NBUF; b++) {
       if (buf[b]) cudaFreeAsync(buf[b], st);
@@ -690,6 +731,13 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
   }
   HC(cudaEventRecord(consumed[0], st));  // the staging buffers exist (stream-ordered) before any copy
   HC(cudaStreamWaitEvent(cp, consumed[0], 0));
+  // the kernel is chosen for the whole call; a large-call kernel builds its plan once, from the
+  // first chunk, accumulates every chunk and folds into H / U once at the end
+  const int variant = attr_choice(s->attr, n);
+  const bool planned = variant == 7 || variant == 8;
+  AttrPlan plan;
+  AttrAcc acc;
+  void *plan_mem = nullptr;
   for (uint64_t off = 0, j = 0; off < n; off += per, j++) {
     int b = (int)(j % NBUF);
     uint64_t m = std::min(per, n - off);
@@ -697,9 +745,25 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
     HC(cudaMemcpyAsync(buf[b], h_samples + off, m * sizeof(gpa_sample), cudaMemcpyHostToDevice, cp));
     HC(cudaEventRecord(copied[b], cp));
     HC(cudaStreamWaitEvent(st, copied[b], 0));
-    HC(launch_attribute(s->attr, buf[b], m, (unsigned long long *)d_inst_hist,
-                        (unsigned long long *)d_unattributed, nullptr, sm_count(s->device), st));
+    if (planned && j == 0) {
+      HC(pool_alloc(&plan_mem, plan_bytes(s->attr, variant), st));
+      plan_mem_err = plan_mem;
+      HC(plan_build(s->attr, variant, reinterpret_cast<const uint4 *>(buf[b]), m, plan_mem, &plan, sm_count(s->device), st));
+      HC(plan_begin(plan, &acc, st));
+    }
+    if (planned)
+      HC(plan_run(s->attr, plan, acc, reinterpret_cast<const uint4 *>(buf[b]), m, nullptr, sm_count(s->device), st));
+    else
+      HC(launch_attribute(s->attr, buf[b], m, (unsigned long long *)d_inst_hist,
+                          (unsigned long long *)d_unattributed, nullptr, sm_count(s->device), st));
     HC(cudaEventRecord(consumed[b], st));
+  }
+  if (planned) {
+    HC(plan_end(s->attr, plan, &acc, (unsigned long long *)d_inst_hist, (unsigned long long *)d_unattributed,
+                sm_count(s->device), st));
+    plan_mem_err = nullptr;
+    HC(cudaFreeAsync(plan_mem, st));
+    plan_mem = nullptr;
   }
 #undef HC
   cleanup();
@@ -708,12 +772,13 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
   return GPA_OK;
 }
 
-gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa_weight_mode mode,
-                               uint64_t max_contexts, gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream) {
+// Steps 1-4 from the instruction histogram (d_inst_hist) or from precomputed Step-1
+// inputs (d_func_hist = S_f, d_call_weight = w; gpa_reconstruct_cct_inputs)
+static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d_inst_hist, const uint64_t *d_func_hist,
+                              const uint64_t *d_call_weight, gpa_weight_mode mode, uint64_t max_contexts, gpa_cct *out,
+                              uint64_t *n_contexts, gpa_stream_t stream) {
   if (!s || !n_contexts || (max_contexts && !out)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
   if (mode != GPA_WEIGHTS_SAMPLES && mode != GPA_WEIGHTS_EXACT) return fail(GPA_ERR_INVALID_ARG, "mode %d", (int)mode);
-  if (!d_inst_hist && s->info.n_inst) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
-  if ((uintptr_t)d_inst_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist must be 16-byte aligned");
   if (out) *out = nullptr;
   DeviceGuard g(s->device);
   CU(g.err);
@@ -742,10 +807,17 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   CC(calloc_dev(c, &c->dag_active, I.n_dag));
   CC(calloc_dev(c, &c->W, I.n_dag));
   CC(calloc_dev(c, &d_cnt, 4));
-  // Step 1: edge weights and per-function samples S_f (the FUNC roll-up)
-  CC(launch_cct_weights(s, d_inst_hist, c->w, st));
-  CC(launch_rollup(&s->roll[ROLL_FUNC], s->roll[ROLL_FUNC].rows, d_inst_hist, s->d_inst_class, c->S_f, nullptr,
-                   nullptr, sm_count(s->device), st));
+  // Step 1: edge weights and per-function samples S_f (the FUNC roll-up), or the caller's
+  // (copied: Step 2 rewrites w)
+  if (from_hist) {
+    CC(launch_cct_weights(s, d_inst_hist, c->w, st));
+    CC(launch_rollup(&s->roll[ROLL_FUNC], s->roll[ROLL_FUNC].rows, d_inst_hist, s->d_inst_class, c->S_f, nullptr,
+                     nullptr, sm_count(s->device), st));
+  } else {
+    if (I.n_call) CC(cudaMemcpyAsync(c->w, d_call_weight, sizeof(uint64_t) * I.n_call, cudaMemcpyDeviceToDevice, st));
+    if (I.n_func)
+      CC(cudaMemcpyAsync(c->S_f, d_func_hist, sizeof(uint64_t) * SLOTS * I.n_func, cudaMemcpyDeviceToDevice, st));
+  }
   unsigned long long h_cnt[2] = {0, 0};
   if (max_contexts && cct_small_ok(s, I.cct_path_bound)) {
     // Small static bound: build straight into bound-sized arrays with one CTA and read the
@@ -1194,6 +1266,13 @@ gpa_status gpa_block_counts(gpa_structure s, uint32_t n_blocks, const uint32_t *
   return GPA_OK;
 }
 
+gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa_weight_mode mode,
+                               uint64_t max_contexts, gpa_cct *out, uint64_t *n_contexts, gpa_stream_t stream) {
+  if (s && !d_inst_hist && s->info.n_inst) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  if ((uintptr_t)d_inst_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist must be 16-byte aligned");
+  return reconstruct(s, true, d_inst_hist, nullptr, nullptr, mode, max_contexts, out, n_contexts, stream);
+}
+
 gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *v) {
   if (!c || !v) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
   v->n = c->n;
@@ -1238,4 +1317,210 @@ gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *
   return GPA_OK;
 }
 
+
+// ---- reusable attribution plans (gpa_attr_plan_*) -------------------------------------------------
+struct gpa_attr_plan_s {
+  int device = 0;
+  const gpa_structure_s *s = nullptr;
+  AttrPlan p;
+  void *mem = nullptr;
+};
+
+gpa_status gpa_attr_plan_create(gpa_structure s, const gpa_sample *d_samples, uint64_t n, gpa_attr_plan *out,
+                                gpa_stream_t stream) {
+  if (!s || !out || (n && !d_samples)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if ((uintptr_t)d_samples & 15) return fail(GPA_ERR_INVALID_ARG, "d_samples is not 16-byte aligned");
+  *out = nullptr;
+  DeviceGuard g(s->device);
+  CU(g.err);
+  if (n) CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
+  gpa_attr_plan_s *pl = new gpa_attr_plan_s();
+  pl->device = s->device;
+  pl->s = s;
+  // the structure's large-call kernel (gpa_set_attr_kernel numbering); none for small samples or
+  // structures without one (planned calls then run gpa_attribute_samples)
+  const int v = attr_choice(s->attr, ~0ull >> 8);
+  if ((v == 7 || v == 8) && n >= 4096) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMalloc(&pl->mem, plan_bytes(s->attr, v));
+    if (e == cudaSuccess) e = plan_build(s->attr, v, reinterpret_cast<const uint4 *>(d_samples), n, pl->mem, &pl->p,
+                                         sm_count(s->device), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      if (pl->mem) cudaFree(pl->mem);
+      delete pl;
+      cudaGetLastError();
+      return fail(e == cudaErrorMemoryAllocation ? GPA_ERR_OUT_OF_MEMORY : GPA_ERR_CUDA, "gpa_attr_plan_create: %s",
+                  cudaGetErrorString(e));
+    }
+  }
+  *out = pl;
+  return GPA_OK;
+}
+
+gpa_status gpa_attr_plan_variant(gpa_attr_plan p, int *which) {
+  if (!p || !which) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  *which = p->p.variant;
+  return GPA_OK;
+}
+
+gpa_status gpa_attribute_samples_planned(gpa_structure s, gpa_attr_plan p, const gpa_sample *d_samples, uint64_t n,
+                                         uint64_t *d_inst_hist, uint64_t *d_unattributed, uint32_t *d_rec_inst,
+                                         gpa_stream_t stream) {
+  if (!s || !p) return fail(GPA_ERR_INVALID_ARG, "structure or plan is NULL");
+  if (p->s != s) return fail(GPA_ERR_INVALID_ARG, "the plan was made for another structure");
+  if (p->p.variant == 0) return gpa_attribute_samples(s, d_samples, n, d_inst_hist, d_unattributed, d_rec_inst, stream);
+  if (n == 0) return GPA_OK;
+  if (!d_samples || !d_unattributed || (!d_inst_hist && s->info.n_inst))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer with n=%llu", (unsigned long long)n);
+  if ((uintptr_t)d_samples & 15) return fail(GPA_ERR_INVALID_ARG, "d_samples is not 16-byte aligned");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
+  CHECK(check_dev_ptr(d_unattributed, s->device, "d_unattributed"));
+  if (d_inst_hist) CHECK(check_dev_ptr(d_inst_hist, s->device, "d_inst_hist"));
+  if (d_rec_inst) CHECK(check_dev_ptr(d_rec_inst, s->device, "d_rec_inst"));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sm = sm_count(s->device);
+  AttrAcc a;
+  CU(plan_begin(p->p, &a, st));
+  cudaError_t e = plan_run(s->attr, p->p, a, reinterpret_cast<const uint4 *>(d_samples), n, d_rec_inst, sm, st);
+  cudaError_t e2 = plan_end(s->attr, p->p, &a, (unsigned long long *)d_inst_hist,
+                            (unsigned long long *)d_unattributed, sm, st);
+  CU(e);
+  CU(e2);
+  return GPA_OK;
+}
+
+void gpa_attr_plan_free(gpa_attr_plan p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  if (p->mem) cudaFree(p->mem);
+  delete p;
+}
+
+// ---- distributed statistics: function-aligned instruction ranges ------------------
+static gpa_status partition_bounds(uint32_t ni, const std::vector<uint32_t> &starts, bool contig, uint32_t n_parts,
+                                   uint32_t *bounds) {
+  if (!contig) return fail(GPA_ERR_STRUCTURE, "a function's instructions are not contiguous: no function-aligned split");
+  bounds[0] = 0;
+  for (uint32_t r = 1; r < n_parts; r++) {
+    const uint64_t target = (uint64_t)ni * r / n_parts;
+    // the function start nearest to the even split point, never before the previous bound
+    auto it = std::lower_bound(starts.begin(), starts.end(), (uint32_t)target);
+    uint32_t b = it == starts.end() ? ni : *it;
+    if (it != starts.begin() && target - *(it - 1) < (uint64_t)b - target) b = *(it - 1);
+    bounds[r] = std::max(b, bounds[r - 1]);
+  }
+  bounds[n_parts] = ni;
+  return GPA_OK;
+}
+
+gpa_status gpa_partition_structure(const gpa_structure_desc *desc, uint32_t n_parts, uint32_t *h_inst_bounds) {
+  if (!h_inst_bounds || n_parts == 0) return fail(GPA_ERR_INVALID_ARG, "n_parts must be > 0 with a bounds array");
+  Derived dv;
+  CHECK(validate(desc, &dv));
+  const uint32_t ni = desc->n_inst, nf = desc->n_func;
+  std::vector<uint32_t> lo(nf, ni), hi(nf, 0), cnt(nf, 0);
+  for (uint32_t i = 0; i < ni; i++) {
+    const uint32_t f = dv.inst_func[i];
+    lo[f] = std::min(lo[f], i);
+    hi[f] = std::max(hi[f], i);
+    cnt[f]++;
+  }
+  bool contig = true;
+  std::vector<uint32_t> starts;
+  for (uint32_t f = 0; f < nf; f++) {
+    contig = contig && (cnt[f] == 0 || hi[f] - lo[f] + 1 == cnt[f]);
+    if (cnt[f]) starts.push_back(lo[f]);
+  }
+  std::sort(starts.begin(), starts.end());
+  return partition_bounds(ni, starts, contig, n_parts, h_inst_bounds);
+}
+
+// [lo, hi) must be function-aligned: each end 0, n_inst or the first instruction of a function
+static gpa_status check_range(gpa_structure s, uint32_t lo, uint32_t hi) {
+  if (!s->funcs_contiguous) return fail(GPA_ERR_STRUCTURE, "functions are not contiguous: no instruction-range statistics");
+  const uint32_t ni = s->info.n_inst;
+  auto aligned = [&](uint32_t x) {
+    return x == 0 || x == ni || std::binary_search(s->h_func_starts.begin(), s->h_func_starts.end(), x);
+  };
+  if (lo > hi || hi > ni || !aligned(lo) || !aligned(hi))
+    return fail(GPA_ERR_INVALID_ARG, "instruction range [%u, %u) is not function-aligned in [0, %u]", lo, hi, ni);
+  return GPA_OK;
+}
+
+// chunk / multi-row runs of roll-up kind k whose function starts in [lo, hi) (hi == n_inst: to the end,
+// including functions without instructions)
+static void range_runs(const RollSet &R, uint32_t lo, uint32_t hi, uint32_t ni, uint32_t *c0, uint32_t *c1,
+                       uint32_t *m0, uint32_t *m1) {
+  auto lb = [](const std::vector<uint32_t> &v, uint32_t x) {
+    return (uint32_t)(std::lower_bound(v.begin(), v.end(), x) - v.begin());
+  };
+  *c0 = lb(R.h_chunk_key, lo);
+  *c1 = hi >= ni ? (uint32_t)R.h_chunk_key.size() : lb(R.h_chunk_key, hi);
+  *m0 = lb(R.h_multi_key, lo);
+  *m1 = hi >= ni ? (uint32_t)R.h_multi_key.size() : lb(R.h_multi_key, hi);
+}
+
+gpa_status gpa_derive_metrics_range(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist, uint32_t inst_lo,
+                                    uint32_t inst_hi, uint64_t *d_scope_hist, uint64_t *d_scope_mix, double *d_metrics,
+                                    gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  int k = scope == GPA_SCOPE_LINE ? ROLL_LINE : scope == GPA_SCOPE_LOOP ? ROLL_LOOP
+        : scope == GPA_SCOPE_INLINE ? ROLL_INLINE : scope == GPA_SCOPE_FUNC ? ROLL_FUNC
+        : scope == GPA_SCOPE_INST ? -1 : -2;
+  if (k == -2) return fail(GPA_ERR_INVALID_ARG, "scope %d has no instruction-range rows", (int)scope);
+  CHECK(check_range(s, inst_lo, inst_hi));
+  if (!d_scope_hist && !d_scope_mix && !d_metrics) return GPA_OK;
+  if (!d_inst_hist) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  if (((uintptr_t)d_inst_hist | (uintptr_t)d_scope_hist | (uintptr_t)d_scope_mix) & 15)
+    return fail(GPA_ERR_INVALID_ARG, "histogram buffers must be 16-byte aligned");
+  if ((uintptr_t)d_metrics & 7) return fail(GPA_ERR_INVALID_ARG, "d_metrics must be 8-byte aligned");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k < 0) {  // INST rows = the range's instructions
+    if (inst_hi == inst_lo) return GPA_OK;
+    CU(launch_rollup(nullptr, inst_hi - inst_lo, d_inst_hist + (uint64_t)inst_lo * SLOTS, s->d_inst_class + inst_lo,
+                     d_scope_hist ? d_scope_hist + (uint64_t)inst_lo * SLOTS : nullptr,
+                     d_scope_mix ? d_scope_mix + (uint64_t)inst_lo * SLOTS : nullptr,
+                     d_metrics ? d_metrics + (uint64_t)inst_lo * NCOLS : nullptr, sm_count(s->device), st));
+    return GPA_OK;
+  }
+  uint32_t c0, c1, m0, m1;
+  range_runs(s->roll[k], inst_lo, inst_hi, s->info.n_inst, &c0, &c1, &m0, &m1);
+  CU(launch_rollup(&s->roll[k], s->roll[k].rows, d_inst_hist, s->d_inst_class, d_scope_hist, d_scope_mix, d_metrics,
+                   sm_count(s->device), st, c0, c1, m0, m1));
+  return GPA_OK;
+}
+
+gpa_status gpa_cct_inputs(gpa_structure s, const uint64_t *d_inst_hist, uint32_t inst_lo, uint32_t inst_hi,
+                          uint64_t *d_func_hist, uint64_t *d_call_weight, gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  CHECK(check_range(s, inst_lo, inst_hi));
+  if ((!d_inst_hist && s->info.n_inst) || (!d_func_hist && s->info.n_func) || (!d_call_weight && s->info.n_call))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  if (((uintptr_t)d_inst_hist | (uintptr_t)d_func_hist) & 15)
+    return fail(GPA_ERR_INVALID_ARG, "histogram buffers must be 16-byte aligned");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t c0, c1, m0, m1;
+  range_runs(s->roll[ROLL_FUNC], inst_lo, inst_hi, s->info.n_inst, &c0, &c1, &m0, &m1);
+  CU(launch_rollup(&s->roll[ROLL_FUNC], s->roll[ROLL_FUNC].rows, d_inst_hist, s->d_inst_class, d_func_hist, nullptr,
+                   nullptr, sm_count(s->device), st, c0, c1, m0, m1));
+  CU(launch_cct_weights_range(s, d_inst_hist, inst_lo, inst_hi, d_call_weight, st));
+  return GPA_OK;
+}
+
+gpa_status gpa_reconstruct_cct_inputs(gpa_structure s, const uint64_t *d_func_hist, const uint64_t *d_call_weight,
+                                      gpa_weight_mode mode, uint64_t max_contexts, gpa_cct *out, uint64_t *n_contexts,
+                                      gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if ((!d_func_hist && s->info.n_func) || (!d_call_weight && s->info.n_call))
+    return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  if ((uintptr_t)d_func_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_func_hist must be 16-byte aligned");
+  return reconstruct(s, false, nullptr, d_func_hist, d_call_weight, mode, max_contexts, out, n_contexts, stream);
+}
 }  // extern "C"

@@ -43,6 +43,10 @@ struct RollSet {
   uint32_t *d_chunk = nullptr;      // [3*n_chunks] (row, begin, end) into d_inst
   uint32_t *d_multi_slot = nullptr; // [rows] scratch slot of a row with > 1 chunk, else NONE
   uint32_t *d_multi_rows = nullptr; // [n_multi] the rows with > 1 chunk
+  // chunks and multi-chunk rows are ordered by their row's function position (the first
+  // instruction of the function; n_inst for an empty function), so the rows of the functions
+  // inside an instruction range are a contiguous run of each (gpa_derive_metrics_range)
+  std::vector<uint32_t> h_chunk_key, h_multi_key;
 };
 
 }  // namespace gpa
@@ -72,6 +76,10 @@ struct gpa_structure_s {
   uint8_t *d_dag_nontrivial = nullptr;
   uint32_t *d_dlev_ptr = nullptr, *d_dlev_node = nullptr;  // DAG nodes grouped by level
   std::vector<uint32_t> h_scc_of;
+  // function layout in the instruction order: first instruction of each function (n_inst when
+  // empty), whether every function's instructions are contiguous, and the sorted function starts
+  std::vector<uint32_t> h_func_lo, h_func_starts;
+  bool funcs_contiguous = false;
   std::vector<void *> allocs;
 };
 
@@ -122,14 +130,37 @@ constexpr size_t kScanScratchWords = 2 * 32768 + 4;
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------
 namespace gpa {
 int attr_choice(const AttrTables &T, uint64_t n);  // kernel a call of n records runs (gpa_attr_kernel_choice)
+// attribution plans of the large-call kernels 7 (probe table) and 8 (code map + byte bins), k_attr.cu
+struct AttrPlan {
+  int variant = 0;
+  uint64_t n_gran = 0;
+  unsigned long long *best = nullptr;                           // 7: table entries
+  uint32_t *bin_of = nullptr, *thr = nullptr, *code = nullptr;  // 8: bins, bin count, code map
+};
+struct AttrAcc {
+  unsigned long long *acc = nullptr, *Hg = nullptr;
+};
+size_t plan_bytes(const AttrTables &T, int variant);
+cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,
+                       int sm_count, cudaStream_t st);
+cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, cudaStream_t st);
+cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
+                     uint32_t *ri, int sm_count, cudaStream_t st);
+cudaError_t plan_end(const AttrTables &T, const AttrPlan &p, AttrAcc *a, unsigned long long *H, unsigned long long *U,
+                     int sm_count, cudaStream_t st);
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr,
                              uint32_t *d_rec_inst, int sm_count, cudaStream_t st);
 // Row-wise roll-up with the fused derived-metric epilogue.  set == nullptr: identity rows
 // (row r = instruction r, `rows` rows).
+// [c0, c1) / [m0, m1): the chunk and multi-chunk-row runs to process (default: all).
 cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_hist, const uint8_t *d_class,
                           uint64_t *d_out_hist, uint64_t *d_out_mix, double *d_metrics, int sm_count,
-                          cudaStream_t st);
+                          cudaStream_t st, uint32_t c0 = 0, uint32_t c1 = 0xFFFFFFFFu, uint32_t m0 = 0,
+                          uint32_t m1 = 0xFFFFFFFFu);
+// w_e = sum_{r<12} H[call_inst[e]][r] for the call sites whose call instruction lies in [lo, hi)
+cudaError_t launch_cct_weights_range(const gpa_structure_s *s, const uint64_t *d_hist, uint32_t lo, uint32_t hi,
+                                     uint64_t *d_w, cudaStream_t st);
 cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st);
 
 // CCT pieces (k_cct.cu)

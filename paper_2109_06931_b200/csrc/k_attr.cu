@@ -862,45 +862,6 @@ bool probe_ok(const AttrTables &T) {
   return T.mode == 0 && T.n_gran < (1ull << 31) && span < (1ull << 32) && (T.base >> 32) == ((T.base + span - 1) >> 32);
 }
 
-cudaError_t launch_probe(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
-                         unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
-  // stream-ordered scratch, zeroed by one memset: best[M] (u64) | acc[M*12] (u64) | Hg[n_gran*16] (u64) | gcnt[n_gran] (u32)
-  const size_t nb = (size_t)kProbeM * 8, na = (size_t)kProbeM * GPA_VALID_SLOTS * 8, nh = (size_t)(T.n_gran + 1) * 128,
-               nc = (size_t)T.n_gran * 4;
-  uint8_t *w = nullptr;
-  cudaError_t e = pool_alloc((void **)&w, nb + na + nh + nc, st);
-  if (e != cudaSuccess) return e;
-  unsigned long long *best = (unsigned long long *)w, *acc = (unsigned long long *)(w + nb),
-                     *Hg = (unsigned long long *)(w + nb + na);
-  uint32_t *gcnt = (uint32_t *)(w + nb + na + nh);
-  cudaMemsetAsync(w, 0, nb + na + nh + nc, st);
-  const uint64_t ns = std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
-                                         std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
-  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, ns / kSampleChunk);
-  const unsigned gb = (unsigned)std::min<uint64_t>((T.n_gran + 255) / 256, (uint64_t)sm_count * 8);
-  k_sample_gran<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, gcnt);
-  k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 0, best);
-  k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 1, best);
-  using RG = RingProbe;
-  auto kern = ri ? k_attr_probe<RG, true> : k_attr_probe<RG, false>;
-  const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) {
-    ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift, (uint32_t)T.n_gran};
-    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, Hg, ri, best, acc);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) {
-    k_fold_probe<<<(kProbeM * GPA_VALID_SLOTS + 255) / 256, 256, 0, st>>>(acc, best, T.gmap, H);
-    const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
-    k_fold_gran<<<(unsigned)b2, 256, 0, st>>>(Hg, T.n_gran, T.gmap, H, U);
-    e = cudaGetLastError();
-  }
-  count_launches(7);
-  cudaError_t e2 = cudaFreeAsync(w, st);
-  return e != cudaSuccess ? e : e2;
-}
-
 // ---- K_attr_code32: packed bins located through a 32-bit per-granule code ------------------------
 // The byte-packed bins of K_attr_bins<8> (131 072 bins in 128 KiB), but the per-call code map holds
 // only the hot information of the granule's instruction (base << 12 | 12-bit hot-slot mask; 0 =
@@ -1005,52 +966,148 @@ done:
   }
 }
 
-cudaError_t launch_code32(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H,
-                          unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
-  constexpr int NW = kHotBins;                 // shared 32-bit words (128 KiB) = 4 NW byte bins
-  constexpr uint32_t K = (uint32_t)NW * 4;
-  // stream-ordered scratch: scnt[n_inst*12] | hot_info[n_inst] | bin_of[K] | V[4096] | thr[4] | code[n_gran] (u32)
-  // | (8-B aligned) acc[K] (u64) | Hg[(n_gran+1)*16] (u64)
+#ifndef GPA_CODE_NC
+#define GPA_CODE_NC 31
+#endif
+#ifndef GPA_CODE_R
+#define GPA_CODE_R 2
+#endif
+#ifndef GPA_CODE_NST
+#define GPA_CODE_NST 2
+#endif
+#ifndef GPA_CODE_LOOK
+#define GPA_CODE_LOOK 1
+#endif
+using RingCode = Ring<GPA_CODE_NC, GPA_CODE_R, GPA_CODE_NST>;
+
+}  // namespace
+
+// ---- attribution plans: the pre-pass of K_attr_probe / K_attr_code32 (which granules / bins live
+// in shared memory), built from a sample of records and reusable for any number of calls and
+// chunks: the result is exact for every plan, only the speed depends on how well it fits ------------
+constexpr uint32_t kCodeK = (uint32_t)kHotBins * 4;  // K_attr_code32 byte bins
+
+static uint64_t plan_sample(uint64_t n) {
+  return std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
+                            std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
+}
+
+size_t plan_bytes(const AttrTables &T, int variant) {
+  if (variant == 7) return (size_t)kProbeM * 8;                                  // best[M]
+  return ((size_t)kCodeK + 4 + T.n_gran) * 4;                                     // bin_of[K] | thr[4] | code[n_gran]
+}
+
+cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,
+                       int sm_count, cudaStream_t st) {
+  p->variant = variant;
+  p->n_gran = T.n_gran;
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, plan_sample(n) / kSampleChunk);
+  cudaError_t e;
+  if (variant == 7) {
+    p->best = reinterpret_cast<unsigned long long *>(mem);
+    uint32_t *gcnt = nullptr;
+    if ((e = pool_alloc((void **)&gcnt, T.n_gran * 4, st)) != cudaSuccess) return e;
+    cudaMemsetAsync(gcnt, 0, T.n_gran * 4, st);
+    cudaMemsetAsync(p->best, 0, (size_t)kProbeM * 8, st);
+    const unsigned gb = (unsigned)std::min<uint64_t>((T.n_gran + 255) / 256, (uint64_t)sm_count * 8);
+    k_sample_gran<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, gcnt);
+    k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 0, p->best);
+    k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 1, p->best);
+    count_launches(3);
+    e = cudaGetLastError();
+    cudaError_t e2 = cudaFreeAsync(gcnt, st);
+    return e != cudaSuccess ? e : e2;
+  }
+  // variant 8: scnt[n_inst*12] | hot_info[n_inst] | V[4096] transient; bin_of | thr | code kept
+  p->bin_of = reinterpret_cast<uint32_t *>(mem);
+  p->thr = p->bin_of + kCodeK;
+  p->code = p->thr + 4;
   const size_t ni = T.n_inst, nbins = ni * kHotSlots;
-  size_t words = nbins + ni + K + kVBins + 4 + T.n_gran;
-  words = (words + 1) & ~(size_t)1;
-  const size_t nh = (size_t)(T.n_gran + 1) * 128;
   uint32_t *w = nullptr;
-  cudaError_t e = pool_alloc((void **)&w, words * 4 + (size_t)K * 8 + nh, st);
-  if (e != cudaSuccess) return e;
-  uint32_t *scnt = w, *hot_info = w + nbins, *bin_of = hot_info + ni, *V = bin_of + K, *thr = V + kVBins, *code = thr + 4;
-  unsigned long long *acc = reinterpret_cast<unsigned long long *>(w + words), *Hg = acc + K;
-  cudaMemsetAsync(acc, 0, (size_t)K * 8 + nh, st);
+  if ((e = pool_alloc((void **)&w, (nbins + ni + kVBins) * 4, st)) != cudaSuccess) return e;
+  uint32_t *scnt = w, *hot_info = w + nbins, *V = hot_info + ni;
   cudaMemsetAsync(scnt, 0, nbins * 4, st);
   cudaMemsetAsync(V, 0, kVBins * 4, st);
-  cudaMemsetAsync(bin_of, 0xFF, (size_t)K * 4, st);
-  const uint64_t ns = std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
-                                         std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
-  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, ns / kSampleChunk);
+  cudaMemsetAsync(p->bin_of, 0xFF, (size_t)kCodeK * 4, st);
   k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, scnt);
   k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)nbins, V);
-  k_pick<<<1, 1024, 0, st>>>(V, thr, K);
-  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, thr, hot_info, bin_of, K);
-  k_codemap32<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, code);
-  using RG = RingBins;
-  auto kern = ri ? k_attr_code32<RG, NW, true> : k_attr_code32<RG, NW, false>;
-  const size_t smem = RG::kBytes + (size_t)NW * 4 + 2 * RG::kStages * 8;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) {
-    ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift, (uint32_t)T.n_gran};
-    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, code, rec, n, Hg, ri, acc, thr);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) {
-    k_fold_acc<<<(K + 255) / 256, 256, 0, st>>>(acc, bin_of, thr, K, H);
-    const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
-    k_fold_gran<<<(unsigned)b2, 256, 0, st>>>(Hg, T.n_gran, T.gmap, H, U);
-    e = cudaGetLastError();
-  }
-  count_launches(8);
+  k_pick<<<1, 1024, 0, st>>>(V, p->thr, kCodeK);
+  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, p->thr, hot_info, p->bin_of, kCodeK);
+  k_codemap32<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, p->code);
+  count_launches(5);
+  e = cudaGetLastError();
   cudaError_t e2 = cudaFreeAsync(w, st);
   return e != cudaSuccess ? e : e2;
 }
+
+// accumulators of one call (or of all chunks of a host-records call): acc (per shared counter) |
+// Hg (granule x slot, + the out-of-module row), zeroed
+cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, cudaStream_t st) {
+  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  const size_t nh = (size_t)(p.n_gran + 1) * 128;
+  cudaError_t e = pool_alloc((void **)&a->acc, na + nh, st);
+  if (e != cudaSuccess) return e;
+  a->Hg = a->acc + na / 8;
+  return cudaMemsetAsync(a->acc, 0, na + nh, st);
+}
+
+cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
+                     uint32_t *ri, int sm_count, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift,
+                    (uint32_t)T.n_gran};
+  cudaError_t e;
+  if (p.variant == 7) {
+    using RG = RingProbe;
+    auto kern = ri ? k_attr_probe<RG, true> : k_attr_probe<RG, false>;
+    const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, p.best, a.acc);
+  } else {
+    using RG = RingCode;
+    auto kern = ri ? k_attr_code32<RG, kHotBins, true, GPA_CODE_LOOK> : k_attr_code32<RG, kHotBins, false, GPA_CODE_LOOK>;
+    const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, p.code, rec, n, a.Hg, ri, a.acc, p.thr);
+  }
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// fold the accumulators into H / U and release them
+cudaError_t plan_end(const AttrTables &T, const AttrPlan &p, AttrAcc *a, unsigned long long *H, unsigned long long *U,
+                     int sm_count, cudaStream_t st) {
+  if (p.variant == 7) k_fold_probe<<<(kProbeM * GPA_VALID_SLOTS + 255) / 256, 256, 0, st>>>(a->acc, p.best, T.gmap, H);
+  else k_fold_acc<<<(kCodeK + 255) / 256, 256, 0, st>>>(a->acc, p.bin_of, p.thr, kCodeK, H);
+  const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
+  k_fold_gran<<<(unsigned)b2, 256, 0, st>>>(a->Hg, T.n_gran, T.gmap, H, U);
+  count_launches(2);
+  cudaError_t e = cudaGetLastError();
+  cudaError_t e2 = cudaFreeAsync(a->acc, st);
+  a->acc = a->Hg = nullptr;
+  return e != cudaSuccess ? e : e2;
+}
+
+// one call with a transient plan built from the call's own records
+cudaError_t launch_planned(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, unsigned long long *H,
+                           unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
+  void *mem = nullptr;
+  cudaError_t e = pool_alloc(&mem, plan_bytes(T, variant), st);
+  if (e != cudaSuccess) return e;
+  AttrPlan p;
+  AttrAcc a;
+  e = plan_build(T, variant, rec, n, mem, &p, sm_count, st);
+  if (e == cudaSuccess) e = plan_begin(p, &a, st);
+  if (e == cudaSuccess) {
+    e = plan_run(T, p, a, rec, n, ri, sm_count, st);
+    cudaError_t e3 = plan_end(T, p, &a, H, U, sm_count, st);
+    if (e == cudaSuccess) e = e3;
+  }
+  cudaError_t e2 = cudaFreeAsync(mem, st);
+  return e != cudaSuccess ? e : e2;
+}
+
+namespace {
 
 template <class RG, int ROWS>
 cudaError_t run_hot(const AttrTables &T, const uint4 *rec, uint64_t n, unsigned long long *H, unsigned long long *U,
@@ -1153,8 +1210,8 @@ cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, u
   if (n == 0) return cudaSuccess;
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
   switch (attr_choice(T, n)) {
-    case 8: return launch_code32(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
-    case 7: return launch_probe(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 8:
+    case 7: return launch_planned(T, attr_choice(T, n), rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
     case 6: return launch_bins<16>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
     case 5: return launch_bins<8>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
     case 4: return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);

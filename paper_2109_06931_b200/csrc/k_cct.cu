@@ -30,9 +30,11 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr unsigned long long SAT = 1ull << 62;
 
 __global__ void k_weights(const uint32_t *__restrict__ call_inst, uint32_t n_call, const uint64_t *__restrict__ H,
-                          uint64_t *__restrict__ w) {
+                          uint64_t *__restrict__ w, uint32_t lo = 0, uint32_t hi = 0xFFFFFFFFu) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n_call; e += gridDim.x * blockDim.x) {
-    const uint64_t *h = H + ((uint64_t)call_inst[e] << 4);
+    const uint32_t ci = call_inst[e];
+    if (ci < lo || ci >= hi) continue;  // another rank's call site (gpa_cct_inputs)
+    const uint64_t *h = H + ((uint64_t)ci << 4);
     uint64_t s = 0;
 #pragma unroll
     for (int r = 0; r < GPA_VALID_SLOTS; r++) s += h[r];
@@ -849,6 +851,15 @@ cudaError_t launch_cct_prof_incl_level(const gpa_cct_s *c, uint64_t a, uint64_t 
   if (b <= a) return cudaSuccess;
   k_cct_prof_incl_level<<<grid_for((b - a) * GPA_SLOTS * P1, 256), 256, 0, st>>>(c->n, a, b, P1, c->first_child,
                                                                                   c->n_children, d_excl, d_incl);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cct_weights_range(const gpa_structure_s *s, const uint64_t *d_hist, uint32_t lo, uint32_t hi,
+                                     uint64_t *d_w, cudaStream_t st) {
+  uint32_t n = s->info.n_call;
+  if (!n || lo >= hi) return cudaSuccess;
+  k_weights<<<grid_for(n, 256), 256, 0, st>>>(s->d_call_inst, n, d_hist, d_w, lo, hi);
   count_launches(1);
   return cudaGetLastError();
 }

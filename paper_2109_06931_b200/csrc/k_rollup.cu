@@ -182,12 +182,17 @@ __global__ void __launch_bounds__(256) k_derive_f64(const double *__restrict__ V
 
 cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_hist, const uint8_t *d_class,
                           uint64_t *d_out_hist, uint64_t *d_out_mix, double *d_metrics, int sm_count,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint32_t c0, uint32_t c1, uint32_t m0, uint32_t m1) {
   if (rows == 0) return cudaSuccess;
   const bool identity = set == nullptr;
-  const uint32_t items = identity ? rows : set->n_chunks;
-  unsigned long long *scratch = nullptr;
-  const uint32_t n_multi = identity ? 0 : set->n_multi;
+  if (!identity) {
+    c1 = c1 < set->n_chunks ? c1 : set->n_chunks;
+    m1 = m1 < set->n_multi ? m1 : set->n_multi;
+    if (c0 >= c1) return cudaSuccess;
+  }
+  const uint32_t items = identity ? rows : c1 - c0;
+  unsigned long long *scratch = nullptr;  // slots [m0, m1) of the n_multi multi-chunk rows
+  const uint32_t n_multi = identity || m0 >= m1 ? 0 : m1 - m0;
   if (n_multi) {
     cudaError_t e = pool_alloc((void **)&scratch, (size_t)n_multi * 32 * 8, st);
     if (e != cudaSuccess) return e;
@@ -196,14 +201,14 @@ cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_h
   uint64_t want = ((uint64_t)items * 4 + 255) / 256;
   uint64_t cap = (uint64_t)sm_count * 8;
   unsigned blocks = (unsigned)(want < cap ? want : cap);
-  k_rollup<<<blocks, 256, 0, st>>>(identity ? nullptr : set->d_chunk, identity ? nullptr : set->d_inst, items,
-                                   identity ? 1 : 0, identity ? nullptr : set->d_multi_slot, d_hist, d_class,
-                                   d_out_hist, d_out_mix, d_metrics, scratch);
+  k_rollup<<<blocks, 256, 0, st>>>(identity ? nullptr : set->d_chunk + 3ull * c0, identity ? nullptr : set->d_inst,
+                                   items, identity ? 1 : 0, identity ? nullptr : set->d_multi_slot, d_hist, d_class,
+                                   d_out_hist, d_out_mix, d_metrics, scratch ? scratch - (size_t)m0 * 32 : nullptr);
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (n_multi) {
     uint64_t b2 = ((uint64_t)n_multi * 4 + 255) / 256;
-    k_rollup_fin<<<(unsigned)(b2 < cap ? b2 : cap), 256, 0, st>>>(set->d_multi_rows, n_multi, scratch, d_out_hist,
+    k_rollup_fin<<<(unsigned)(b2 < cap ? b2 : cap), 256, 0, st>>>(set->d_multi_rows + m0, n_multi, scratch, d_out_hist,
                                                                    d_out_mix, d_metrics);
     count_launches(1);
     cudaError_t e2 = cudaGetLastError();

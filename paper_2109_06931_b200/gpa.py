@@ -101,6 +101,15 @@ def _load():
         "gpa_cct_profiles": ([_vp, _vp, _vp, _u32, _vp, _vp, _vp], S),
         "gpa_profile_stats_f64": ([_u64, _vp, _u32, _vp, ctypes.c_int, _vp], S),
         "gpa_idleness_blame": ([ctypes.POINTER(TraceDesc), _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp], S),
+        "gpa_partition_structure": ([ctypes.POINTER(StructureDesc), _u32, _vp], S),
+        "gpa_attr_plan_create": ([_vp, _vp, _u64, ctypes.POINTER(_vp), _vp], S),
+        "gpa_attr_plan_variant": ([_vp, ctypes.POINTER(ctypes.c_int)], S),
+        "gpa_attribute_samples_planned": ([_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp], S),
+        "gpa_attr_plan_free": ([_vp], None),
+        "gpa_derive_metrics_range": ([_vp, ctypes.c_int, _vp, _u32, _u32, _vp, _vp, _vp, _vp], S),
+        "gpa_cct_inputs": ([_vp, _vp, _u32, _u32, _vp, _vp, _vp], S),
+        "gpa_reconstruct_cct_inputs": ([_vp, _vp, _vp, ctypes.c_int, _u64, ctypes.POINTER(_vp), ctypes.POINTER(_u64),
+                                        _vp], S),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -179,6 +188,14 @@ def _desc(d: dict):
 def validate_structure(d: dict) -> None:
     desc, keep = _desc(d)
     _check(_lib.gpa_validate_structure(ctypes.byref(desc)), "gpa_validate_structure")
+
+
+def partition_structure(d: dict, n_parts: int) -> np.ndarray:
+    """Host only: function-aligned instruction bounds [n_parts + 1] of an N-way split (gpa.h)."""
+    desc, keep = _desc(d)
+    b = np.zeros(int(n_parts) + 1, np.uint32)
+    _check(_lib.gpa_partition_structure(ctypes.byref(desc), int(n_parts), b.ctypes.data), "gpa_partition_structure")
+    return b
 
 
 class Structure:
@@ -489,6 +506,72 @@ def derive_metrics(s: Structure, scope: str, inst_hist=None, cct: Cct | None = N
                                    cct.handle if cct is not None else None, _ptr(scope_hist, "scope_hist"),
                                    _ptr(scope_mix, "scope_mix"), _ptr(metrics, "metrics"),
                                    _stream_ptr(stream, dev)), "gpa_derive_metrics")
+
+
+class AttrPlan:
+    """A reusable attribution plan (gpa_attr_plan): which granules / bins the large-call kernel
+    counts in shared memory, chosen once from a sample of records."""
+
+    def __init__(self, s: "Structure", samples, n: int | None = None, stream=None):
+        n = samples.numel() * samples.element_size() // 16 if n is None else int(n)
+        h = _vp()
+        _check(_lib.gpa_attr_plan_create(s.handle, _ptr(samples, "samples", 16 * n), n, ctypes.byref(h),
+                                         _stream_ptr(stream, samples.device)), "gpa_attr_plan_create")
+        self._h, self.s = h, s
+        v = ctypes.c_int(0)
+        _check(_lib.gpa_attr_plan_variant(self._h, ctypes.byref(v)), "gpa_attr_plan_variant")
+        self.variant = int(v.value)
+
+    def attribute(self, samples, inst_hist, unattributed, rec_inst=None, n: int | None = None, stream=None) -> None:
+        """gpa_attribute_samples_planned: accumulate records into inst_hist / unattributed."""
+        n = samples.numel() * samples.element_size() // 16 if n is None else int(n)
+        _check(_lib.gpa_attribute_samples_planned(self.s.handle, self._h, _ptr(samples, "samples", 16 * n), n,
+                                                  _ptr(inst_hist, "inst_hist", 128 * self.s.info["n_inst"]),
+                                                  _ptr(unattributed, "unattributed", 128),
+                                                  _ptr(rec_inst, "rec_inst", 4 * n),
+                                                  _stream_ptr(stream, samples.device)), "gpa_attribute_samples_planned")
+
+    def free(self) -> None:
+        if self._h is not None:
+            _lib.gpa_attr_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def derive_metrics_range(s: Structure, scope: str, inst_hist, inst_lo: int, inst_hi: int, scope_hist=None,
+                         scope_mix=None, metrics=None, stream=None) -> None:
+    """derive_metrics for the rows of the functions in [inst_lo, inst_hi) (gpa.h)."""
+    _check(_lib.gpa_derive_metrics_range(s.handle, SCOPES[scope], _ptr(inst_hist, "inst_hist"), int(inst_lo),
+                                         int(inst_hi), _ptr(scope_hist, "scope_hist"), _ptr(scope_mix, "scope_mix"),
+                                         _ptr(metrics, "metrics"), _stream_ptr(stream, inst_hist.device)),
+           "gpa_derive_metrics_range")
+
+
+def cct_inputs(s: Structure, inst_hist, inst_lo: int, inst_hi: int, func_hist, call_weight, stream=None) -> None:
+    """CCT Step 1 inputs (S_f, w) of an instruction range (gpa.h)."""
+    _check(_lib.gpa_cct_inputs(s.handle, _ptr(inst_hist, "inst_hist"), int(inst_lo), int(inst_hi),
+                               _ptr(func_hist, "func_hist", 128 * s.info["n_func"]),
+                               _ptr(call_weight, "call_weight", 8 * s.info["n_call"]),
+                               _stream_ptr(stream, inst_hist.device)), "gpa_cct_inputs")
+
+
+def reconstruct_cct_inputs(s: Structure, func_hist, call_weight, mode: int = WEIGHTS_SAMPLES,
+                           max_contexts: int = (1 << 63) - 1, stream=None):
+    """reconstruct_cct from Step-1 inputs (S_f, w).  Returns a Cct (or the count when max_contexts == 0)."""
+    h = _vp()
+    n = _u64()
+    _check(_lib.gpa_reconstruct_cct_inputs(s.handle, _ptr(func_hist, "func_hist", 128 * s.info["n_func"]),
+                                           _ptr(call_weight, "call_weight", 8 * s.info["n_call"]), mode,
+                                           max_contexts, ctypes.byref(h), ctypes.byref(n),
+                                           _stream_ptr(stream, func_hist.device)), "gpa_reconstruct_cct_inputs")
+    if max_contexts == 0:
+        return n.value
+    return Cct(h, s.device)
 
 
 def scope_row_count(s: Structure, scope: str, cct: Cct | None = None) -> int:

@@ -40,6 +40,24 @@ def reduce_histogram(hist, dst: int = 0, group=None) -> None:
     dist.reduce(hist, dst=dst, op=dist.ReduceOp.SUM, group=group)
 
 
+def reduce_scatter_histogram(hist, bounds, n_inst: int, group=None) -> None:
+    """Reduce-scatter of H_inst || U at function-aligned instruction bounds (gpa_partition_structure):
+    rank r receives the element-wise sum of rows [bounds[r], bounds[r+1]) (the last rank also U),
+    in place; the rest of its buffer keeps its own partial sums.  One reduce per destination (the
+    parts are uneven), so NCCL and gloo run the same code; "aggregated by a second
+    reduction", after which each rank generates the statistics of its part (DESIGN.md §6)."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    world = dist.get_world_size(group)
+    assert len(bounds) == world + 1 and bounds[0] == 0 and bounds[-1] == n_inst
+    for r in range(world):
+        a = int(bounds[r]) * 16
+        b = (int(bounds[r + 1]) * 16) if r < world - 1 else hist.numel()
+        if b > a:
+            dist.reduce(hist[a:b], dst=r, op=dist.ReduceOp.SUM, group=group)
+
+
 def shard_trace(lines: dict, rank: int, world: int) -> dict:
     """f4: ranks of a trace set are independent problems, so worker r of N takes
     the contiguous range of trace ranks whose change points fall in [floor(r*E/N),

@@ -476,3 +476,45 @@ def test_f1_invalid_args(gpa):
     with pytest.raises(gpa.GpaError):
         gpa.profile_stats_f64(torch.zeros((2, 4, 16), dtype=torch.float64, device=DEV), 3,
                               torch.empty((4, 6, 16), dtype=torch.float64, device=DEV))
+
+
+# ---- reusable attribution plans and the host-records path --------------------------------------
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_attr_plan_reuse_exact(gpa, name):
+    """A plan built from one batch serves other batches (and a batch from another part of the
+    stream): results equal the oracle bit for bit, whatever the plan."""
+    w = gen.workload(name, records=6_000_000)
+    s = gpa.load_structure(w.structure, 0)
+    first = _device_records(w, 0, 2_000_000)
+    plan = gpa.AttrPlan(s, first)
+    assert plan.variant in (7, 8)
+    for k0, n in [(2_000_000, 3_999_999), (0, 2_000_000), (5_999_000, 1000)]:
+        rec = _device_records(w, k0, n)
+        H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device=DEV)
+        U = torch.zeros(16, dtype=torch.int64, device=DEV)
+        ri = torch.empty(n, dtype=torch.int32, device=DEV)
+        plan.attribute(rec, H, U, ri)
+        torch.cuda.synchronize()
+        Ho, Uo, rio = oracle.attribute(w.structure, w.records_host(k0, n), rec_inst=True)
+        assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo), (k0, n)
+        assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
+    plan.free()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_path_many_chunks(gpa, pinned):
+    """gpa_attribute_samples_host over more than 3 x 2^22 + 17 records (several passes of the
+    3-buffer staging rotation and a ragged last chunk, one plan for the whole call), pinned and
+    pageable host memory."""
+    n = 3 * (1 << 22) + 17 + 1_000_003
+    w = gen.workload("C4", records=n)
+    s = gpa.load_structure(w.structure, 0)
+    host = torch.empty((n, 2), dtype=torch.int64, pin_memory=pinned)
+    w.records_host(0, n, out=host.numpy().view(gen.RECORD_DTYPE).reshape(-1))
+    H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device=DEV)
+    U = torch.zeros(16, dtype=torch.int64, device=DEV)
+    gpa.attribute_samples_host(s, host, H, U)
+    torch.cuda.synchronize()
+    Ho, Uo, _ = oracle.attribute(w.structure, host.numpy().view(gen.RECORD_DTYPE).reshape(-1),
+                                 threads=len(__import__("os").sched_getaffinity(0)))
+    assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)

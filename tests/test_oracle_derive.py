@@ -77,3 +77,52 @@ def test_derive_random_rows_sum_to_one():
     outf = oracle.derive_f64(V.astype(np.float64))
     assert np.array_equal(outf[:, :17], out[:, :17])
     assert np.isnan(outf[:, 17:]).all()
+
+
+def _mix_fixture():
+    g = load_golden("mix_example.json")
+    cls = np.array(g["structure"]["inst_class"], np.uint8)
+    n = len(cls)
+    st = dict(inst_addr=np.arange(n, dtype=np.uint64) * 16 + 0x1000, inst_len=np.full(n, 16, np.uint16),
+              inst_class=cls, inst_scope=np.ones(n, np.uint32),
+              scope_parent=np.array([0xFFFFFFFF, 0], np.uint32), scope_kind=np.array([0, 3], np.uint8),
+              func_scope=np.array([0], np.uint32), call_inst=np.zeros(0, np.uint32), call_callee=np.zeros(0, np.uint32))
+    H = np.zeros((n, 16), np.uint64)
+    for i, slots in g["structure"]["H"].items():
+        for r, c in slots.items():
+            H[int(i), int(r)] = c
+    return g, st, H
+
+
+@pytest.mark.parametrize("scope", ["FUNC", "LINE"])
+def test_mix_columns_hand_worked(scope):
+    """Every derived column of the one-function row, columns 17..32 included, against the values
+    written out by hand: a class -> column permutation, a dropped class or counting slot 15 in
+    the mix would each fail."""
+    g, st, H = _mix_fixture()
+    e = g["expect"]
+    hist, mix = oracle.scope_hist(st, H, scope)
+    assert hist.shape[0] == 1 and mix.shape[0] == 1
+    for k in range(16):
+        assert mix[0, k] == e["mix_counts"].get(str(k), 0), k
+    out = oracle.derive_u64(hist, mix)[0]
+    assert out[0] == e["S"] and out[16] == e["invalid"]
+    assert out[1] == float(e["W"]) and out[2] == float(e["latency_hiding"]) and out[3] == float(e["latency_stall"])
+    for r in range(12):
+        assert out[4 + r] == float(e["stall_fraction"].get(str(r), "0")), r
+    for c in range(17, 33):
+        assert out[c] == float(e["mix_columns"][str(c)]), c
+
+
+def test_inst_row_mix_hand_worked():
+    """INST rows: each instruction's whole valid-sample total sits in its own class column (1.0),
+    every other mix column is 0, and slot 15 counts only as 'invalid'."""
+    g, st, H = _mix_fixture()
+    hist, mix = oracle.scope_hist(st, H, "INST")
+    out = oracle.derive_u64(hist, mix)
+    for row in g["expect"]["inst_rows"]:
+        i = row["inst"]
+        assert out[i, 0] == row["S"] and mix[i].sum() == row["S"]
+        for c in range(17, 33):
+            assert out[i, c] == (1.0 if c == row["mix_col"] else 0.0), (i, c)
+        assert out[i, 16] == row.get("invalid", 0)

@@ -134,3 +134,108 @@ def test_shard_trace_partitions():
         assert parts[-1]["event1"] == len(tr["time"])
         for a, b in zip(parts, parts[1:]):
             assert a["scope0"] + a["n_scopes"] == b["scope0"] and a["event1"] == b["event0"]
+
+
+# ---- distributed statistics: reduce-scatter at function-aligned bounds (R29) ---------
+def _scatter_worker(rank, world, port, name, records, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2109_06931_b200 import gpa
+        from paper_2109_06931_b200.parallel import reduce_scatter_histogram
+        w = gen.workload(name, records=records)
+        st = w.structure
+        ni = len(st["inst_addr"])
+        bounds = gpa.partition_structure(st, world)
+        a, b = shard_range(w.cfg.records, rank, world)
+        H, U, _ = oracle.attribute(st, w.records_host(a, b - a))
+        HU = torch.from_numpy(np.concatenate([H.reshape(-1), U]).view(np.int64).copy())
+        reduce_scatter_histogram(HU, bounds, ni)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        mine = HU.numpy().view(np.uint64)
+        # this rank's rows only: the rest of its buffer holds partial sums and must not matter
+        Hr = np.zeros((ni, 16), np.uint64)
+        Hr[lo:hi] = mine[:ni * 16].reshape(ni, 16)[lo:hi]
+        res = {"lo": lo, "hi": hi, "H": Hr[lo:hi]}
+        if rank == world - 1:
+            res["U"] = mine[ni * 16:]
+        for sc in ("LINE", "LOOP", "INLINE", "FUNC"):
+            res[sc] = oracle.scope_hist(st, Hr, sc)[0]
+        np.save(out_path.replace(".npy", f"_{rank}.npy"), np.array([res], dtype=object))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,records,world", [("C2", 100_003, 2), ("C4", 60_001, 3), ("C1", 5_000, 4)])
+def test_reduce_scatter_rows_equal_single_process(tmp_path, name, records, world):
+    """Every rank's reduced rows equal the single-process histogram on its function-aligned range,
+    and the scope rows computed from a rank's range alone equal the full roll-up on the rows of the
+    functions inside that range (so the per-rank derivation is exact); empty ranges (C1 at 4 ranks:
+    3 functions) included."""
+    from paper_2109_06931_b200 import gpa
+    out = str(tmp_path / "rs.npy")
+    mp.start_processes(_scatter_worker, args=(world, _free_port(), name, records, out), nprocs=world, join=True,
+                       start_method="spawn")
+    w = gen.workload(name, records=records)
+    st = w.structure
+    H, U, _ = oracle.attribute(st, w.records_host(0, w.cfg.records))
+    bounds = gpa.partition_structure(st, world)
+    for r in range(world):
+        res = np.load(out.replace(".npy", f"_{r}.npy"), allow_pickle=True)[0]
+        lo, hi = res["lo"], res["hi"]
+        assert (lo, hi) == (int(bounds[r]), int(bounds[r + 1]))
+        assert np.array_equal(res["H"], H[lo:hi])
+        if r == world - 1:
+            assert np.array_equal(res["U"], U)
+        for sc in ("LINE", "LOOP", "INLINE", "FUNC"):
+            full = oracle.scope_hist(st, H, sc)[0]
+            rows = _rows_in_range(st, sc, lo, hi)
+            assert np.array_equal(res[sc][rows], full[rows]), (sc, r)
+
+
+def _rows_in_range(st, scope, lo, hi):
+    """Rows of `scope` whose function's first instruction lies in [lo, hi) (the function layout
+    of gpa_derive_metrics_range), computed from the description by walking scope parents."""
+    parent = np.asarray(st["scope_parent"], np.int64)
+    kind = np.asarray(st["scope_kind"])
+    fscope = np.asarray(st["func_scope"], np.int64)
+    func_of_root = {int(x): f for f, x in enumerate(fscope)}
+    inst_scope = np.asarray(st["inst_scope"], np.int64)
+    ns = len(parent)
+    root = np.arange(ns)
+    for _ in range(64):
+        nxt = np.where(parent[root] == 0xFFFFFFFF, root, parent[root])
+        if np.array_equal(nxt, root):
+            break
+        root = nxt
+    func_first = {}
+    for i, x in enumerate(inst_scope):
+        f = func_of_root[int(root[x])]
+        func_first.setdefault(f, i)
+    if scope == "FUNC":
+        return np.array([f for f in range(len(fscope)) if lo <= func_first.get(f, 1 << 40) < hi], np.int64)
+    code = {"LINE": 3, "LOOP": 2, "INLINE": 1}[scope]
+    ids = np.nonzero(kind == code)[0]
+    return np.array([r for r, x in enumerate(ids) if lo <= func_first.get(func_of_root[int(root[x])], 1 << 40) < hi],
+                    np.int64)
+
+
+def test_partition_structure_bounds():
+    """Host-only split: non-decreasing function starts from 0 to n_inst, near the even split."""
+    from paper_2109_06931_b200 import gpa
+    for name in ("C1", "C2", "C3", "C5"):
+        st = gen.workload(name).structure
+        ni = len(st["inst_addr"])
+        for parts in (1, 2, 3, 8):
+            b = gpa.partition_structure(st, parts).astype(np.int64)
+            assert b[0] == 0 and b[-1] == ni and np.all(np.diff(b) >= 0)
+            if name != "C1":
+                assert np.abs(b[1:-1] - ni * np.arange(1, parts) / parts).max(initial=0) < ni / parts
+    # a function split into two runs has no function-aligned partition
+    st = dict(gen.workload("C1").structure)
+    ins = np.asarray(st["inst_scope"]).copy()
+    ins[[0, 150]] = ins[[150, 0]]
+    st["inst_scope"] = ins
+    with pytest.raises(gpa.GpaError) as ei:
+        gpa.partition_structure(st, 2)
+    assert ei.value.status == 2
