@@ -443,13 +443,22 @@ def run_gpa(args):
         return
     peak, peak_src = _peaks()
     achieved = algo_bytes / world / (attr_ms / 1e3) / 1e9   # per GPU: mean bytes / slowest launch
-    traffic = None
+    # DRAM traffic of the timed kernel from the committed ncu capture (tools/capture_traffic.py),
+    # used only while the kernel sources are the ones it was captured from; scaled to this launch
+    traffic, traffic_src = None, "no capture"
     tp = os.path.join(ROOT, "profiles", f"k_attr_traffic_{w.cfg.name}.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from capture_traffic import source_hash
+            cap = json.load(open(tp))
+            if cap.get("source_sha1") == source_hash():
+                traffic = cap["dram_bytes_per_launch"] * (algo_bytes / world) / cap["algorithmic_bytes"]
+                traffic_src = f"ncu capture {cap.get('when')} ({cap['records']} records, {cap['kernel']})"
+            else:
+                traffic_src = "stale capture (kernel sources changed): not used"
+        except Exception as ex:
+            traffic, traffic_src = None, f"capture unreadable: {ex}"
     # phase times on rank 0 and the secondary sum-of-counts rate
     phases = {"attr_ms": attr_ms,
               "scopes_ms_side_stream": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_b1)) / max(1, len(ev_b1)),
@@ -469,7 +478,8 @@ def run_gpa(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": gpa.ATTR_KERNEL_NAMES.get(gpa.attr_kernel_choice(s, n), "?"),
-                         "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src},
+                         "kernel_ms": attr_ms, "algorithmic_bytes": algo_bytes, "peak_source": peak_src,
+                         "traffic_source": traffic_src},
             "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e, "phases_ms": phases,
             "observations_per_s": observations / (ms / 1e3)}
     if not args.no_cpu_baseline:   # rank 0 at every N (the other ranks have finished their GPU work)

@@ -26,9 +26,18 @@ static std::atomic<unsigned long long> g_launches{0};
 
 void gpa::count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[64] = {};
+
+// return reserved pool memory above the release threshold to the driver (after large frees)
+static void pool_trim(int dev) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (dev >= 0 && dev < 64 && g_pools[dev]) cudaMemPoolTrimTo(g_pools[dev], 1ull << 30);
+}
+
 cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
+  std::mutex &mu = g_pool_mu;
+  cudaMemPool_t *pools = g_pools;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -45,7 +54,11 @@ cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
       props.location.id = dev;
       e = cudaMemPoolCreate(&pools[dev], &props);
       if (e != cudaSuccess) return e;
-      uint64_t keep = UINT64_MAX;
+      // keep up to 1 GiB reserved between calls (the per-call scratch of a C5 attribution is
+      // ~0.1 GB, so repeated calls never go back to the driver); memory above that is returned to
+      // the driver at synchronization points, so a large one-off (an exact-mode tree, a sparse
+      // cube) does not stay reserved (gpa_free_cct / gpa_free_sparse also trim)
+      uint64_t keep = 1ull << 30;
       cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
@@ -573,7 +586,9 @@ static void free_cct(gpa_cct_s *c) {
       cudaGetLastError();
       cudaFree(p);
     }
+  const int dev = c->device;
   delete c;
+  pool_trim(dev);  // whatever the stream has already released beyond the pool's threshold
 }
 
 template <class T>
@@ -1178,7 +1193,9 @@ static void free_sparse(gpa_sparse_s *sp) {
       cudaGetLastError();
       cudaFree(p);
     }
+  const int dev = sp->device;
   delete sp;
+  pool_trim(dev);
 }
 
 gpa_status gpa_sparse_build(gpa_structure s, const uint64_t *d_prof_hist, uint32_t n_profiles, gpa_sparse_major major,

@@ -2,32 +2,32 @@
 // stall-reason histogram (§4.2 P:365-374 "an instruction address, a stall reason,
 // and a count"; §4.5 P:475-479 raw metric = sum; §5 P:614-617 disjoint relocated ranges).
 //
-// Four kernels; launch_attribute picks K_attr_bins for large calls (granule map, from
-// max(6e6, 40 x n_inst) records) and K_attr_stream below (DESIGN.md §7 has the measurements).
+// attr_choice() picks the kernel of a call (numbering of gpa_set_attr_kernel):
+// from max(4e6, 8 x n_inst) records on (granule-map structures) a large-call kernel with a
+// per-call plan (sample -> shared-memory hot set), below that register streaming (1).
 //
-// Why privatise: measured on B200 (tools/microbench.cu), u64 reductions into L2 sustain
-// ~1.9e11/s at spread addresses (each RED lane costs ~1.3 SM cycles of LSU issue), far below
-// the ~4.3e11 records/s the HBM roofline allows; shared-memory u32 atomics sustain ~1.3e12/s.
+// Why privatise: measured on B200 (tools/microbench.cu), u64 reductions into L2 cost ~1.3 SM
+// cycles of LSU issue per lane (~1.9e11/s at spread addresses), far below the ~4.1e11 records/s
+// the HBM roofline allows; shared-memory u32 atomics sustain ~1.3e12/s.  Every large-call kernel
+// streams record tiles HBM -> shared memory with 1-D TMA bulk copies (cp.async.bulk, L2
+// evict-first) into an mbarrier ring driven by one producer lane; consumer warps read their
+// records from shared memory, free the stage (proxy fence + arrive) and count hot records with
+// shared atomics, the rest with L2 reductions.  Results are identical for every kernel.
 //
-//  K_attr_bins (default for large calls): the ~32 k most-sampled (instruction, slot) BINS live
-//     in shared memory, per CTA.  Per call:
-//       1. k_sample_bins  bin hits of 2^21 sampled records (16 384 evenly spaced runs of 128)
-//       2. k_vhist/k_pick/k_assign_bins   choose the hottest bins; each instruction gets a
-//                         12-bit hot-slot mask and a base index into the shared table
-//       3. k_codemap_bins per-call 64-bit code per granule (instruction, hot mask, base): one
-//                         gather resolves a record
-//       4. k_attr_bins    persistent CTA per SM (1024 threads).  One producer lane streams
-//                         record tiles HBM -> shared memory with 1-D bulk copies (cp.async.bulk
-//                         = TMA engine, L2 evict-first) into a 2-stage mbarrier ring; 31 consumer
-//                         warps copy their 2 records per lane to registers, free the stage (proxy
-//                         fence + arrive), gather the codes of the next tile, and accumulate: hot
-//                         records -> u32 shared atomics (a u32 wrap, old + cnt < old, is repaid as
-//                         +2^32 in L2, so any count is exact), others -> u64 L2 reductions.  Each
-//                         CTA flushes its bins once.  The hot set only moves where a count lands.
-//  K_attr_hot: the same with whole 12-slot rows of the hottest instructions (k_sample, k_assign,
-//     k_codemap; 16 consumer warps, 4 stages).
-//  K_attr_tma: the TMA ring with warp-aggregated L2 reductions only.
-//  K_attr_stream (small calls, sparse address spaces via binary search): register streaming.
+//  7 K_attr_probe (structures up to 2^18 granules, C3/C4): a 2-way set-associative table of 8192
+//     granules in shared memory (key = the granule) with a row of 12 byte counters each: the record
+//     path has no global load at all (probe, shared atomic or L2 reduction into a granule-indexed
+//     scratch); k_sample_gran / k_place choose the table per plan.
+//  8 K_attr_code32 (larger structures, C5): 131 072 byte-packed (instruction, slot) bins found
+//     through a 32-bit per-granule code (base << 12 | hot-slot mask); non-hot records go to the
+//     granule-indexed scratch.  k_sample_bins / k_vhist / k_pick / k_assign_bins / k_codemap32
+//     choose the bins per plan.
+//  Byte / half-word counters: a carry out of a packed counter is visible in the atomic's old value
+//  and repaid exactly in L2 (acc), so any count is exact.  Plans are reusable (gpa_attr_plan_*).
+//  3 / 5 / 6 K_attr_bins<32 / 8 / 16>: the round-1 kernel (64-bit code map: instruction + hot
+//     info) with u32 / u8 / u16 bins.  4 K_attr_hot: hot 12-slot rows.  2 K_attr_tma: TMA ring,
+//     warp-aggregated L2 reductions only.  1 K_attr_stream: register streaming (small calls and
+//     binary-search structures).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,23 +43,6 @@ namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
-// pc -> instruction: granule map (MODE 0) or binary search over the sorted starts (MODE 1)
-template <int MODE>
-__device__ __forceinline__ uint32_t lookup(const AttrTables &T, uint64_t pc) {
-  if (MODE == 0) {
-    uint64_t g = (pc - T.base) >> T.gshift;  // pc < base wraps to a huge g
-    return g < T.n_gran ? __ldg(T.gmap + g) : NONE;
-  } else {
-    if (!(pc >= T.base && pc < T.end)) return NONE;
-    uint32_t lo = 0, hi = T.n_inst;
-    while (lo < hi) {
-      uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(T.inst_addr + mid) <= pc) lo = mid + 1; else hi = mid;
-    }
-    uint32_t j = lo - 1;  // lo >= 1 because pc >= base = inst_addr[0]
-    return pc - __ldg(T.inst_addr + j) < (uint64_t)__ldg(T.inst_len + j) ? j : NONE;
-  }
-}
 
 // Warp-aggregated accumulate: lanes with equal `key` sum their counts; the lowest lane of
 // each group issues one u64 reduction.  key == FULL marks an idle lane.
@@ -391,6 +374,9 @@ done:
 #define GPA_HOT_BINS 32768
 #endif
 constexpr int kHotBins = GPA_HOT_BINS;               // x 4 B = 128 KiB (the rest of the SM's 256 KiB is L1 for the code-map gathers)
+static_assert((kHotBins & (kHotBins - 1)) == 0, "GPA_HOT_BINS: shared words must be a power of two");
+static_assert((uint64_t)kHotBins * 4 <= (1u << 20), "GPA_HOT_BINS: byte-bin index must fit the 20-bit code base field");
+static_assert((size_t)kHotBins * 4 + 2 * 31 * 64 * 16 + 64 <= 227 * 1024, "GPA_HOT_BINS: table + ring exceed shared memory");
 // 31 consumer warps x 2 records per lane (tile = 1984 records, 2 x 31 KiB stages) + the producer
 // = 1024 threads, 1 tile of lookahead: C5 15.6 -> 14.9 ms, C4 3.71 -> 3.21 ms against 16 x 2 x 4
 // stages with lookahead 2 (DESIGN.md §7 geometry sweep; fewer stage releases per record, each of

@@ -21,22 +21,6 @@ namespace {
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int kThreads = 256, kUnroll = 4;
 
-template <int MODE>
-__device__ __forceinline__ uint32_t lookup(const AttrTables &T, uint64_t pc) {
-  if (MODE == 0) {
-    uint64_t g = (pc - T.base) >> T.gshift;
-    return g < T.n_gran ? __ldg(T.gmap + g) : NONE;
-  } else {
-    if (!(pc >= T.base && pc < T.end)) return NONE;
-    uint32_t lo = 0, hi = T.n_inst;
-    while (lo < hi) {
-      uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(T.inst_addr + mid) <= pc) lo = mid + 1; else hi = mid;
-    }
-    uint32_t j = lo - 1;
-    return pc - __ldg(T.inst_addr + j) < (uint64_t)__ldg(T.inst_len + j) ? j : NONE;
-  }
-}
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads)

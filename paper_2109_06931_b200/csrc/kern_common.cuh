@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "gpa_internal.cuh"
+
 namespace gpa {
 namespace {
 
@@ -107,6 +109,25 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+
+// pc -> instruction (a-2, R6): granule map (MODE 0) or binary search over the sorted
+// instruction starts (MODE 1); NONE outside every [addr, addr + len)
+template <int MODE>
+__device__ __forceinline__ uint32_t lookup(const AttrTables &T, uint64_t pc) {
+  if (MODE == 0) {
+    uint64_t g = (pc - T.base) >> T.gshift;  // pc < base wraps to a huge g
+    return g < T.n_gran ? __ldg(T.gmap + g) : NONE;
+  } else {
+    if (!(pc >= T.base && pc < T.end)) return NONE;
+    uint32_t lo = 0, hi = T.n_inst;
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(T.inst_addr + mid) <= pc) lo = mid + 1; else hi = mid;
+    }
+    uint32_t j = lo - 1;  // lo >= 1 because pc >= base = inst_addr[0]
+    return pc - __ldg(T.inst_addr + j) < (uint64_t)__ldg(T.inst_len + j) ? j : NONE;
+  }
 }
 
 // ---- TMA ring geometry ----------------------------------------------------------------------------
