@@ -197,6 +197,11 @@ GPA_API uint64_t gpa_kernel_launches(void);
  * 4096 records).  Also settable by the environment variable GPA_ATTR_VARIANT before the first
  * call.  DESIGN.md §7 describes the kernels. */
 GPA_API gpa_status gpa_set_attr_kernel(int which);
+/* Testing only: level L in 1..64 makes the TMA-ring kernels (7, 8) sleep pseudo-random times up to
+ * L/2 us before each stage's bulk copy (producer) and before reading each stage (consumers), so
+ * producer-ahead and consumer-ahead orders of the ring protocol are exercised; results must not
+ * change.  0 (default) = off.  Process-wide. */
+GPA_API gpa_status gpa_set_ring_stress(int level);
 /* The kernel (1..8, numbering above) gpa_attribute_samples runs for a call of n records on s
  * under the current setting.  Host-only; *which is written on GPA_OK. */
 GPA_API gpa_status gpa_attr_kernel_choice(gpa_structure s, uint64_t n, int *which);

@@ -611,6 +611,12 @@ gpa_status gpa_set_attr_kernel(int which) {
   return GPA_OK;
 }
 
+gpa_status gpa_set_ring_stress(int level) {
+  if (level < 0 || level > 64) return fail(GPA_ERR_INVALID_ARG, "ring stress level %d (0 off, 1-64)", level);
+  gpa::set_ring_stress(level);
+  return GPA_OK;
+}
+
 gpa_status gpa_attr_kernel_choice(gpa_structure s, uint64_t n, int *which) {
   if (!s || !which) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
   *which = attr_choice(s->attr, n);

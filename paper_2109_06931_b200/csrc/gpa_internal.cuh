@@ -118,6 +118,7 @@ struct gpa_cct_s {
 namespace gpa {
 void count_launches(uint64_t k);
 void set_attr_kernel(int which);
+void set_ring_stress(int level);
 // Stream-ordered scratch from the library's own memory pool on the current device (release
 // threshold = unlimited, so memory freed at one call is reused by the next without going
 // back to the driver; the process's default pool is left untouched).

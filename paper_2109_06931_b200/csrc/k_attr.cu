@@ -42,6 +42,7 @@ namespace gpa {
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
+std::atomic<int> g_ring_stress{0};  // gpa_set_ring_stress (testing): TMA-ring timing perturbation, 0 = off
 
 
 // Warp-aggregated accumulate: lanes with equal `key` sum their counts; the lowest lane of
@@ -708,6 +709,7 @@ __device__ __forceinline__ uint32_t best_gran(unsigned long long b) { return b ?
 
 struct ProbeArgs {
   uint32_t base_lo, base_hi, span, gshift, n_gran;  // span = n_gran << gshift, one 4 GiB window (probe_ok)
+  uint32_t stress;                                  // ring stress test (gpa_set_ring_stress), 0 = off
 };
 
 // one record: granule (n_gran when outside the module), 2-way probe, shared byte add or L2 reduction.
@@ -771,7 +773,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles);
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles, A.stress);
     return;
   }
   uint64_t keep;  // L2 evict-last for Hg / acc (the record stream is evict-first)
@@ -785,6 +787,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   for (uint32_t it = 0; it < ntiles_me; ++it) {
     const uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait_s(full_s + st * 8, ph);
+    stress_sleep(A.stress, it, warp);
     uint4 v[R];
 #pragma unroll
     for (int u = 0; u < R; u++) v[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the tile end: masked
@@ -884,7 +887,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles);
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles, A.stress);
     return;
   }
   uint64_t keep;  // L2 evict-last for the code map and the reductions (the record stream is evict-first)
@@ -897,6 +900,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *gg, uint32_t *cc) {
     const uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait_s(full_s + st * 8, ph);
+    stress_sleep(A.stress, it, warp);
 #pragma unroll
     for (int u = 0; u < R; u++) vv[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the end: masked
     __syncwarp();
@@ -1041,7 +1045,7 @@ cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, c
                      uint32_t *ri, int sm_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift,
-                    (uint32_t)T.n_gran};
+                    (uint32_t)T.n_gran, (uint32_t)g_ring_stress.load(std::memory_order_relaxed)};
   cudaError_t e;
   if (p.variant == 7) {
     using RG = RingProbe;
@@ -1171,6 +1175,7 @@ cudaError_t launch_stream(const AttrTables &T, const uint4 *rec, uint64_t n, uns
 }  // namespace
 
 void set_attr_kernel(int which) { g_attr_kernel.store(which, std::memory_order_relaxed); }
+void set_ring_stress(int level) { g_ring_stress.store(level, std::memory_order_relaxed); }
 
 // the kernel a call of n records runs (1..8, gpa_set_attr_kernel numbering)
 int attr_choice(const AttrTables &T, uint64_t n) {

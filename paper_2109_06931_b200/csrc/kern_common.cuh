@@ -141,9 +141,21 @@ struct Ring {
 
 // producer warp body: one elected lane drives the bulk-copy engine over this CTA's tiles
 // (tiles t0, t0+step, ... < t1 of S records; the last tile of the stream may be partial)
+// ring stress testing (gpa_set_ring_stress): pseudo-random sleeps of 0..(stress*0.5) us that let the
+// producer run ahead of slow consumers and vice versa; 0 in production
+__device__ __forceinline__ void stress_sleep(uint32_t stress, uint32_t a, uint32_t b) {
+  if (stress) {
+    uint32_t h = (a * 0x9E3779B1u) ^ (b * 0x85EBCA77u) ^ stress;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if (h & 1u) __nanosleep((h >> 8) % (stress * 500u + 1u));
+  }
+}
+
 template <class RG>
 __device__ __forceinline__ void ring_produce(uint4 *ring, uint64_t *full, uint64_t *empty, const uint4 *rec,
-                                             uint64_t n, uint64_t t0, uint64_t step, uint64_t t1) {
+                                             uint64_t n, uint64_t t0, uint64_t step, uint64_t t1, uint32_t stress = 0) {
   constexpr int S = RG::kTile, NST = RG::kStages;
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
@@ -151,6 +163,7 @@ __device__ __forceinline__ void ring_produce(uint4 *ring, uint64_t *full, uint64
   for (uint64_t tile = t0; tile < t1; tile += step, ++it) {
     uint32_t st = it % NST, ph = (it / NST) & 1;
     if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
+    stress_sleep(stress, (uint32_t)tile, 0xFFFFu);
     uint64_t left = n - tile * S;
     uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);
     mbar_arrive_expect_tx(full + st, bytes);

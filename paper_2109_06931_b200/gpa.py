@@ -93,6 +93,7 @@ def _load():
         "gpa_profile_stats": ([_vp, _vp, _u32, _vp, _vp], S),
         "gpa_set_attr_kernel": ([ctypes.c_int], S),
         "gpa_attr_kernel_choice": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int)], S),
+        "gpa_set_ring_stress": ([ctypes.c_int], S),
         "gpa_sparse_build": ([_vp, _vp, _u32, ctypes.c_int, ctypes.POINTER(_vp), _vp], S),
         "gpa_get_sparse_view": ([_vp, ctypes.POINTER(SparseView)], S),
         "gpa_free_sparse": ([_vp], None),
@@ -132,6 +133,11 @@ def set_attr_kernel(which: int) -> None:
     4 TMA + shared-memory rows, 5 / 6 byte / half-word packed bins, 7 shared-memory probe table of
     granule rows, 8 byte bins through a 32-bit code map (include/gpa.h)."""
     _check(_lib.gpa_set_attr_kernel(int(which)), "gpa_set_attr_kernel")
+
+
+def set_ring_stress(level: int) -> None:
+    """Testing: perturb the TMA-ring timing of kernels 7 / 8 (0 = off; gpa.h)."""
+    _check(_lib.gpa_set_ring_stress(int(level)), "gpa_set_ring_stress")
 
 
 ATTR_KERNEL_NAMES = {1: "k_attr_stream", 2: "k_attr_tma", 3: "k_attr_bins", 4: "k_attr_hot", 5: "k_attr_bins",

@@ -518,3 +518,22 @@ def test_host_path_many_chunks(gpa, pinned):
     Ho, Uo, _ = oracle.attribute(w.structure, host.numpy().view(gen.RECORD_DTYPE).reshape(-1),
                                  threads=len(__import__("os").sched_getaffinity(0)))
     assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
+
+
+@pytest.mark.parametrize("kernel", [7, 8])
+@pytest.mark.parametrize("stress", [1, 8])
+def test_ring_stress_exact(gpa, attr_kernel, kernel, stress):
+    """Adversarial TMA-ring timing (gpa_set_ring_stress: random producer and consumer sleeps, so
+    the producer runs ahead of slow consumers and consumers wait on refills): a stage refilled
+    before every consumer read it would corrupt H; the result stays bit-exact."""
+    attr_kernel(kernel)
+    gpa.set_ring_stress(stress)
+    try:
+        w = gen.workload("C4" if kernel == 7 else "C5", records=4_200_007)
+        s = gpa.load_structure(w.structure, 0)
+        H, U, ri = _attribute(gpa, s, _device_records(w))
+    finally:
+        gpa.set_ring_stress(0)
+    Ho, Uo, rio = oracle.attribute(w.structure, w.records_host(), rec_inst=True)
+    assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
+    assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
