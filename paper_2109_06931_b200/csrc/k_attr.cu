@@ -960,7 +960,7 @@ done:
 #define GPA_CODE_NC 31
 #endif
 #ifndef GPA_CODE_R
-#define GPA_CODE_R 2
+#define GPA_CODE_R 3
 #endif
 #ifndef GPA_CODE_NST
 #define GPA_CODE_NST 2
@@ -977,9 +977,12 @@ using RingCode = Ring<GPA_CODE_NC, GPA_CODE_R, GPA_CODE_NST>;
 // chunks: the result is exact for every plan, only the speed depends on how well it fits ------------
 constexpr uint32_t kCodeK = (uint32_t)kHotBins * 4;  // K_attr_code32 byte bins
 
-static uint64_t plan_sample(uint64_t n) {
-  return std::min<uint64_t>(std::min<uint64_t>((uint64_t)kSampleChunks * kSampleChunk, 1ull << GPA_SAMPLE_MAX_LOG),
-                            std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
+// records sampled to build a plan: n/256, at least 2^18, at most 2^21 for the probe table (7) and
+// 2^22 for the 131 072 byte bins of 8, whose ranking needs the finer counts (C5: 12.77 -> 12.7 ms;
+// C4 with 7 got slower with 2^22)
+static uint64_t plan_sample(uint64_t n, int variant) {
+  const int cap = variant == 8 ? GPA_SAMPLE_MAX_LOG + 1 : GPA_SAMPLE_MAX_LOG;
+  return std::min<uint64_t>(1ull << cap, std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
 }
 
 size_t plan_bytes(const AttrTables &T, int variant) {
@@ -991,7 +994,7 @@ cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint6
                        int sm_count, cudaStream_t st) {
   p->variant = variant;
   p->n_gran = T.n_gran;
-  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, plan_sample(n) / kSampleChunk);
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, plan_sample(n, variant) / kSampleChunk);
   cudaError_t e;
   if (variant == 7) {
     p->best = reinterpret_cast<unsigned long long *>(mem);
