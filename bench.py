@@ -253,8 +253,7 @@ def run_gpa(args):
         if timed:
             ev_b0.append(ready)
         side.wait_event(ready)
-        for sc in SCOPES:
-            gpa.derive_metrics_range(s, sc, H, lo, hi, metrics=met[sc], stream=side)
+        gpa.derive_scopes(s, H, {sc: {"metrics": met[sc]} for sc in SCOPES}, lo, hi, stream=side)
         if timed:
             sd = torch.cuda.Event(enable_timing=True)
             sd.record(side)
@@ -291,8 +290,7 @@ def run_gpa(args):
         if timed:
             ev_b0.append(ready)
         side.wait_event(ready)
-        for sc in SCOPES:
-            gpa.derive_metrics(s, sc, H, metrics=met[sc], stream=side)
+        gpa.derive_scopes(s, H, {sc: {"metrics": met[sc]} for sc in SCOPES}, stream=side)
         if timed:
             sd = torch.cuda.Event(enable_timing=True)
             sd.record(side)

@@ -432,6 +432,14 @@ GPA_API gpa_status gpa_partition_structure(const gpa_structure_desc *desc, uint3
 GPA_API gpa_status gpa_derive_metrics_range(gpa_structure s, gpa_scope scope, const uint64_t *d_inst_hist,
                                             uint32_t inst_lo, uint32_t inst_hi, uint64_t *d_scope_hist,
                                             uint64_t *d_scope_mix, double *d_metrics, gpa_stream_t stream);
+/* All static scope kinds in one pass (one kernel launch + one for multi-chunk rows instead of one
+ * or two per scope): outs[k] for k = GPA_SCOPE_INST .. GPA_SCOPE_FUNC (5 entries) gives that
+ * scope's d_scope_hist / d_scope_mix / d_metrics exactly as gpa_derive_metrics would (any NULL;
+ * an all-NULL entry skips the scope).  inst_lo = 0, inst_hi = n_inst: every row; otherwise the
+ * rows of the function-aligned range, as gpa_derive_metrics_range.  Enqueue-only. */
+typedef struct { uint64_t *scope_hist; uint64_t *scope_mix; double *metrics; } gpa_scope_out;
+GPA_API gpa_status gpa_derive_scopes(gpa_structure s, const uint64_t *d_inst_hist, uint32_t inst_lo, uint32_t inst_hi,
+                                     const gpa_scope_out *outs, gpa_stream_t stream);
 /* CCT Step 1 on a range: S_f (d_func_hist[f*16 + r], u64) for the functions of
  * [inst_lo, inst_hi) and w_e (d_call_weight[e] = sum_{r<12} H[call_inst[e]][r], R10) for the call
  * sites whose call instruction lies in it; other entries are left untouched (zero them, then

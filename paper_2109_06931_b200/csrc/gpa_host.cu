@@ -403,6 +403,7 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
     row_func[k][row_of[x]] = dv.func_of_scope[y];
   }
   for (uint32_t f = 0; f < nf; f++) row_func[ROLL_FUNC][f] = f;
+  std::vector<std::vector<uint32_t>> h_chunks(ROLL_KINDS), h_mrows(ROLL_KINDS);
   for (int k = 0; k < ROLL_KINDS; k++) {
     UP(R[k].d_ptr, ptr[k]);
     UP(R[k].d_inst, lst[k]);
@@ -435,6 +436,51 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
     UP(R[k].d_chunk, chunk);
     UP(R[k].d_multi_slot, mslot);
     UP(R[k].d_multi_rows, mrows);
+    h_chunks[k] = std::move(chunk);
+    h_mrows[k] = std::move(mrows);
+  }
+  // the four kinds merged for gpa_derive_scopes: chunks and multi rows in function order (ties:
+  // LINE, LOOP, INLINE, FUNC), instruction lists concatenated
+  {
+    MultiRoll &M = s->multi;
+    std::vector<uint32_t> off(ROLL_KINDS + 1, 0);
+    for (int k = 0; k < ROLL_KINDS; k++) off[k + 1] = off[k] + (uint32_t)lst[k].size();
+    std::vector<uint32_t> all_lst(off[ROLL_KINDS]);
+    for (int k = 0; k < ROLL_KINDS; k++) std::copy(lst[k].begin(), lst[k].end(), all_lst.begin() + off[k]);
+    struct Item { uint32_t key, kind, a, b, c; };
+    std::vector<Item> items, mitems;
+    for (int k = 0; k < ROLL_KINDS; k++) {
+      for (size_t c = 0; c < R[k].h_chunk_key.size(); c++)
+        items.push_back({R[k].h_chunk_key[c], (uint32_t)k + 1, h_chunks[k][3 * c], h_chunks[k][3 * c + 1] + off[k],
+                         h_chunks[k][3 * c + 2] + off[k]});
+      for (size_t c = 0; c < h_mrows[k].size(); c++) mitems.push_back({R[k].h_multi_key[c], (uint32_t)k + 1, h_mrows[k][c], 0, 0});
+    }
+    auto by_key = [](const Item &x, const Item &y) { return x.key != y.key ? x.key < y.key : x.kind < y.kind; };
+    std::stable_sort(items.begin(), items.end(), by_key);
+    std::stable_sort(mitems.begin(), mitems.end(), by_key);
+    std::vector<uint32_t> ch(4 * items.size()), mr(2 * mitems.size());
+    M.h_chunk_key.resize(items.size());
+    M.h_multi_key.resize(mitems.size());
+    for (size_t i = 0; i < items.size(); i++) {
+      ch[4 * i] = items[i].kind; ch[4 * i + 1] = items[i].a; ch[4 * i + 2] = items[i].b; ch[4 * i + 3] = items[i].c;
+      M.h_chunk_key[i] = items[i].key;
+    }
+    std::vector<std::vector<uint32_t>> ms(ROLL_KINDS + 1);
+    for (int k = 0; k < ROLL_KINDS; k++) ms[k + 1].assign(R[k].rows ? R[k].rows : 1, NONE);
+    for (size_t i = 0; i < mitems.size(); i++) {
+      mr[2 * i] = mitems[i].kind; mr[2 * i + 1] = mitems[i].a;
+      M.h_multi_key[i] = mitems[i].key;
+      ms[mitems[i].kind][mitems[i].a] = (uint32_t)i;
+    }
+    M.n_chunks = (uint32_t)items.size();
+    M.n_multi = (uint32_t)mitems.size();
+    if (ch.empty()) ch.assign(4, 0);
+    if (mr.empty()) mr.assign(2, 0);
+    if (all_lst.empty()) all_lst.assign(1, 0);
+    UP(M.d_chunk, ch);
+    UP(M.d_lst, all_lst);
+    UP(M.d_mrows, mr);
+    for (int k = 1; k <= ROLL_KINDS; k++) UP(M.d_mslot[k], ms[k]);
   }
 
   // ---- Step 1 structure: call graph from call instructions ---------------------
@@ -1515,6 +1561,50 @@ gpa_status gpa_derive_metrics_range(gpa_structure s, gpa_scope scope, const uint
   range_runs(s->roll[k], inst_lo, inst_hi, s->info.n_inst, &c0, &c1, &m0, &m1);
   CU(launch_rollup(&s->roll[k], s->roll[k].rows, d_inst_hist, s->d_inst_class, d_scope_hist, d_scope_mix, d_metrics,
                    sm_count(s->device), st, c0, c1, m0, m1));
+  return GPA_OK;
+}
+
+gpa_status gpa_derive_scopes(gpa_structure s, const uint64_t *d_inst_hist, uint32_t inst_lo, uint32_t inst_hi,
+                             const gpa_scope_out *outs, gpa_stream_t stream) {
+  if (!s || !outs) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  const uint32_t ni = s->info.n_inst;
+  const bool whole = inst_lo == 0 && inst_hi == ni;
+  if (!whole) CHECK(check_range(s, inst_lo, inst_hi));
+  else if (inst_lo > inst_hi) return fail(GPA_ERR_INVALID_ARG, "bad range");
+  uint64_t *hist[5], *mix[5];
+  double *met[5];
+  bool any = false;
+  for (int k = 0; k < 5; k++) {
+    hist[k] = outs[k].scope_hist;
+    mix[k] = outs[k].scope_mix;
+    met[k] = outs[k].metrics;
+    if (((uintptr_t)hist[k] | (uintptr_t)mix[k]) & 15)
+      return fail(GPA_ERR_INVALID_ARG, "histogram buffers must be 16-byte aligned");
+    if ((uintptr_t)met[k] & 7) return fail(GPA_ERR_INVALID_ARG, "metrics buffers must be 8-byte aligned");
+    any = any || hist[k] || mix[k] || met[k];
+  }
+  if (!any) return GPA_OK;
+  if (!d_inst_hist && ni) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  if ((uintptr_t)d_inst_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist must be 16-byte aligned");
+  DeviceGuard g(s->device);
+  CU(g.err);
+  const MultiRoll &M = s->multi;
+  uint32_t c0 = 0, c1 = M.n_chunks, m0 = 0, m1 = M.n_multi;
+  if (!whole) {
+    auto lb = [](const std::vector<uint32_t> &v, uint32_t x) {
+      return (uint32_t)(std::lower_bound(v.begin(), v.end(), x) - v.begin());
+    };
+    c0 = lb(M.h_chunk_key, inst_lo);
+    c1 = inst_hi >= ni ? M.n_chunks : lb(M.h_chunk_key, inst_hi);
+    m0 = lb(M.h_multi_key, inst_lo);
+    m1 = inst_hi >= ni ? M.n_multi : lb(M.h_multi_key, inst_hi);
+  }
+  bool tree = false;
+  for (int k = 1; k < 5; k++) tree = tree || hist[k] || mix[k] || met[k];
+  if (!tree) c0 = c1 = m0 = m1 = 0;
+  const bool inst = hist[0] || mix[0] || met[0];
+  CU(launch_rollup_multi(M, c0, c1, m0, m1, inst_lo, inst ? inst_hi - inst_lo : 0, d_inst_hist, s->d_inst_class, hist,
+                         mix, met, sm_count(s->device), (cudaStream_t)stream));
   return GPA_OK;
 }
 

@@ -49,6 +49,17 @@ struct RollSet {
   std::vector<uint32_t> h_chunk_key, h_multi_key;
 };
 
+// the four tree kinds merged (gpa_derive_scopes): one chunk list in function order over the
+// concatenated instruction lists, multi-chunk rows with merged slots
+struct MultiRoll {
+  uint32_t n_chunks = 0, n_multi = 0;
+  uint32_t *d_chunk = nullptr;   // [4*n_chunks] (kind, row, begin, end); kind 1..4 = LINE, LOOP, INLINE, FUNC
+  uint32_t *d_lst = nullptr;     // concatenated instruction lists
+  uint32_t *d_mrows = nullptr;   // [2*n_multi] (kind, row)
+  uint32_t *d_mslot[5] = {};     // per kind (index 1..4): row -> merged multi slot or NONE; [0] unused
+  std::vector<uint32_t> h_chunk_key, h_multi_key;
+};
+
 }  // namespace gpa
 
 struct gpa_structure_s {
@@ -63,6 +74,7 @@ struct gpa_structure_s {
   uint32_t *d_gfunc = nullptr;      // function of each granule of the pc map (NONE in gaps)
   uint32_t *d_gmap = nullptr;
   gpa::RollSet roll[gpa::ROLL_KINDS];
+  gpa::MultiRoll multi;
   // call graph (function level)
   uint32_t *d_call_inst = nullptr, *d_call_callee = nullptr, *d_call_caller = nullptr;
   uint32_t *d_fin_ptr = nullptr, *d_fin_e = nullptr;    // in-edges per function
@@ -163,6 +175,12 @@ cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_h
 cudaError_t launch_cct_weights_range(const gpa_structure_s *s, const uint64_t *d_hist, uint32_t lo, uint32_t hi,
                                      uint64_t *d_w, cudaStream_t st);
 cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st);
+// all scope kinds in one launch: INST rows [ident_lo, ident_lo + n_ident) and merged chunks [c0, c1),
+// multi rows [m0, m1); outputs indexed by gpa_scope (0 INST .. 4 FUNC), NULL = not produced
+cudaError_t launch_rollup_multi(const MultiRoll &M, uint32_t c0, uint32_t c1, uint32_t m0, uint32_t m1, uint32_t ident_lo,
+                                uint32_t n_ident, const uint64_t *d_hist, const uint8_t *d_class,
+                                uint64_t *const hist[5], uint64_t *const mix[5], double *const met[5], int sm_count,
+                                cudaStream_t st);
 
 // CCT pieces (k_cct.cu)
 cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist, uint64_t *d_w,

@@ -146,6 +146,78 @@ __global__ void __launch_bounds__(256) k_rollup_fin(const uint32_t *__restrict__
   }
 }
 
+// ---- all scope kinds in one launch (gpa_derive_scopes) ----------------------------------------
+// items [0, n_ident): INST rows ident_lo + w (identity); then the merged chunk list of the tree
+// kinds (kind, row, begin, end into the concatenated instruction lists), ordered by function.
+struct ScopeOuts {
+  uint64_t *hist[5];
+  uint64_t *mix[5];
+  double *met[5];
+  const uint32_t *mslot[5];  // per tree kind: row -> merged multi slot (NONE = single chunk)
+};
+
+__global__ void __launch_bounds__(256) k_rollup_multi(const uint4 *__restrict__ chunk, uint32_t n_chunk,
+                                                      uint32_t ident_lo, uint32_t n_ident,
+                                                      const uint32_t *__restrict__ lst, const uint64_t *__restrict__ H,
+                                                      const uint8_t *__restrict__ cls, ScopeOuts O,
+                                                      unsigned long long *__restrict__ scratch) {
+  const int q = threadIdx.x & 3;
+  const unsigned qm = quad_mask();
+  const uint32_t nq = (gridDim.x * blockDim.x) >> 2;
+  const uint32_t items = n_ident + n_chunk;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 2; w < items; w += nq) {
+    uint32_t kind, row, b, e;
+    const bool ident = w < n_ident;
+    if (ident) {
+      kind = 0; row = ident_lo + w; b = row; e = row + 1;
+    } else {
+      const uint4 c = __ldg(chunk + (w - n_ident));
+      kind = c.x; row = c.y; b = c.z; e = c.w;
+    }
+    Acc a = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    uint32_t j = b;
+    for (; j + 4 <= e; j += 4) {
+      uint32_t i0 = ident ? j : __ldg(lst + j), i1 = ident ? j + 1 : __ldg(lst + j + 1);
+      uint32_t i2 = ident ? j + 2 : __ldg(lst + j + 2), i3 = ident ? j + 3 : __ldg(lst + j + 3);
+      acc_inst(a, H, cls, i0, q, qm);
+      acc_inst(a, H, cls, i1, q, qm);
+      acc_inst(a, H, cls, i2, q, qm);
+      acc_inst(a, H, cls, i3, q, qm);
+    }
+    for (; j < e; j++) acc_inst(a, H, cls, ident ? j : __ldg(lst + j), q, qm);
+    const uint32_t slot = ident ? NONE : __ldg(O.mslot[kind] + row);
+    if (slot == NONE) {
+      finalize(a, row, q, qm, O.hist[kind], O.mix[kind], O.met[kind]);
+    } else {
+      unsigned long long *sp = scratch + (uint64_t)slot * 32;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        if (a.h[t]) atomicAdd(sp + 4 * q + t, a.h[t]);
+        if (a.m[t]) atomicAdd(sp + 16 + 4 * q + t, a.m[t]);
+      }
+    }
+  }
+}
+
+// multi-chunk rows: (kind, row) pairs, slots m0 .. m0 + n of the merged multi list
+__global__ void __launch_bounds__(256) k_rollup_fin_multi(const uint2 *__restrict__ mrows, uint32_t n_multi,
+                                                          const unsigned long long *__restrict__ scratch, ScopeOuts O) {
+  const int q = threadIdx.x & 3;
+  const unsigned qm = quad_mask();
+  const uint32_t nq = (gridDim.x * blockDim.x) >> 2;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 2; w < n_multi; w += nq) {
+    const unsigned long long *sp = scratch + (uint64_t)w * 32;
+    Acc a;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      a.h[t] = sp[4 * q + t];
+      a.m[t] = sp[16 + 4 * q + t];
+    }
+    const uint2 kr = __ldg(mrows + w);
+    finalize(a, kr.y, q, qm, O.hist[kr.x], O.mix[kr.x], O.met[kr.x]);
+  }
+}
+
 // CCT rows: fp64 vectors; S and the latency sum fold slots left to right (R3, R4).
 __global__ void __launch_bounds__(256) k_derive_f64(const double *__restrict__ V, uint64_t rows,
                                                     double *__restrict__ metrics) {
@@ -210,6 +282,45 @@ cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_h
     uint64_t b2 = ((uint64_t)n_multi * 4 + 255) / 256;
     k_rollup_fin<<<(unsigned)(b2 < cap ? b2 : cap), 256, 0, st>>>(set->d_multi_rows + m0, n_multi, scratch, d_out_hist,
                                                                    d_out_mix, d_metrics);
+    count_launches(1);
+    cudaError_t e2 = cudaGetLastError();
+    cudaError_t e3 = cudaFreeAsync(scratch, st);
+    if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
+  }
+  return e;
+}
+
+cudaError_t launch_rollup_multi(const MultiRoll &M, uint32_t c0, uint32_t c1, uint32_t m0, uint32_t m1, uint32_t ident_lo,
+                                uint32_t n_ident, const uint64_t *d_hist, const uint8_t *d_class,
+                                uint64_t *const hist[5], uint64_t *const mix[5], double *const met[5], int sm_count,
+                                cudaStream_t st) {
+  ScopeOuts O;
+  for (int k = 0; k < 5; k++) {
+    O.hist[k] = hist[k];
+    O.mix[k] = mix[k];
+    O.met[k] = met[k];
+    O.mslot[k] = M.d_mslot[k];
+  }
+  const uint32_t n_chunk = c1 > c0 ? c1 - c0 : 0, n_multi = m1 > m0 ? m1 - m0 : 0;
+  const uint32_t items = n_ident + n_chunk;
+  if (items == 0) return cudaSuccess;
+  unsigned long long *scratch = nullptr;
+  if (n_multi) {
+    cudaError_t e = pool_alloc((void **)&scratch, (size_t)n_multi * 32 * 8, st);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(scratch, 0, (size_t)n_multi * 32 * 8, st);
+  }
+  uint64_t want = ((uint64_t)items * 4 + 255) / 256;
+  uint64_t cap = (uint64_t)sm_count * 8;
+  unsigned blocks = (unsigned)(want < cap ? want : cap);
+  k_rollup_multi<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4 *>(M.d_chunk) + c0, n_chunk, ident_lo, n_ident,
+                                         M.d_lst, d_hist, d_class, O, scratch ? scratch - (size_t)m0 * 32 : nullptr);
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (n_multi) {
+    uint64_t b2 = ((uint64_t)n_multi * 4 + 255) / 256;
+    k_rollup_fin_multi<<<(unsigned)(b2 < cap ? b2 : cap), 256, 0, st>>>(
+        reinterpret_cast<const uint2 *>(M.d_mrows) + m0, n_multi, scratch, O);
     count_launches(1);
     cudaError_t e2 = cudaGetLastError();
     cudaError_t e3 = cudaFreeAsync(scratch, st);

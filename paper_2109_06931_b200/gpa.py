@@ -103,6 +103,7 @@ def _load():
         "gpa_profile_stats_f64": ([_u64, _vp, _u32, _vp, ctypes.c_int, _vp], S),
         "gpa_idleness_blame": ([ctypes.POINTER(TraceDesc), _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp], S),
         "gpa_partition_structure": ([ctypes.POINTER(StructureDesc), _u32, _vp], S),
+        "gpa_derive_scopes": ([_vp, _vp, _u32, _u32, _vp, _vp], S),
         "gpa_attr_plan_create": ([_vp, _vp, _u64, ctypes.POINTER(_vp), _vp], S),
         "gpa_attr_plan_variant": ([_vp, ctypes.POINTER(ctypes.c_int)], S),
         "gpa_attribute_samples_planned": ([_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp], S),
@@ -556,6 +557,22 @@ def derive_metrics_range(s: Structure, scope: str, inst_hist, inst_lo: int, inst
                                          int(inst_hi), _ptr(scope_hist, "scope_hist"), _ptr(scope_mix, "scope_mix"),
                                          _ptr(metrics, "metrics"), _stream_ptr(stream, inst_hist.device)),
            "gpa_derive_metrics_range")
+
+
+_SCOPE_ORDER = ("INST", "LINE", "LOOP", "INLINE", "FUNC")
+
+
+def derive_scopes(s: Structure, inst_hist, outs: dict, inst_lo: int = 0, inst_hi: int | None = None,
+                  stream=None) -> None:
+    """All static scopes in one pass: outs = {scope: {"scope_hist"|"scope_mix"|"metrics": tensor}} (gpa.h)."""
+    arr = (ctypes.c_void_p * 15)()
+    for k, sc in enumerate(_SCOPE_ORDER):
+        o = outs.get(sc, {})
+        for j, key in enumerate(("scope_hist", "scope_mix", "metrics")):
+            arr[3 * k + j] = _ptr(o.get(key), key)
+    hi = s.info["n_inst"] if inst_hi is None else int(inst_hi)
+    _check(_lib.gpa_derive_scopes(s.handle, _ptr(inst_hist, "inst_hist"), int(inst_lo), hi, arr,
+                                  _stream_ptr(stream, inst_hist.device)), "gpa_derive_scopes")
 
 
 def cct_inputs(s: Structure, inst_hist, inst_lo: int, inst_hi: int, func_hist, call_weight, stream=None) -> None:

@@ -205,3 +205,43 @@ def test_bench_two_ranks(gpa):
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and "reduce-scatter" in d["config"]["parallelism"]
+
+
+@pytest.mark.parametrize("name,records", [("C2", 3_000_000), ("C3", 2_000_000), ("C1", 50_000)])
+def test_derive_scopes_matches_per_scope(gpa, name, records):
+    """gpa_derive_scopes (all kinds in one launch) writes exactly what gpa_derive_metrics writes per
+    scope (histograms, mixes, metrics; bit-identical), for the whole structure and for
+    function-aligned ranges."""
+    w = gen.workload(name, records=records)
+    st = w.structure
+    s = gpa.load_structure(st, 0)
+    rec = torch.empty((w.cfg.records, 2), dtype=torch.int64, device="cuda")
+    w.records_device(rec)
+    ni = s.info["n_inst"]
+    H = torch.zeros((ni, 16), dtype=torch.int64, device="cuda")
+    U = torch.zeros(16, dtype=torch.int64, device="cuda")
+    gpa.attribute_samples(s, rec, H, U)
+    rows = {sc: len(s.rows(sc)) for sc in SCOPES}
+
+    def outs(fill):
+        return {sc: {"scope_hist": torch.full((max(rows[sc], 1), 16), fill, dtype=torch.int64, device="cuda"),
+                     "scope_mix": torch.full((max(rows[sc], 1), 16), fill, dtype=torch.int64, device="cuda"),
+                     "metrics": torch.full((max(rows[sc], 1), 33), float(fill), dtype=torch.float64, device="cuda")}
+                for sc in SCOPES}
+
+    ref = outs(-1)
+    for sc in SCOPES:
+        if rows[sc]:
+            gpa.derive_metrics(s, sc, H, **ref[sc])
+    got = outs(-1)
+    gpa.derive_scopes(s, H, got)
+    parts = outs(-1)
+    b = [int(x) for x in gpa.partition_structure(st, 3)]
+    for r in range(3):
+        gpa.derive_scopes(s, H, parts, b[r], b[r + 1])
+    torch.cuda.synchronize()
+    for sc in SCOPES:
+        for k in ("scope_hist", "scope_mix", "metrics"):
+            a = ref[sc][k].cpu().numpy().view(np.uint64)
+            assert np.array_equal(got[sc][k].cpu().numpy().view(np.uint64), a), (sc, k)
+            assert np.array_equal(parts[sc][k].cpu().numpy().view(np.uint64), a), (sc, k, "ranges")
