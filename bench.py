@@ -213,12 +213,8 @@ def run_gpa(args):
         return r
 
     rec = make_shard(a, n)
-    HU = torch.zeros(ni * 16 + 16, dtype=torch.int64, device=dev)   # H_inst || U, one buffer
-    H, U = HU[:ni * 16].view(ni, 16), HU[ni * 16:]
     rows = {sc: max(1, gpa.scope_row_count(s, sc)) for sc in SCOPES}
     met = {sc: torch.empty((rows[sc], gpa.NUM_DERIVED), dtype=torch.float64, device=dev) for sc in SCOPES}
-    ev_a0, ev_a1 = [], []
-
     # N > 1: the reduced histogram is scattered at function-aligned
     # instruction bounds and every rank derives the rows of its own functions; the CCT's Step-1
     # inputs (S_f, w: 0.7 MB at C5) are summed to rank 0, which reconstructs the tree
@@ -227,90 +223,119 @@ def run_gpa(args):
         bounds = [int(x) for x in gpa.partition_structure(w.structure, world)]
         lo, hi = bounds[rank], bounds[rank + 1]
         nf, nc = s.info["n_func"], s.info["n_call"]
-        SW = torch.zeros(nf * 16 + nc, dtype=torch.int64, device=dev)   # S_f || w
-        SF, CW = SW[:nf * 16].view(nf, 16), SW[nf * 16:]
-    ev_a0, ev_a1 = [], []
+    # Two batch buffers.  Default: one batch at a time (attribution on stream A, then the combine
+    # and CCT on the high-priority stream B with the scope roll-ups on a side stream).  --pipeline
+    # enqueues batch i + 1's attribution before batch i's analysis; measured slower:
+    # the persistent attribution CTAs occupy every SM, so the analysis kernels wait for them.
+    class Buf:
+        pass
 
-    def step(timed: bool):
-        HU.zero_()
+    bufs = []
+    for _ in range(2):
+        x = Buf()
+        x.HU = torch.zeros(ni * 16 + 16, dtype=torch.int64, device=dev)   # H_inst || U, one buffer
+        x.H, x.U = x.HU[:ni * 16].view(ni, 16), x.HU[ni * 16:]
+        if scatter:
+            x.SW = torch.zeros(nf * 16 + nc, dtype=torch.int64, device=dev)   # S_f || w
+            x.SF, x.CW = x.SW[:nf * 16].view(nf, 16), x.SW[nf * 16:]
+        x.attr_done = torch.cuda.Event()
+        x.freed = torch.cuda.Event()
+        x.freed.record(stream)
+        bufs.append(x)
+    B = stream                                       # combine + CCT (high priority)
+    A = torch.cuda.Stream(dev) if args.pipeline else B   # attribution
+    side = torch.cuda.Stream(dev)                    # scope roll-ups
+    ev_a0, ev_a1, ev_b0, ev_b1, ev_c1 = [], [], [], [], []
+
+    def enqueue_attr(i: int, timed: bool, host=None):
+        x = bufs[i % 2]
+        A.wait_event(x.freed)
+        with torch.cuda.stream(A):
+            x.HU.zero_()
         if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        gpa.attribute_samples(s, rec, H, U, n=n, stream=stream)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(A)
+        if host is None:
+            gpa.attribute_samples(s, rec, x.H, x.U, n=n, stream=A)
+        else:
+            gpa.attribute_samples_host(s, host, x.H, x.U, stream=A)
         if timed:
-            e1.record(stream)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(A)
             ev_a0.append(e0)
             ev_a1.append(e1)
-        return combine_analyse(timed)
+        x.attr_done.record(A)
 
-    def combine_analyse(timed: bool = False):
-        if not scatter:
-            reduce_histogram(HU, dst=0)
-            return analyse(timed) if rank == 0 else 0
-        reduce_scatter_histogram(HU, bounds, ni)
-        ready = torch.cuda.Event(enable_timing=timed)
-        ready.record(stream)
-        if timed:
-            ev_b0.append(ready)
-        side.wait_event(ready)
-        gpa.derive_scopes(s, H, {sc: {"metrics": met[sc]} for sc in SCOPES}, lo, hi, stream=side)
-        if timed:
-            sd = torch.cuda.Event(enable_timing=True)
-            sd.record(side)
-            ev_b1.append(sd)
-        SW.zero_()
-        gpa.cct_inputs(s, H, lo, hi, SF, CW, stream=stream)
-        dist.reduce(SW, dst=0)
-        nctx = 0
-        if rank == 0:
-            cct = gpa.reconstruct_cct_inputs(s, SF, CW, stream=stream)
-            cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
-            gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
-            gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
+    def analyse(i: int, timed: bool, results=None):
+        """Batch i after its attribution: combine (N > 1), the five scopes' roll-ups + metrics on the
+        side stream concurrently with the CCT + its metrics on B; returns the context count."""
+        x = bufs[i % 2]
+        B.wait_event(x.attr_done)
+        with torch.cuda.stream(B):
+            if world > 1:
+                if scatter:
+                    reduce_scatter_histogram(x.HU, bounds, ni)
+                else:
+                    reduce_histogram(x.HU, dst=0)
+            ready = torch.cuda.Event(enable_timing=timed)
+            ready.record(B)
             if timed:
-                ce = torch.cuda.Event(enable_timing=True)
-                ce.record(stream)
-                ev_c1.append(ce)
-            nctx = cct.n
-        stream.wait_stream(side)
-        stream.synchronize()
-        if rank == 0:
-            cct.free()
+                ev_b0.append(ready)
+            do_scopes = scatter or rank == 0
+            if do_scopes:
+                side.wait_event(ready)
+                if scatter:
+                    gpa.derive_scopes(s, x.H, {sc: {"metrics": met[sc]} for sc in SCOPES}, lo, hi, stream=side)
+                else:
+                    gpa.derive_scopes(s, x.H, {sc: {"metrics": met[sc]} for sc in SCOPES}, stream=side)
+                if timed:
+                    sd = torch.cuda.Event(enable_timing=True)
+                    sd.record(side)
+                    ev_b1.append(sd)
+            nctx, cct = 0, None
+            if scatter:
+                x.SW.zero_()
+                gpa.cct_inputs(s, x.H, lo, hi, x.SF, x.CW, stream=B)
+                dist.reduce(x.SW, dst=0)
+                if rank == 0:
+                    cct = gpa.reconstruct_cct_inputs(s, x.SF, x.CW, stream=B)
+            elif rank == 0:
+                cct = gpa.reconstruct_cct(s, x.H, stream=B)
+            if cct is not None:
+                cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+                gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=B)
+                gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=B)
+                if timed:
+                    ce = torch.cuda.Event(enable_timing=True)
+                    ce.record(B)
+                    ev_c1.append(ce)
+                nctx = cct.n
+            if do_scopes:
+                B.wait_stream(side)
+            if results is not None:      # e2e: read the batch's results back to the host
+                for dst, src in results(x):
+                    dst.copy_(src, non_blocking=True)
+            x.freed.record(B)
+            if cct is not None:
+                cct.free()               # stream-ordered on B
         return nctx
 
-    side = torch.cuda.Stream(dev)
+    pipeline = args.pipeline
 
-    ev_b0, ev_b1, ev_c1 = [], [], []
-
-    def analyse(timed: bool = False):
-        """Roll-up + metrics of the five scopes on a side stream, concurrently with the CCT
-        (both only read H)."""
-        ready = torch.cuda.Event(enable_timing=timed)
-        ready.record(stream)
-        if timed:
-            ev_b0.append(ready)
-        side.wait_event(ready)
-        gpa.derive_scopes(s, H, {sc: {"metrics": met[sc]} for sc in SCOPES}, stream=side)
-        if timed:
-            sd = torch.cuda.Event(enable_timing=True)
-            sd.record(side)
-            ev_b1.append(sd)
-        cct = gpa.reconstruct_cct(s, H, stream=stream)
-        cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
-        gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=stream)
-        gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=stream)
-        if timed:
-            ce = torch.cuda.Event(enable_timing=True)
-            ce.record(stream)
-            ev_c1.append(ce)
-        stream.wait_stream(side)
-        stream.synchronize()
-        nctx = cct.n
-        cct.free()
+    def run_steps(k: int, timed: bool, host=None, results=None):
+        """k batches; pipelined: attribution of i + 1 is enqueued before the analysis of i."""
+        nctx = 0
+        for i in range(k):
+            enqueue_attr(i, timed, host)
+            if not pipeline:
+                nctx = analyse(i, timed, results)
+            elif i > 0:
+                nctx = analyse(i - 1, timed, results)
+        if pipeline and k > 0:
+            nctx = analyse(k - 1, timed, results)
         return nctx
 
-    for _ in range(args.warmup):
-        nctx = step(False)
+    nctx = run_steps(args.warmup, False)
     torch.cuda.synchronize()
     root_less = 0
     if world > 1 and not args.no_balance:
@@ -320,14 +345,13 @@ def run_gpa(args):
         # the shards are regenerated and re-warmed before the timed region.
         cal = []
         for _ in range(2):
-            HU.zero_()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            ev[0].record(stream)
-            gpa.attribute_samples(s, rec, H, U, n=n, stream=stream)
-            ev[1].record(stream)
-            ev[2].record(stream)
-            combine_analyse(False)
-            ev[3].record(stream)
+            ev[0].record(A)
+            enqueue_attr(0, False)
+            ev[1].record(A)
+            ev[2].record(A)
+            analyse(0, False)
+            ev[3].record(B)
             torch.cuda.synchronize()
             cal.append((ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])))
         t_at, t_an = cal[-1]
@@ -343,8 +367,7 @@ def run_gpa(args):
             torch.cuda.empty_cache()
             a, b, n = a2, b2, b2 - a2
             rec = make_shard(a, n)
-        for _ in range(args.warmup):
-            nctx = step(False)
+        nctx = run_steps(args.warmup, False)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -355,10 +378,10 @@ def run_gpa(args):
             dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.steps):
-            nctx = step(True)
-        t1.record(stream)
+        t0.record(A)
+        nctx = run_steps(args.steps, True)
+        B.wait_stream(A)
+        t1.record(B)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -378,37 +401,30 @@ def run_gpa(args):
         launches = int(lt.item())
     clocks = clk.summary()
 
-    # e2e: the same step through the C ABI with HOST records (pinned), H2D inside the timed
-    # region (gpa_attribute_samples_host pipelines the copies), D2H of the step's results.
+    # e2e: the same steps through the C ABI with HOST records (pinned), H2D inside the timed
+    # region (gpa_attribute_samples_host pipelines the copies), D2H of each batch's results.
     e2e = None
     if not args.no_e2e:
         host = torch.empty((n, 2), dtype=torch.int64, pin_memory=True)
         w.records_host(a, n, out=host.numpy().view(gen.RECORD_DTYPE).reshape(-1))
-        res_h = torch.empty(HU.numel(), dtype=torch.int64, pin_memory=True)
+        res_h = torch.empty(ni * 16 + 16, dtype=torch.int64, pin_memory=True)
         fm_h = torch.empty(met["FUNC"].shape, dtype=torch.float64, pin_memory=True)
 
-        def e2e_step():
-            HU.zero_()
-            gpa.attribute_samples_host(s, host, H, U, stream=stream)
-            combine_analyse()
-            if rank == 0:
-                res_h.copy_(HU, non_blocking=True)
-                fm_h.copy_(met["FUNC"], non_blocking=True)
-                stream.synchronize()
+        def results(x):
+            return [(res_h, x.HU), (fm_h, met["FUNC"])] if rank == 0 else []
 
         e_w = min(args.warmup, 1) if args.e2e_steps else args.warmup
         e_k = args.e2e_steps or args.steps
-        for _ in range(e_w):
-            e2e_step()
+        run_steps(e_w, False, host, results)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         q0 = torch.cuda.Event(enable_timing=True)
         q1 = torch.cuda.Event(enable_timing=True)
-        q0.record(stream)
-        for _ in range(e_k):
-            e2e_step()
-        q1.record(stream)
+        q0.record(A)
+        run_steps(e_k, False, host, results)
+        B.wait_stream(A)
+        q1.record(B)
         torch.cuda.synchronize()
         ems = q0.elapsed_time(q1) / e_k
         if world > 1:
@@ -426,9 +442,9 @@ def run_gpa(args):
             dst.copy_(src, non_blocking=True)
             torch.cuda.synchronize()
             h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            h0.record(stream)
+            h0.record(torch.cuda.current_stream())
             dst.copy_(src, non_blocking=True)
-            h1.record(stream)
+            h1.record(torch.cuda.current_stream())
             torch.cuda.synchronize()
             link = 16 * m / (h0.elapsed_time(h1) / 1e3) / 1e9
             e2e["h2d_link_gbs"] = link
@@ -461,7 +477,7 @@ def run_gpa(args):
     phases = {"attr_ms": attr_ms,
               "scopes_ms_side_stream": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_b1)) / max(1, len(ev_b1)),
               "cct_and_cct_metrics_ms": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_c1)) / max(1, len(ev_c1))}
-    observations = int(HU.sum().item())  # sum of counts of the last step (two's complement = u64 here)
+    observations = int(bufs[(args.steps - 1) % 2].HU.sum().item())  # sum of counts of the last batch (u64 as int64)
     line = {"metric": METRIC, "value": n_all / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
@@ -514,6 +530,8 @@ def main():
     ap.add_argument("--combine", default="scatter", choices=["scatter", "reduce"],
                     help="N > 1: reduce-scatter + per-rank roll-ups (default) or reduce to rank 0")
     ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="enqueue batch i+1's attribution before batch i's analysis (measured slower; DESIGN.md §7)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

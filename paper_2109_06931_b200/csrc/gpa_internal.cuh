@@ -152,6 +152,7 @@ struct AttrPlan {
 };
 struct AttrAcc {
   unsigned long long *acc = nullptr, *Hg = nullptr;
+  unsigned int *ctr = nullptr;  // dynamic tile counter (reset before every launch)
 };
 size_t plan_bytes(const AttrTables &T, int variant);
 cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,

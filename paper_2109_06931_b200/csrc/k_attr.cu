@@ -756,7 +756,8 @@ template <class RG, bool REC>
 __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_probe(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint4 *__restrict__ rec, uint64_t n,
                  unsigned long long *__restrict__ Hg, uint32_t *__restrict__ rec_inst,
-                 const unsigned long long *__restrict__ best, unsigned long long *__restrict__ acc) {
+                 const unsigned long long *__restrict__ best, unsigned long long *__restrict__ acc,
+                 unsigned int *__restrict__ tile_ctr) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane;
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
@@ -764,46 +765,47 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   uint32_t *cnt8 = reinterpret_cast<uint32_t *>(keys + kProbeSets);
   uint64_t *full = reinterpret_cast<uint64_t *>(cnt8 + kProbeWords);
   uint64_t *empty = full + NST;
+  uint32_t *tile_of = reinterpret_cast<uint32_t *>(empty + NST);
   const uint32_t key_s = smem_u32(keys), cnt_s = smem_u32(cnt8), full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t tile_s = smem_u32(tile_of);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t ntiles = (n + S - 1) / S;
+  const uint32_t ntiles = (uint32_t)((n + S - 1) / S);
   for (uint32_t x = threadIdx.x; x < kProbeSets; x += blockDim.x)
     keys[x] = make_uint2(best_gran(best[2 * x]), best_gran(best[2 * x + 1]));
   for (uint32_t x = threadIdx.x; x < kProbeWords; x += blockDim.x) cnt8[x] = 0;
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles, A.stress);
+    if (lane == 0) ring_produce_dyn<RG>(ring, full, empty, tile_of, rec, n, ntiles, tile_ctr, A.stress);
     return;
   }
   uint64_t keep;  // L2 evict-last for Hg / acc (the record stream is evict-first)
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
   const uint32_t ring_s = smem_u32(ring) + (warp * 32 + lane) * 16;
-  const uint32_t ntiles_me = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
-  const bool has_last = ntiles_me && blockIdx.x + (uint64_t)(ntiles_me - 1) * gridDim.x == ntiles - 1;
-  const uint32_t last_m = (uint32_t)(n - (ntiles - 1) * S);  // records in the stream's last tile
-  const uint32_t full_tiles = has_last && last_m < (uint32_t)S ? ntiles_me - 1 : ntiles_me;
+  const uint32_t last_m = (uint32_t)(n - (uint64_t)(ntiles - 1) * S);  // records in the stream's last tile
   uint32_t *ri = nullptr;
-  for (uint32_t it = 0; it < ntiles_me; ++it) {
+  for (uint32_t it = 0;; ++it) {
     const uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait_s(full_s + st * 8, ph);
+    const uint32_t tile = ld_shared_u32(tile_s + st * 4);
+    if (tile >= ntiles) break;
     stress_sleep(A.stress, it, warp);
     uint4 v[R];
 #pragma unroll
     for (int u = 0; u < R; u++) v[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the tile end: masked
     __syncwarp();
     if (lane == 0) ring_release_s(empty_s + st * 8);
-    if (it < full_tiles) {
+    if (tile != ntiles - 1 || last_m == (uint32_t)S) {
 #pragma unroll
       for (int u = 0; u < R; u++) {
-        if (REC) ri = rec_inst + (blockIdx.x + (uint64_t)it * gridDim.x) * S + (u * NC + warp) * 32 + lane;
+        if (REC) ri = rec_inst + (uint64_t)tile * S + (u * NC + warp) * 32 + lane;
         probe_record<REC>(A, v[u], true, key_s, cnt_s, Hg, acc, keep, ri, gmap);
       }
     } else {  // the stream's partial last tile
 #pragma unroll
       for (int u = 0; u < R; u++) {
         const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
-        if (REC) ri = rec_inst + (blockIdx.x + (uint64_t)it * gridDim.x) * S + j;
+        if (REC) ri = rec_inst + (uint64_t)tile * S + j;
         probe_record<REC>(A, v[u], j < last_m, key_s, cnt_s, Hg, acc, keep, ri, gmap);
       }
     }
@@ -870,36 +872,43 @@ template <class RG, int NW, bool REC, int LOOK = 1>
 __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_code32(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint32_t *__restrict__ code,
                   const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ Hg,
-                  uint32_t *__restrict__ rec_inst, unsigned long long *__restrict__ acc, const uint32_t *__restrict__ thr) {
+                  uint32_t *__restrict__ rec_inst, unsigned long long *__restrict__ acc, const uint32_t *__restrict__ thr,
+                  unsigned int *__restrict__ tile_ctr) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = LOOK + 1;
   constexpr uint32_t kLogNW = __builtin_ctz(NW);
   uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NW * 4);
   uint64_t *empty = full + NST;
+  uint32_t *tile_of = reinterpret_cast<uint32_t *>(empty + NST);
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
-  const uint32_t tab_s = smem_u32(tab), full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t tab_s = smem_u32(tab), full_s = smem_u32(full), empty_s = smem_u32(empty), tile_s = smem_u32(tile_of);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t ntiles = (n + S - 1) / S;
+  const uint32_t ntiles = (uint32_t)((n + S - 1) / S);
   const uint32_t nb = min(thr[1], (uint32_t)NW * 4);
   const uint32_t nw = min(nb, (uint32_t)NW);
   for (uint32_t x = threadIdx.x; x < nw; x += blockDim.x) tab[x] = 0;
   ring_init(full, empty, NST, NC);
   __syncthreads();
   if (warp == NC) {
-    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, blockIdx.x, gridDim.x, ntiles, A.stress);
+    if (lane == 0) ring_produce_dyn<RG>(ring, full, empty, tile_of, rec, n, ntiles, tile_ctr, A.stress);
     return;
   }
   uint64_t keep;  // L2 evict-last for the code map and the reductions (the record stream is evict-first)
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
   const uint32_t ring_s = smem_u32(ring) + (warp * 32 + lane) * 16;
-  const uint32_t ntiles_me = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
-  const uint32_t last_m = (uint32_t)(n - (ntiles - 1) * S);
+  const uint32_t last_m = (uint32_t)(n - (uint64_t)(ntiles - 1) * S);
   uint4 v[D][R];
-  uint32_t g[D][R], c[D][R];
-  auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *gg, uint32_t *cc) {
+  uint32_t g[D][R], c[D][R], tid[D];
+  bool ended = false;  // the end marker has been read: fetch no further stage
+  auto fetch = [&](uint32_t it, uint4 *vv, uint32_t *gg, uint32_t *cc, uint32_t &tt) {
     const uint32_t st = it % NST, ph = (it / NST) & 1;
     mbar_wait_s(full_s + st * 8, ph);
+    tt = ld_shared_u32(tile_s + st * 4);
+    if (tt >= ntiles) {
+      ended = true;
+      return;
+    }
     stress_sleep(A.stress, it, warp);
 #pragma unroll
     for (int u = 0; u < R; u++) vv[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the end: masked
@@ -913,22 +922,24 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     }
   };
 #pragma unroll
+  for (int q = 0; q < D; q++) tid[q] = ntiles;
+#pragma unroll
   for (int q = 0; q < LOOK; q++)
-    if ((uint32_t)q < ntiles_me) fetch(q, v[q], g[q], c[q]);
+    if (!ended) fetch(q, v[q], g[q], c[q], tid[q]);
   for (uint32_t it0 = 0;; it0 += D) {
 #pragma unroll
     for (int q = 0; q < D; q++) {
       const uint32_t it = it0 + q;
-      if (it >= ntiles_me) goto done;
-      if (it + LOOK < ntiles_me) fetch(it + LOOK, v[(q + LOOK) % D], g[(q + LOOK) % D], c[(q + LOOK) % D]);
-      const bool last = blockIdx.x + (uint64_t)it * gridDim.x == ntiles - 1;
+      const uint32_t tile = tid[q];
+      if (tile >= ntiles) goto done;
+      if (!ended) fetch(it + LOOK, v[(q + LOOK) % D], g[(q + LOOK) % D], c[(q + LOOK) % D], tid[(q + LOOK) % D]);
+      const bool last = tile == ntiles - 1;
 #pragma unroll
       for (int u = 0; u < R; u++) {
         const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
         const bool live = !last || j < last_m;
         const uint32_t cnt = v[q][u].z, st16 = v[q][u].w & 0xFFFFu, cd = c[q][u], gq = g[q][u];
-        if (REC && live)
-          rec_inst[(blockIdx.x + (uint64_t)it * gridDim.x) * S + j] = gq == A.n_gran ? NONE : __ldg(gmap + gq);
+        if (REC && live) rec_inst[(uint64_t)tile * S + j] = gq == A.n_gran ? NONE : __ldg(gmap + gq);
         const uint32_t mask = cd & 0xFFFu;
         const bool hot = live && st16 < (uint32_t)GPA_VALID_SLOTS && ((mask >> st16) & 1u) && cnt < 256u;
         const uint32_t idx = (cd >> 12) + __popc(mask & ((1u << st16) - 1u));
@@ -942,6 +953,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
           red_add_u64(Hg + ((uint64_t)gq * GPA_SLOTS + slot), cnt);
         }
       }
+      tid[q] = ntiles;  // consumed
     }
   }
 done:
@@ -1038,30 +1050,35 @@ cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint6
 cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, cudaStream_t st) {
   const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
   const size_t nh = (size_t)(p.n_gran + 1) * 128;
-  cudaError_t e = pool_alloc((void **)&a->acc, na + nh, st);
+  cudaError_t e = pool_alloc((void **)&a->acc, na + nh + 16, st);
   if (e != cudaSuccess) return e;
   a->Hg = a->acc + na / 8;
+  a->ctr = reinterpret_cast<unsigned int *>(a->Hg + nh / 8);
   return cudaMemsetAsync(a->acc, 0, na + nh, st);
 }
 
 cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
                      uint32_t *ri, int sm_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  cudaError_t e0 = cudaMemsetAsync(a.ctr, 0, sizeof(unsigned int), st);  // the dynamic tile counter of this launch
+  if (e0 != cudaSuccess) return e0;
   const ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift,
                     (uint32_t)T.n_gran, (uint32_t)g_ring_stress.load(std::memory_order_relaxed)};
   cudaError_t e;
   if (p.variant == 7) {
     using RG = RingProbe;
     auto kern = ri ? k_attr_probe<RG, true> : k_attr_probe<RG, false>;
-    const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8;
+    const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
-    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, p.best, a.acc);
+    // dynamic tile order for the probe kernel (C4: 2.82 -> 2.71 ms)
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, p.best, a.acc, a.ctr);
   } else {
     using RG = RingCode;
     auto kern = ri ? k_attr_code32<RG, kHotBins, true, GPA_CODE_LOOK> : k_attr_code32<RG, kHotBins, false, GPA_CODE_LOOK>;
-    const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8;
+    const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
-    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, p.code, rec, n, a.Hg, ri, a.acc, p.thr);
+    // static tile order for the code-map kernel (C5: 12.54 ms vs 13.16 ms with the dynamic order)
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, p.code, rec, n, a.Hg, ri, a.acc, p.thr, nullptr);
   }
   count_launches(1);
   return cudaGetLastError();

@@ -171,6 +171,38 @@ __device__ __forceinline__ void ring_produce(uint4 *ring, uint64_t *full, uint64
   }
 }
 
+// Producer with the tile index published in tile_of[stage] before arming the stage (the arrive
+// releases it; consumers read it after their acquiring wait).  Dynamic order: the next tile of the
+// whole stream comes from a global counter (atomicAdd), so CTAs that start late or run slowly take
+// fewer tiles.  The end is a stage armed without a copy whose tile index is >= ntiles.
+template <class RG>
+__device__ __forceinline__ void ring_produce_dyn(uint4 *ring, uint64_t *full, uint64_t *empty, uint32_t *tile_of,
+                                                 const uint4 *rec, uint64_t n, uint32_t ntiles, unsigned int *ctr,
+                                                 uint32_t stress = 0) {
+  constexpr int S = RG::kTile, NST = RG::kStages;
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  // ctr == nullptr: static order (tile blockIdx.x + it * gridDim.x), else the index of the
+  // following tile is fetched one stage ahead, so the atomic's round trip overlaps the wait
+  uint32_t next = ctr ? atomicAdd(ctr, 1u) : blockIdx.x;
+  for (uint32_t it = 0;; ++it) {
+    uint32_t st = it % NST, ph = (it / NST) & 1;
+    const uint32_t tile = next;
+    if (tile < ntiles) next = ctr ? atomicAdd(ctr, 1u) : tile + gridDim.x;
+    if (it >= (uint32_t)NST) mbar_wait(empty + st, ph ^ 1);
+    stress_sleep(stress, tile, 0xFFFFu);
+    tile_of[st] = tile;
+    if (tile >= ntiles) {
+      mbar_arrive(full + st);  // end marker: no bytes
+      return;
+    }
+    uint64_t left = n - (uint64_t)tile * S;
+    uint32_t bytes = (uint32_t)((left < (uint64_t)S ? left : (uint64_t)S) * 16);
+    mbar_arrive_expect_tx(full + st, bytes);
+    bulk_g2s(ring + (size_t)st * S, rec + (uint64_t)tile * S, bytes, full + st, policy);
+  }
+}
+
 __device__ __forceinline__ void ring_init(uint64_t *full, uint64_t *empty, int nst, uint32_t consumers) {
   if (threadIdx.x == 0) {
     for (int q = 0; q < nst; q++) {
