@@ -868,7 +868,7 @@ __global__ void k_codemap32(const uint32_t *__restrict__ gmap, uint64_t n_gran, 
   }
 }
 
-template <class RG, int NW, bool REC, int LOOK = 1>
+template <class RG, int NW, int PACK, bool REC, int LOOK = 1>
 __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_code32(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint32_t *__restrict__ code,
                   const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ Hg,
@@ -876,7 +876,10 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
                   unsigned int *__restrict__ tile_ctr) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = LOOK + 1;
-  constexpr uint32_t kLogNW = __builtin_ctz(NW);
+  // PACK 0: bin idx in word idx % NW, byte idx / NW (NW a power of two: the consecutive bins of one
+  // instruction fall in different banks); PACK 1: word idx / 4, byte idx % 4 (any NW)
+  static_assert(PACK == 1 || (NW & (NW - 1)) == 0, "interleaved bins need a power-of-two word count");
+  constexpr uint32_t kLogNW = PACK ? 0 : __builtin_ctz(NW);
   uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NW * 4);
   uint64_t *empty = full + NST;
@@ -886,7 +889,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t ntiles = (uint32_t)((n + S - 1) / S);
   const uint32_t nb = min(thr[1], (uint32_t)NW * 4);
-  const uint32_t nw = min(nb, (uint32_t)NW);
+  const uint32_t nw = PACK ? min((nb + 3) / 4, (uint32_t)NW) : min(nb, (uint32_t)NW);
   for (uint32_t x = threadIdx.x; x < nw; x += blockDim.x) tab[x] = 0;
   ring_init(full, empty, NST, NC);
   __syncthreads();
@@ -943,11 +946,15 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
         const uint32_t mask = cd & 0xFFFu;
         const bool hot = live && st16 < (uint32_t)GPA_VALID_SLOTS && ((mask >> st16) & 1u) && cnt < 256u;
         const uint32_t idx = (cd >> 12) + __popc(mask & ((1u << st16) - 1u));
-        const uint32_t sh = (idx >> kLogNW) << 3;
+        const uint32_t word = PACK ? idx >> 2 : idx & (NW - 1);
+        const uint32_t sh = PACK ? (idx & 3u) << 3 : (idx >> kLogNW) << 3;
         const uint32_t delta = cnt << sh;
         if (hot) {
-          const uint32_t old = atoms_add(tab_s + (idx & (NW - 1)) * 4, delta);
-          if (((old >> sh) & 0xFFu) + cnt > 255u) repay_carries<8, NW>(acc, idx & (NW - 1), old, delta, keep);
+          const uint32_t old = atoms_add(tab_s + word * 4, delta);
+          if (((old >> sh) & 0xFFu) + cnt > 255u) {
+            if (PACK) repay_carries<8, 1>(acc + 4 * word, 0, old, delta, keep);  // bins 4 word .. 4 word + 3
+            else repay_carries<8, NW>(acc, word, old, delta, keep);
+          }
         } else if (live) {
           const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
           red_add_u64(Hg + ((uint64_t)gq * GPA_SLOTS + slot), cnt);
@@ -963,13 +970,20 @@ done:
 #pragma unroll
     for (int p = 0; p < 4; p++) {
       const uint32_t val = (word >> (8 * p)) & 0xFFu;
-      if (val && (uint32_t)p * NW + x < nb) red_add_u64_keep(acc + (uint32_t)p * NW + x, val, keep);  // coalesced
+      const uint32_t bin = PACK ? 4 * x + p : (uint32_t)p * NW + x;
+      if (val && bin < nb) red_add_u64_keep(acc + bin, val, keep);
     }
   }
 }
 
 #ifndef GPA_CODE_NC
 #define GPA_CODE_NC 31
+#endif
+#ifndef GPA_CODE_NW
+#define GPA_CODE_NW 32768
+#endif
+#ifndef GPA_CODE_PACK
+#define GPA_CODE_PACK 0
 #endif
 #ifndef GPA_CODE_R
 #define GPA_CODE_R 3
@@ -987,7 +1001,7 @@ using RingCode = Ring<GPA_CODE_NC, GPA_CODE_R, GPA_CODE_NST>;
 // ---- attribution plans: the pre-pass of K_attr_probe / K_attr_code32 (which granules / bins live
 // in shared memory), built from a sample of records and reusable for any number of calls and
 // chunks: the result is exact for every plan, only the speed depends on how well it fits ------------
-constexpr uint32_t kCodeK = (uint32_t)kHotBins * 4;  // K_attr_code32 byte bins
+constexpr uint32_t kCodeK = (uint32_t)GPA_CODE_NW * 4;  // K_attr_code32 byte bins
 
 // records sampled to build a plan: n/256, at least 2^18, at most 2^21 for the probe table (7) and
 // 2^22 for the 131 072 byte bins of 8, whose ranking needs the finer counts (C5: 12.77 -> 12.7 ms;
@@ -1074,8 +1088,9 @@ cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, c
     kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, p.best, a.acc, a.ctr);
   } else {
     using RG = RingCode;
-    auto kern = ri ? k_attr_code32<RG, kHotBins, true, GPA_CODE_LOOK> : k_attr_code32<RG, kHotBins, false, GPA_CODE_LOOK>;
-    const size_t smem = RG::kBytes + (size_t)kHotBins * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
+    auto kern = ri ? k_attr_code32<RG, GPA_CODE_NW, GPA_CODE_PACK, true, GPA_CODE_LOOK>
+                   : k_attr_code32<RG, GPA_CODE_NW, GPA_CODE_PACK, false, GPA_CODE_LOOK>;
+    const size_t smem = RG::kBytes + (size_t)GPA_CODE_NW * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
     // static tile order for the code-map kernel (C5: 12.54 ms vs 13.16 ms with the dynamic order)
     kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, p.code, rec, n, a.Hg, ri, a.acc, p.thr, nullptr);

@@ -60,10 +60,18 @@ def run(name):
         HU.zero_()
         gpa.attribute_samples(s, rec, H, U)
 
+    plan = gpa.AttrPlan(s, rec, min(n, 1 << 22)) if n >= 4096 else None
+
+    def attr_planned():  # a plan built once from the first 2^22 records, reused (gpa_attr_plan)
+        HU.zero_()
+        if plan is not None and plan.variant:
+            plan.attribute(rec, H, U)
+        else:
+            gpa.attribute_samples(s, rec, H, U)
+
     def step():
         attr()
-        for sc in SCOPES:
-            gpa.derive_metrics(s, sc, H, metrics=met[sc])
+        gpa.derive_scopes(s, H, {sc: {"metrics": met[sc]} for sc in SCOPES})
         c = gpa.reconstruct_cct(s, H)
         cm = torch.empty((max(c.n, 1), 33), dtype=torch.float64, device="cuda")
         gpa.derive_metrics(s, "CCT_EXCL", cct=c, metrics=cm)
@@ -72,6 +80,7 @@ def run(name):
         c.free()
 
     t_attr = med(attr)
+    t_plan = med(attr_planned)
     t_step = med(step)
     del rec
     torch.cuda.empty_cache()
@@ -93,18 +102,18 @@ def run(name):
     oracle.derive_f64(R["excl"])
     oracle.derive_f64(R["incl"])
     t4 = time.perf_counter()
-    return dict(name=name, n=n, t_attr=t_attr, gbs=16 * n / t_attr / 1e6, t_step=t_step,
+    return dict(name=name, n=n, t_attr=t_attr, gbs=16 * n / t_attr / 1e6, t_step=t_step, t_plan=t_plan,
                 o1=m / (t1 - t0), oc=m / (t2 - t1), cores=cores, o_rest=(t4 - t3) * 1e3, ctx=R["n"])
 
 
 if __name__ == "__main__":
     names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C1", "C2", "C3", "C4", "C5"]
     print(f"peak {PEAK} GB/s")
-    print("| config | records | K_attr ms | GB/s (frac) | step ms | samples/s (step) | oracle D1 1 thread | "
-          "oracle D1 all threads | oracle rest (1 thread) | CCT contexts |")
-    print("|---|---|---|---|---|---|---|---|---|---|")
+    print("| config | records | K_attr ms | GB/s (frac) | K_attr ms, reused plan (frac) | step ms | samples/s (step) | "
+          "oracle D1 1 thread | oracle D1 all threads | oracle rest (1 thread) | CCT contexts |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|")
     for nm in names:
         d = run(nm)
         print(f"| {d['name']} | {d['n']:.3g} | {d['t_attr']:.3f} | {d['gbs']:.0f} ({d['gbs'] / PEAK:.3f}) | "
-              f"{d['t_step']:.3f} | {d['n'] / d['t_step'] * 1e3:.3g} | {d['o1']:.3g}/s | {d['oc']:.3g}/s "
+              f"{d['t_plan']:.3f} ({16 * d['n'] / d['t_plan'] / 1e6 / PEAK:.3f}) | {d['t_step']:.3f} | {d['n'] / d['t_step'] * 1e3:.3g} | {d['o1']:.3g}/s | {d['oc']:.3g}/s "
               f"({d['cores']}) | {d['o_rest']:.1f} ms | {d['ctx']} |", flush=True)
