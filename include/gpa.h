@@ -410,8 +410,9 @@ GPA_API gpa_status gpa_attribute_samples_planned(gpa_structure s, gpa_attr_plan 
 GPA_API void gpa_attr_plan_free(gpa_attr_plan p);
 
 /* ---- a-4 / a-5 across GPUs: statistics over function-aligned instruction ranges -------------
- * The paper generates statistics "in parallel" after the profiles are aggregated by a second
- * reduction (reading R29 in DESIGN.md): every scope row (LINE, LOOP, INLINE, FUNC)
+ * The paper reads measurements "in parallel, propagating values up the calling context tree"
+ * and aggregates accumulators "by a second reduction operation" (reading R29 in
+ * DESIGN.md): every scope row (LINE, LOOP, INLINE, FUNC)
  * lies inside one function, so when each function's instructions are contiguous, rank r of N can
  * receive the reduced histogram rows [b_r, b_{r+1}) of a function-aligned split (one
  * reduce-scatter instead of a reduce to one rank) and derive the rows of its own functions.

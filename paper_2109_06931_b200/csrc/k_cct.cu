@@ -491,7 +491,7 @@ __host__ __device__ inline size_t small2_smem(uint32_t n_func, uint32_t m) {
 
 __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_func, uint32_t m, uint32_t n_dag,
                                                      const uint32_t *din_ptr, const uint8_t *dact, uint32_t *lev_out,
-                                                     unsigned long long *built, uint32_t stage) {
+                                                     unsigned long long *built, uint32_t stage, uint32_t par) {
   extern __shared__ __align__(16) uint8_t sm2[];
   __shared__ uint32_t lev[kSmallLevels + 1];
   double *eratio = reinterpret_cast<double *>(sm2);
@@ -532,6 +532,32 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
     for (uint32_t q = fout_ptr[g]; q < fout_ptr[g + 1]; q++) c += ekind[q] != kSkip;
     nzc[g] = (uint16_t)c;
   }
+  // par = 1: children are written thread-per-child (a level's contexts keep their first child's
+  // index in loff; a child finds its parent by binary search and its call site in wq, the
+  // weighted external calls of every function compacted in call-instruction order from wptr)
+  uint32_t *wptr = nullptr, *wq = nullptr, *loff = nullptr;
+  if (par) {
+    uint32_t *pp = reinterpret_cast<uint32_t *>(sm2 + par);
+    wptr = pp;
+    wq = wptr + n_func + 1;
+    loff = wq + m;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t base = 0; base < n_func; base += nt) {
+      const uint32_t g = base + t;
+      uint32_t tot;
+      const uint32_t o = run + block_exscan(g < n_func ? (uint32_t)nzc[g] : 0u, &tot);
+      if (g < n_func) wptr[g] = o;
+      run += tot;
+    }
+    if (t == 0) wptr[n_func] = run;
+    __syncthreads();
+    for (uint32_t g = t; g < n_func; g += nt) {
+      uint32_t k = wptr[g];
+      for (uint32_t q = fout_ptr[g]; q < fout_ptr[g + 1]; q++)
+        if (ekind[q] != kSkip) wq[k++] = q;
+    }
+  }
   uint32_t running = 0;
   for (uint32_t base = 0; base < n_dag; base += nt) {  // roots in DAG order (R15)
     uint32_t X = base + t;
@@ -560,6 +586,66 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
     if (t == 0) lev[L + 1] = b;
     L++;
     uint32_t next = b;
+    if (par && b - a <= kSmallCap) {
+      // phase A: child counts -> offsets (BFS numbering, R17) per context of the level
+      for (uint32_t base = a; base < b; base += nt) {
+        const uint32_t c = base + t;
+        uint32_t cnt = 0;
+        if (c < b) {
+          const uint8_t k = ckind[c - a];
+          const uint32_t nd = cnode[c - a];
+          cnt = k == GPA_CTX_SCC ? dmem_ptr[nd + 1] - dmem_ptr[nd]
+                                 : (uint32_t)nzc[k == GPA_CTX_SCC_MEMBER ? nd : dmem[dmem_ptr[nd]]];
+        }
+        uint32_t tot;
+        const uint32_t o = next + block_exscan(cnt, &tot);
+        if (c < b) {
+          loff[c - a] = o;
+          A.first_child[c] = o;
+          A.n_children[c] = cnt;
+        }
+        next += tot;
+      }
+      __syncthreads();
+      // phase B: one thread per child
+      const uint32_t w = b - a;
+      for (uint32_t d = b + t; d < next; d += nt) {
+        uint32_t lo = 0, hi = w;  // last context i with loff[i] <= d
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (loff[mid] <= d) lo = mid + 1; else hi = mid;
+        }
+        const uint32_t i = lo - 1, c = a + i, j = d - loff[i];
+        const uint8_t k = ckind[i];
+        const uint32_t nd = cnode[i];
+        const double f = cfrac[i];
+        uint8_t ck;
+        uint32_t cn;
+        double cf;
+        A.parent[d] = c;
+        if (k == GPA_CTX_SCC) {  // members in ascending function id (R14)
+          ck = GPA_CTX_SCC_MEMBER;
+          cn = dmem[dmem_ptr[nd] + j];
+          cf = f;
+          A.site[d] = NONE;
+        } else {  // the j-th weighted external call in call-instruction order (R15, R17)
+          const uint32_t g = k == GPA_CTX_SCC_MEMBER ? nd : dmem[dmem_ptr[nd]];
+          const uint32_t q = wq[wptr[g] + j];
+          ck = ekind[q];
+          cn = enode[q];
+          cf = __dmul_rn(f, eratio[q]);
+          A.site[d] = esite[q];
+        }
+        A.node[d] = cn;
+        A.kind[d] = ck;
+        A.frac[d] = cf;
+        if (d - b < kSmallCap) {
+          nkind[d - b] = ck;
+          nnode[d - b] = cn;
+          nfrac[d - b] = cf;
+        }
+      }
+    } else
     for (uint32_t base = a; base < b; base += nt) {
       const uint32_t c = base + t;
       uint8_t k = 0;
@@ -974,11 +1060,16 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
   const uint32_t stage = sm2s <= 200 * 1024 ? 1u : 0u;
   cudaError_t e = cudaSuccess;
   if (sm2 <= 200 * 1024 && s->info.n_func < 65536) {
-    const size_t smx = stage ? sm2s : sm2;
+    size_t smx = stage ? sm2s : sm2;
+    // thread-per-child level writes when their tables fit as well (wptr, wq, loff)
+    const size_t par_at = (smx + 15) & ~(size_t)15;
+    const size_t par_bytes = 4ull * (s->info.n_func + 1 + m_ext + kSmallCap);
+    const uint32_t par = par_at + par_bytes <= 227 * 1024 - 8 * 1024 ? (uint32_t)par_at : 0u;
+    if (par) smx = par_at + par_bytes;
     e = cudaFuncSetAttribute(k_cct_small2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smx);
     if (e != cudaSuccess) return e;
     k_cct_small2<<<1, 1024, smx, st>>>(A, s->info.n_func, m_ext, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev,
-                                       d_built, stage);
+                                       d_built, stage, par);
   } else {
     k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built);
   }
