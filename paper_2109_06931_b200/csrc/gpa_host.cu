@@ -886,12 +886,15 @@ static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d
       CC(cudaMemcpyAsync(c->S_f, d_func_hist, sizeof(uint64_t) * SLOTS * I.n_func, cudaMemcpyDeviceToDevice, st));
   }
   unsigned long long h_cnt[2] = {0, 0};
-  if (max_contexts && cct_small_ok(s, I.cct_path_bound)) {
+  const bool small_static = cct_small_ok(s, I.cct_path_bound);
+  if (max_contexts && (small_static || cct_small_ok(s, kSmallContexts))) {
     // Small static bound: build straight into bound-sized arrays with one CTA and read the
-    // size back once at the end (no separate path count, one host synchronization).
+    // size back once at the end (no separate path count, one host synchronization).  Larger
+    // static bounds (C3: 4.19 M paths, ~37 k sampled contexts) try the same into kSmallContexts
+    // slots first and fall back to the counted build only if the tree does not fit.
     CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, mode == GPA_WEIGHTS_EXACT,
                             false, st));
-    const uint64_t nb = I.cct_path_bound;
+    const uint64_t nb = small_static ? I.cct_path_bound : kSmallContexts;
     c->n = nb;
     CC(calloc_dev(c, &c->parent, nb));
     CC(calloc_dev(c, &c->site, nb));
@@ -908,20 +911,30 @@ static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d
     CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
     CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CC(cudaStreamSynchronize(st));
-    if (h_cnt[1] > nb) {
+    if (h_cnt[1] > nb && small_static) {
       free_cct(c);
       return fail(GPA_ERR_INTERNAL, "tree of %llu contexts exceeds the static bound %llu", h_cnt[1],
                   (unsigned long long)nb);
     }
-    c->n = h_cnt[1];
-    *n_contexts = c->n;
-    if (c->n > max_contexts) {
-      free_cct(c);
-      return fail(GPA_ERR_CAPACITY, "%llu contexts > max_contexts %llu", (unsigned long long)*n_contexts,
-                  (unsigned long long)max_contexts);
+    if (h_cnt[1] <= nb) {
+      c->n = h_cnt[1];
+      *n_contexts = c->n;
+      if (c->n > max_contexts) {
+        free_cct(c);
+        return fail(GPA_ERR_CAPACITY, "%llu contexts > max_contexts %llu", (unsigned long long)*n_contexts,
+                    (unsigned long long)max_contexts);
+      }
+      *out = c;
+      return GPA_OK;
     }
-    *out = c;
-    return GPA_OK;
+    // the optimistic build overflowed: the counted build below.  Step 2 rewrote w in place and
+    // the activity it derived is not recoverable from w alone, so w is reset to the Step-1
+    // weights first (the slots above stay allocated until gpa_free_cct)
+    c->n = 0;
+    c->d_lev = nullptr; c->lev_fmt = 0; c->lev_len = 0;
+    if (from_hist) CC(launch_cct_weights(s, d_inst_hist, c->w, st));
+    else if (I.n_call)
+      CC(cudaMemcpyAsync(c->w, d_call_weight, sizeof(uint64_t) * I.n_call, cudaMemcpyDeviceToDevice, st));
   }
   // Step 2 + guard (R12) + W + context count (path DP over the DAG)
   CC(launch_cct_propagate(s, c->S_f, c->w, c->func_active, c->dag_active, c->W, d_cnt, mode == GPA_WEIGHTS_EXACT,

@@ -249,7 +249,9 @@ cudaError_t launch_cct_level(const gpa_structure_s *s, gpa_cct_s *c, uint64_t a,
                              uint32_t *d_tmp, uint32_t *d_blocksum, unsigned long long *d_next,
                              cudaStream_t st);
 cudaError_t launch_cct_excl(const gpa_structure_s *s, gpa_cct_s *c, cudaStream_t st);
-// whole Step 4 in one CTA when cct_small_ok (writes the built context count to *d_built)
+// whole Step 4 in one CTA when cct_small_ok (writes the built context count to *d_built; ~0 when
+// the tree exceeds the c->n allocated slots or the level table)
+constexpr uint64_t kSmallContexts = 1ull << 16;
 bool cct_small_ok(const gpa_structure_s *s, uint64_t n);
 // whole Step 4 in one cooperative grid launch (large trees); d_bsum >= 2*SMs entries
 cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_tmp, uint32_t *d_bsum, uint32_t *d_lev,

@@ -432,7 +432,7 @@ __device__ __forceinline__ void write_children(const LevelArgs &A, uint64_t c, u
 
 __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag, const uint32_t *din_ptr,
                                                     const uint8_t *dact, uint32_t *lev_out,
-                                                    unsigned long long *built) {
+                                                    unsigned long long *built, uint64_t cap) {
   __shared__ uint32_t lev[kSmallLevels + 1];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   uint32_t running = 0;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag,
     uint32_t flag = X < n_dag && din_ptr[X] == din_ptr[X + 1] && dact[X];
     uint32_t tot;
     uint32_t pos = running + block_exscan(flag, &tot);
-    if (flag) {
+    if (flag && pos < cap) {
       A.parent[pos] = NONE;
       A.site[pos] = NONE;
       A.node[pos] = X;
@@ -462,17 +462,19 @@ __global__ void __launch_bounds__(1024) k_cct_small(LevelArgs A, uint32_t n_dag,
       uint32_t cnt = c < b ? child_count(A, c) : 0;
       uint32_t tot;
       uint32_t off = block_exscan(cnt, &tot);
-      if (c < b) write_children(A, c, next + off);
+      if (c < b && next + off + cnt <= cap) write_children(A, c, next + off);
       next += tot;
     }
     __syncthreads();
     a = b;
     b = next;
+    if (b > cap) break;  // more contexts than the arrays hold (the host falls back)
   }
   __syncthreads();
   for (uint32_t l = t; l <= L; l += nt) lev_out[l + 1] = lev[l];  // lev_out[0] = number of levels
   if (t == 0) lev_out[0] = L;
-  if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
+  if (t == 0) built[0] = (b > a || b > cap) ? ~0ull : b;  // ~0: level or capacity overflow (host falls back)
+  if ((b > a || b > cap) && t == 0) lev_out[0] = 0;        // nothing for the fold to walk
 }
 
 // k_cct_small with its working set in shared memory (used when it fits): per external call
@@ -491,7 +493,8 @@ __host__ __device__ inline size_t small2_smem(uint32_t n_func, uint32_t m) {
 
 __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_func, uint32_t m, uint32_t n_dag,
                                                      const uint32_t *din_ptr, const uint8_t *dact, uint32_t *lev_out,
-                                                     unsigned long long *built, uint32_t stage, uint32_t par) {
+                                                     unsigned long long *built, uint32_t stage, uint32_t par,
+                                                     uint64_t cap) {
   extern __shared__ __align__(16) uint8_t sm2[];
   __shared__ uint32_t lev[kSmallLevels + 1];
   double *eratio = reinterpret_cast<double *>(sm2);
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
     uint32_t flag = X < n_dag && din_ptr[X] == din_ptr[X + 1] && dact[X];
     uint32_t tot;
     uint32_t pos = running + block_exscan(flag, &tot);
-    if (flag) {
+    if (flag && pos < cap) {
       const uint8_t k = A.nontriv[X] ? GPA_CTX_SCC : GPA_CTX_FUNC;
       A.parent[pos] = NONE;
       A.site[pos] = NONE;
@@ -582,7 +585,8 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
   __syncthreads();
   uint32_t a = 0, b = running, L = 0;
   if (t == 0) lev[0] = 0;
-  while (b > a && L < kSmallLevels) {
+  bool over = b > cap;  // more contexts than the arrays hold: stop, the host falls back
+  while (!over && b > a && L < kSmallLevels) {
     if (t == 0) lev[L + 1] = b;
     L++;
     uint32_t next = b;
@@ -607,6 +611,10 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
         next += tot;
       }
       __syncthreads();
+      if (next > cap) {
+        over = true;
+        break;
+      }
       // phase B: one thread per child
       const uint32_t w = b - a;
       for (uint32_t d = b + t; d < next; d += nt) {
@@ -670,7 +678,7 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
       }
       uint32_t tot;
       const uint32_t o = next + block_exscan(cnt, &tot);
-      if (c < b) {
+      if (c < b && o + cnt <= cap) {
         if (k == GPA_CTX_SCC) {  // members in ascending function id (R14)
           uint32_t d = o;
           for (uint32_t q = dmem_ptr[nd]; q < dmem_ptr[nd + 1]; q++, d++) {
@@ -718,11 +726,12 @@ __global__ void __launch_bounds__(1024) k_cct_small2(LevelArgs A, uint32_t n_fun
     }
     a = b;
     b = next;
+    over = over || b > cap;
   }
   __syncthreads();
   for (uint32_t l = t; l <= L; l += nt) lev_out[l + 1] = lev[l];  // lev_out[0] = number of levels
-  if (t == 0) lev_out[0] = L;
-  if (t == 0) built[0] = (b > a) ? ~0ull : b;  // ~0: level overflow (host falls back)
+  if (t == 0) lev_out[0] = over ? 0 : L;                            // overflow: nothing to fold
+  if (t == 0) built[0] = (over || b > a) ? ~0ull : b;  // ~0: level or capacity overflow (host falls back)
 }
 
 // Exact counts from instrumentation: block b's execution count goes to slot 0 of
@@ -1069,9 +1078,9 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
     e = cudaFuncSetAttribute(k_cct_small2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smx);
     if (e != cudaSuccess) return e;
     k_cct_small2<<<1, 1024, smx, st>>>(A, s->info.n_func, m_ext, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev,
-                                       d_built, stage, par);
+                                       d_built, stage, par, c->n);
   } else {
-    k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built);
+    k_cct_small<<<1, 1024, 0, st>>>(A, s->info.n_dag, s->d_din_ptr, c->dag_active, d_lev, d_built, c->n);
   }
   count_launches(1);
   e = cudaGetLastError();
