@@ -29,10 +29,19 @@ void gpa::count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order
 static std::mutex g_pool_mu;
 static cudaMemPool_t g_pools[64] = {};
 
+// bytes the library's memory pool keeps reserved (environment GPA_POOL_KEEP_BYTES, default 8 GiB)
+static uint64_t pool_keep() {
+  static const uint64_t keep = [] {
+    const char *e = getenv("GPA_POOL_KEEP_BYTES");
+    return e ? strtoull(e, nullptr, 10) : (8ull << 30);
+  }();
+  return keep;
+}
+
 // return reserved pool memory above the release threshold to the driver (after large frees)
 static void pool_trim(int dev) {
   std::lock_guard<std::mutex> lock(g_pool_mu);
-  if (dev >= 0 && dev < 64 && g_pools[dev]) cudaMemPoolTrimTo(g_pools[dev], 1ull << 30);
+  if (dev >= 0 && dev < 64 && g_pools[dev]) cudaMemPoolTrimTo(g_pools[dev], pool_keep());
 }
 
 cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
@@ -54,11 +63,12 @@ cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
       props.location.id = dev;
       e = cudaMemPoolCreate(&pools[dev], &props);
       if (e != cudaSuccess) return e;
-      // keep up to 1 GiB reserved between calls (the per-call scratch of a C5 attribution is
-      // ~0.1 GB, so repeated calls never go back to the driver); memory above that is returned to
-      // the driver at synchronization points, so a large one-off (an exact-mode tree, a sparse
-      // cube) does not stay reserved (gpa_free_cct / gpa_free_sparse also trim)
-      uint64_t keep = 1ull << 30;
+      // keep up to pool_keep() bytes reserved between calls (default 8 GiB: the scratch of the
+      // largest calls measured — f4 blame over 31 M events, a 4.19 M-context exact tree — so
+      // repeated calls never go back to the driver; with 1 GiB f4 took 19.5 ms instead of 2.3);
+      // memory above it is returned to the driver at synchronization points and after
+      // gpa_free_cct / gpa_free_sparse, so a larger one-off does not stay reserved
+      uint64_t keep = pool_keep();
       cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }

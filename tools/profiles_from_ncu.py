@@ -83,5 +83,5 @@ if __name__ == "__main__":
     P = os.path.join(ROOT, "profiles")
     tot, s = launches(lcsv, os.path.join(P, f"{rnd}_launches_{cfg}.md"))
     kname = sys.argv[6] if len(sys.argv) > 6 else "k_attr_bins"
-    js = full(rep, os.path.join(P, f"{rnd}_{kname}_{cfg}.md"), os.path.join(P, f"k_attr_traffic_{cfg}.json"), algo)
+    js = full(rep, os.path.join(P, f"{rnd}_{kname}_{cfg}.md"), os.path.join(P, f"{rnd}_{kname}_{cfg}_traffic.json"), algo)
     print(json.dumps(js))
