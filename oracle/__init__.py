@@ -277,6 +277,56 @@ def cct_profiles(R: dict, Hp) -> tuple:
     return E, I
 
 
+def cct_per_profile(st: dict, Hp_inst, exact: bool = False) -> dict:
+    """D12 (reading R30): an approximate CCT for each profile ("for each GPU kernel invocation",
+    P:872) from that profile's own instruction histogram Hp_inst[p] (D3-D6 per profile), then the
+    trees unified by call path ("unify the tree of call paths from each profile into a
+    single tree"): a unified context is a path present in at least one profile's tree; roots in
+    DAG order, the children of a context in the order its trees give them (SCC members by
+    function id, calls by call instruction), numbered breadth first.  Per profile p and unified
+    context u: frac[u, p], excl[u, p, :], incl[u, p, :] are p's own tree values, 0 where p's tree
+    lacks the path.  Plain Python over the per-profile trees (small inputs)."""
+    Hp_inst = np.ascontiguousarray(Hp_inst, np.uint64)
+    P = Hp_inst.shape[0]
+    trees = [cct(st, Hp_inst[p], exact=exact) for p in range(P)]
+    ci = np.asarray(st["call_inst"], np.int64)
+    KIND_SCC = 1
+    # unified context: (kind, node, parent uid, site, {p: context id in p's tree})
+    roots = {}
+    for p, R in enumerate(trees):
+        for c in range(R["n"]):
+            if R["parent"][c] == NONE:
+                roots.setdefault(int(R["node"][c]), (int(R["kind"][c]), {}))[1][p] = c
+    U = [(k, node, NONE, NONE, mem) for node, (k, mem) in sorted(roots.items())]
+    i = 0
+    while i < len(U):
+        kind, node, _, _, mem = U[i]
+        kids = {}
+        for p, c in mem.items():
+            R = trees[p]
+            for d in range(int(R["first_child"][c]), int(R["first_child"][c] + R["n_children"][c])):
+                site = int(R["site"][d])
+                key = int(R["node"][d]) if kind == KIND_SCC else int(ci[site])  # members / call sites
+                ent = kids.setdefault(key, [int(R["kind"][d]), int(R["node"][d]), site, {}])
+                ent[3][p] = d
+        for key in sorted(kids):
+            k, nd, site, m = kids[key]
+            U.append((k, nd, i, site, m))
+        i += 1
+    n = len(U)
+    out = dict(n=n, n_profiles=P,
+               kind=np.array([u[0] for u in U], np.uint8), node=np.array([u[1] for u in U], np.uint32),
+               parent=np.array([u[2] for u in U], np.uint32), site=np.array([u[3] for u in U], np.uint32),
+               frac=np.zeros((n, P), np.float64), excl=np.zeros((n, P, SLOTS), np.float64),
+               incl=np.zeros((n, P, SLOTS), np.float64), trees=trees)
+    for u, (_, _, _, _, mem) in enumerate(U):
+        for p, c in mem.items():
+            out["frac"][u, p] = trees[p]["frac"][c]
+            out["excl"][u, p] = trees[p]["excl"][c]
+            out["incl"][u, p] = trees[p]["incl"][c]
+    return out
+
+
 def profile_stats_f64(X, n_prof: int) -> np.ndarray:
     """D11: statistics of an fp64 cube [>= n_prof, rows, 16] over profiles 0..n_prof-1."""
     X = np.ascontiguousarray(X, np.float64)
