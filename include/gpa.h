@@ -383,6 +383,43 @@ GPA_API gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const ui
                               gpa_cct cct, uint64_t *d_scope_hist, uint64_t *d_scope_mix,
                               double *d_metrics, gpa_stream_t stream);
 
+/* ---- f1 extension: a CCT per profile, unified by call path (reading R30) -----------------------
+ * The paper reconstructs an approximate CCT "for each GPU kernel invocation" and unifies
+ * the trees of all profiles into one.  Here a profile is a value of the records'
+ * `stream` field (R25).  Per profile p the inputs are its function histogram S_f,p (the FUNC rows
+ * of gpa_attribute_profiles) and its call-site weights w_p (gpa_profile_call_weights); Steps 2-4
+ * run per profile exactly as gpa_reconstruct_cct_inputs would on (S_f,p, w_p).  The unified tree
+ * holds every call path present in at least one profile's tree, numbered breadth first with the
+ * order every tree uses (roots by DAG node, SCC members by function id, calls by call
+ * instruction); frac / excl / incl of profile p at a unified context are p's own tree values
+ * (bit for bit), 0 where p's tree lacks the path.
+ *
+ * gpa_profile_call_weights: adds, per record with a valid stall slot on a call instruction,
+ *   its count to d_prof_call_weight[min(stream, n_profiles) * n_call + site] (DEVICE u64
+ *   [(n_profiles+1) * n_call], accumulated; the last row collects stream ids >= n_profiles).
+ * gpa_reconstruct_cct_per_profile: d_prof_func_hist DEVICE u64 [n_profiles][n_func][16] (16-byte
+ *   aligned), d_prof_call_weight DEVICE u64 [n_profiles][n_call]; max_contexts bounds the unified
+ *   tree and the union tree it is cut from (0: count only, *n_contexts = the unified count);
+ *   GPA_ERR_CAPACITY when exceeded.  Synchronizes `stream`. */
+typedef struct gpa_cct_multi_s *gpa_cct_multi;
+typedef struct {
+  uint64_t n;
+  uint32_t n_profiles;
+  const uint32_t *parent, *site, *node;   /* [n] (NONE for roots / no site) */
+  const uint8_t *kind;                    /* [n] gpa_ctx_kind */
+  const uint32_t *first_child, *n_children;
+  const double *frac;                     /* [n][n_profiles] */
+  const double *excl, *incl;              /* [n][n_profiles][16] */
+} gpa_cct_multi_view;
+GPA_API gpa_status gpa_profile_call_weights(gpa_structure s, const gpa_sample *d_samples, uint64_t n,
+                                            uint32_t n_profiles, uint64_t *d_prof_call_weight, gpa_stream_t stream);
+GPA_API gpa_status gpa_reconstruct_cct_per_profile(gpa_structure s, const uint64_t *d_prof_func_hist,
+                                                   const uint64_t *d_prof_call_weight, uint32_t n_profiles,
+                                                   gpa_weight_mode mode, uint64_t max_contexts, gpa_cct_multi *out,
+                                                   uint64_t *n_contexts, gpa_stream_t stream);
+GPA_API gpa_status gpa_get_cct_multi_view(gpa_cct_multi c, gpa_cct_multi_view *out);
+GPA_API void gpa_free_cct_multi(gpa_cct_multi c);
+
 /* ---- reusable attribution plans -----------------------------------------------------------------
  * The large-call attribution kernels (gpa_set_attr_kernel 7 / 8) first choose, from a sample of
  * the call's records, which granules / (instruction, slot) bins are counted in shared memory (a

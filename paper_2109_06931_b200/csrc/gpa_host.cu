@@ -499,6 +499,11 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
   UP(s->d_call_callee, cc);
   UP(s->d_call_caller, dv.call_caller);
   UP(s->d_inst_func, dv.inst_func);
+  {
+    std::vector<uint32_t> ic(ni ? ni : 1, NONE);
+    for (uint32_t e = 0; e < nc; e++) ic[ci[e]] = e;  // one call site per call instruction (R22)
+    UP(s->d_inst_call, ic);
+  }
   std::vector<uint32_t> order(nc);
   std::iota(order.begin(), order.end(), 0u);
   std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ci[a] < ci[b]; });
@@ -1490,6 +1495,166 @@ void gpa_attr_plan_free(gpa_attr_plan p) {
   if (p->mem) cudaFree(p->mem);
   delete p;
 }
+
+// ---- per-profile trees unified by call path (f1 extension, reading R30) ------------------------
+static void free_cct_multi(gpa_cct_multi_s *m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  for (void *p : m->allocs)
+    if (cudaFreeAsync(p, m->stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(p);
+    }
+  const int dev = m->device;
+  delete m;
+  pool_trim(dev);
+}
+
+static cudaError_t calloc_multi_bytes(gpa_cct_multi_s *m, void **p, size_t bytes) {
+  *p = nullptr;
+  cudaError_t e = pool_alloc(p, bytes ? bytes : 1, m->stream);
+  if (e != cudaSuccess) return e;
+  m->allocs.push_back(*p);
+  return cudaMemsetAsync(*p, 0, bytes ? bytes : 1, m->stream);
+}
+#define calloc_multi(m, pp, n) calloc_multi_bytes((m), (void **)(pp), sizeof(**(pp)) * (size_t)(n))
+
+gpa_status gpa_profile_call_weights(gpa_structure s, const gpa_sample *d_samples, uint64_t n, uint32_t n_profiles,
+                                    uint64_t *d_prof_call_weight, gpa_stream_t stream) {
+  if (!s) return fail(GPA_ERR_INVALID_ARG, "structure is NULL");
+  if (n == 0 || s->info.n_call == 0) return GPA_OK;
+  if (!d_samples || !d_prof_call_weight) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  if ((uintptr_t)d_samples & 15) return fail(GPA_ERR_INVALID_ARG, "d_samples is not 16-byte aligned");
+  if (n_profiles > 65535) return fail(GPA_ERR_INVALID_ARG, "n_profiles %u > 65535", n_profiles);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  CHECK(check_dev_ptr(d_samples, s->device, "d_samples"));
+  CHECK(check_dev_ptr(d_prof_call_weight, s->device, "d_prof_call_weight"));
+  CU(launch_prof_call_weights(s->attr, s->d_inst_call, d_samples, n, n_profiles, s->info.n_call,
+                              (unsigned long long *)d_prof_call_weight, sm_count(s->device), (cudaStream_t)stream));
+  return GPA_OK;
+}
+
+gpa_status gpa_reconstruct_cct_per_profile(gpa_structure s, const uint64_t *d_prof_func_hist,
+                                           const uint64_t *d_prof_call_weight, uint32_t n_profiles,
+                                           gpa_weight_mode mode, uint64_t max_contexts, gpa_cct_multi *out,
+                                           uint64_t *n_contexts, gpa_stream_t stream) {
+  if (!s || !out || !n_contexts) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if (mode != GPA_WEIGHTS_SAMPLES && mode != GPA_WEIGHTS_EXACT) return fail(GPA_ERR_INVALID_ARG, "mode %d", (int)mode);
+  const gpa_structure_info &I = s->info;
+  const uint32_t P = n_profiles;
+  if (P == 0 || P > 65535) return fail(GPA_ERR_INVALID_ARG, "n_profiles %u (1..65535)", P);
+  if ((!d_prof_func_hist && I.n_func) || (!d_prof_call_weight && I.n_call)) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
+  if ((uintptr_t)d_prof_func_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_prof_func_hist must be 16-byte aligned");
+  *out = nullptr;
+  *n_contexts = 0;
+  DeviceGuard g(s->device);
+  CU(g.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  PoolScratch mem(st);
+  const uint32_t nf = I.n_func, nc = I.n_call, nd = I.n_dag;
+  // Steps 1-2 + guard + W of every profile (its own tree's inputs); w is rewritten by Step 2
+  uint64_t *w = nullptr, *W = nullptr, *S_u = nullptr, *w_u = nullptr;
+  uint8_t *fact = nullptr, *dact = nullptr;
+  unsigned long long *d_cnt = nullptr;
+  CU(mem.get(&w, (uint64_t)P * nc));
+  CU(mem.get(&W, (uint64_t)P * nd));
+  CU(mem.get(&fact, (uint64_t)P * nf));
+  CU(mem.get(&dact, (uint64_t)P * nd));
+  CU(mem.get(&S_u, (uint64_t)nf * SLOTS));
+  CU(mem.get(&w_u, nc));
+  CU(mem.get(&d_cnt, 4));
+  if (nc) CU(cudaMemcpyAsync(w, d_prof_call_weight, sizeof(uint64_t) * P * nc, cudaMemcpyDeviceToDevice, st));
+  for (uint32_t p = 0; p < P; p++)
+    CU(launch_cct_propagate(s, d_prof_func_hist + (uint64_t)p * nf * SLOTS, w + (uint64_t)p * nc, fact + (uint64_t)p * nf,
+                            dact + (uint64_t)p * nd, W + (uint64_t)p * nd, d_cnt, mode == GPA_WEIGHTS_EXACT, false, st));
+  // the union tree: activity and weighted edges of any profile (Step 2 on these is a no-op)
+  CU(launch_union_inputs(P, nf, nc, fact, w, S_u, w_u, st));
+  gpa_cct sup = nullptr;
+  uint64_t n_sup = 0;
+  // the union tree holds every profile's tree; count-only calls still need it built
+  CHECK(reconstruct(s, false, nullptr, S_u, w_u, mode, max_contexts ? max_contexts : kScanMaxWords, &sup, &n_sup,
+                    stream));
+  struct SupGuard {
+    gpa_cct c;
+    ~SupGuard() { free_cct(c); }
+  } sg{sup};
+  gpa_status r = cct_levels(sup);
+  if (r != GPA_OK) return r;
+  if (n_sup > kScanMaxWords) return fail(GPA_ERR_CAPACITY, "%llu union contexts", (unsigned long long)n_sup);
+  if (n_sup == 0) {
+    if (max_contexts) {
+      gpa_cct_multi_s *m = new gpa_cct_multi_s();
+      m->device = s->device;
+      m->stream = st;
+      m->n_profiles = P;
+      *out = m;
+    }
+    return GPA_OK;
+  }
+  uint8_t *pres = nullptr;
+  double *frac = nullptr;
+  uint32_t *uid = nullptr, *scan_scratch = nullptr;
+  CU(mem.get(&pres, n_sup * P));
+  CU(mem.get(&frac, n_sup * P));
+  CU(mem.get(&uid, n_sup + 1));
+  CU(mem.get(&scan_scratch, kScanScratchWords));
+  CU(launch_multi_tree(s, sup, P, d_prof_func_hist, w, W, dact, pres, frac, uid, scan_scratch, d_cnt + 1, st));
+  unsigned long long n_u = 0;
+  CU(cudaMemcpyAsync(&n_u, d_cnt + 1, sizeof(n_u), cudaMemcpyDeviceToHost, st));
+  // unified level starts: the scan value at every union-level start
+  std::vector<uint32_t> lv(sup->level_start.size(), 0);
+  for (size_t L = 0; L + 1 < sup->level_start.size(); L++)
+    CU(cudaMemcpyAsync(&lv[L], uid + sup->level_start[L], 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  *n_contexts = n_u;
+  if (max_contexts == 0) return GPA_OK;
+  if (n_u > max_contexts)
+    return fail(GPA_ERR_CAPACITY, "%llu contexts > max_contexts %llu", n_u, (unsigned long long)max_contexts);
+  gpa_cct_multi_s *m = new gpa_cct_multi_s();
+  m->device = s->device;
+  m->stream = st;
+  m->n = n_u;
+  m->n_profiles = P;
+  if (!lv.empty()) lv.back() = (uint32_t)n_u;
+  for (uint32_t v : lv) m->level_start.push_back(v);
+#define CM(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      free_cct_multi(m);                                                                  \
+      cudaGetLastError();                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? GPA_ERR_OUT_OF_MEMORY : GPA_ERR_CUDA, \
+                  "%s: %s", #call, cudaGetErrorString(e_));                               \
+    }                                                                                     \
+  } while (0)
+  CM(calloc_multi(m, &m->parent, n_u));
+  CM(calloc_multi(m, &m->site, n_u));
+  CM(calloc_multi(m, &m->node, n_u));
+  CM(calloc_multi(m, &m->first_child, n_u));
+  CM(calloc_multi(m, &m->n_children, n_u));
+  CM(calloc_multi(m, &m->kind, n_u));
+  CM(calloc_multi(m, &m->frac, n_u * P));
+  CM(calloc_multi(m, &m->excl, n_u * P * SLOTS));
+  CM(calloc_multi(m, &m->incl, n_u * P * SLOTS));
+  CM(launch_multi_compact(sup, P, pres, uid, frac, m, st));
+  CM(launch_multi_values(s, m, d_prof_func_hist, st));
+#undef CM
+  *out = m;
+  return GPA_OK;
+}
+
+gpa_status gpa_get_cct_multi_view(gpa_cct_multi m, gpa_cct_multi_view *v) {
+  if (!m || !v) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  v->n = m->n;
+  v->n_profiles = m->n_profiles;
+  v->parent = m->parent; v->site = m->site; v->node = m->node; v->kind = m->kind;
+  v->first_child = m->first_child; v->n_children = m->n_children;
+  v->frac = m->frac; v->excl = m->excl; v->incl = m->incl;
+  return GPA_OK;
+}
+
+void gpa_free_cct_multi(gpa_cct_multi m) { free_cct_multi(m); }
 
 // ---- distributed statistics: function-aligned instruction ranges ------------------
 static gpa_status partition_bounds(uint32_t ni, const std::vector<uint32_t> &starts, bool contig, uint32_t n_parts,

@@ -71,6 +71,7 @@ struct gpa_structure_s {
   uint16_t *d_inst_len = nullptr;
   uint8_t *d_inst_class = nullptr;
   uint32_t *d_inst_func = nullptr;  // function of each instruction (per-profile histograms)
+  uint32_t *d_inst_call = nullptr;  // call site of each call instruction, NONE elsewhere (per-profile weights)
   uint32_t *d_gfunc = nullptr;      // function of each granule of the pc map (NONE in gaps)
   uint32_t *d_gmap = nullptr;
   gpa::RollSet roll[gpa::ROLL_KINDS];
@@ -92,6 +93,19 @@ struct gpa_structure_s {
   // empty), whether every function's instructions are contiguous, and the sorted function starts
   std::vector<uint32_t> h_func_lo, h_func_starts;
   bool funcs_contiguous = false;
+  std::vector<void *> allocs;
+};
+
+// f1 extension (R30): per-profile trees unified by call path
+struct gpa_cct_multi_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t n = 0;
+  uint32_t n_profiles = 0;
+  uint32_t *parent = nullptr, *site = nullptr, *node = nullptr, *first_child = nullptr, *n_children = nullptr;
+  uint8_t *kind = nullptr;
+  double *frac = nullptr, *excl = nullptr, *incl = nullptr;  // [n][P], [n][P][16], [n][P][16]
+  std::vector<uint64_t> level_start;
   std::vector<void *> allocs;
 };
 
@@ -138,6 +152,7 @@ cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 // scratch words a scan_u32 call (kern_common.cuh) needs: look-back state for up to 2^27
 // elements + the tile ticket
 constexpr size_t kScanScratchWords = 2 * 32768 + 4;
+constexpr uint64_t kScanMaxWords = 1ull << 27;  // the largest scan_u32 input
 }
 
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------
@@ -259,4 +274,16 @@ cudaError_t launch_cct_coop(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_
 cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d_lev, unsigned long long *d_built,
                              int sm_count, cudaStream_t st);
 cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStream_t st);
+// per-profile trees unified by call path (k_cctp.cu, R30)
+cudaError_t launch_prof_call_weights(const AttrTables &T, const uint32_t *inst_call, const gpa_sample *d_samples,
+                                     uint64_t n, uint32_t n_prof, uint32_t n_call, unsigned long long *wp,
+                                     int sm_count, cudaStream_t st);
+cudaError_t launch_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, const uint8_t *fact, const uint64_t *w,
+                                uint64_t *S_u, uint64_t *w_u, cudaStream_t st);
+cudaError_t launch_multi_tree(const gpa_structure_s *s, const gpa_cct_s *sup, uint32_t P, const uint64_t *Sp,
+                              const uint64_t *w, const uint64_t *W, const uint8_t *dact, uint8_t *pres, double *frac,
+                              uint32_t *flag, uint32_t *scan_scratch, unsigned long long *d_total, cudaStream_t st);
+cudaError_t launch_multi_compact(const gpa_cct_s *sup, uint32_t P, const uint8_t *pres, const uint32_t *uid,
+                                 const double *frac, gpa_cct_multi_s *m, cudaStream_t st);
+cudaError_t launch_multi_values(const gpa_structure_s *s, gpa_cct_multi_s *m, const uint64_t *Sp, cudaStream_t st);
 }  // namespace gpa

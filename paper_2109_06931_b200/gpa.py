@@ -57,6 +57,11 @@ class CctView(ctypes.Structure):
                 ("func_hist", _vp)]
 
 
+class CctMultiView(ctypes.Structure):
+    _fields_ = [("n", _u64), ("n_profiles", _u32), ("parent", _vp), ("site", _vp), ("node", _vp), ("kind", _vp),
+                ("first_child", _vp), ("n_children", _vp), ("frac", _vp), ("excl", _vp), ("incl", _vp)]
+
+
 class TraceDesc(ctypes.Structure):
     _fields_ = [("n_lines", _u32), ("line_off", _vp), ("line_kind", _vp), ("line_scope", _vp),
                 ("n_scopes", _u32), ("n_routines", _u32)]
@@ -112,6 +117,11 @@ def _load():
         "gpa_cct_inputs": ([_vp, _vp, _u32, _u32, _vp, _vp, _vp], S),
         "gpa_reconstruct_cct_inputs": ([_vp, _vp, _vp, ctypes.c_int, _u64, ctypes.POINTER(_vp), ctypes.POINTER(_u64),
                                         _vp], S),
+        "gpa_profile_call_weights": ([_vp, _vp, _u64, _u32, _vp, _vp], S),
+        "gpa_reconstruct_cct_per_profile": ([_vp, _vp, _vp, _u32, ctypes.c_int, _u64, ctypes.POINTER(_vp),
+                                             ctypes.POINTER(_u64), _vp], S),
+        "gpa_get_cct_multi_view": ([_vp, ctypes.POINTER(CctMultiView)], S),
+        "gpa_free_cct_multi": ([_vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -603,3 +613,76 @@ def scope_row_count(s: Structure, scope: str, cct: Cct | None = None) -> int:
     n = _u64()
     _check(_lib.gpa_scope_rows(s.handle, SCOPES[scope], ctypes.byref(n), None), "gpa_scope_rows")
     return n.value
+
+
+# ---- f1 extension: per-profile trees unified by call path (reading R30) ----------------------
+def profile_call_weights(s: Structure, samples, n_profiles: int, prof_call_weight, n: int | None = None,
+                         stream=None) -> None:
+    """Per-profile call-site weights w_p (Step 1, R10) from the records, accumulated into
+    prof_call_weight [(n_profiles+1), n_call] u64 (gpa.h)."""
+    nb = samples.numel() * samples.element_size()
+    n = nb // 16 if n is None else int(n)
+    _check(_lib.gpa_profile_call_weights(
+        s.handle, _ptr(samples, "samples", 16 * n), n, int(n_profiles),
+        _ptr(prof_call_weight, "prof_call_weight", 8 * (int(n_profiles) + 1) * s.info["n_call"]),
+        _stream_ptr(stream, samples.device)), "gpa_profile_call_weights")
+
+
+class CctMulti:
+    """Per-profile CCTs unified by call path (gpa_cct_multi): library-owned device arrays."""
+
+    def __init__(self, h, device):
+        self._h = h
+        self.device = device
+        v = CctMultiView()
+        _check(_lib.gpa_get_cct_multi_view(h, ctypes.byref(v)), "gpa_get_cct_multi_view")
+        self._v = v
+        self.n, self.n_profiles = v.n, v.n_profiles
+
+    def tensors(self) -> dict:
+        """Zero-copy torch views (valid until free())."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        v, n, P = self._v, self.n, self.n_profiles
+        spec = {"parent": ("<i4", (n,)), "site": ("<i4", (n,)), "node": ("<i4", (n,)), "kind": ("|u1", (n,)),
+                "first_child": ("<i4", (n,)), "n_children": ("<i4", (n,)), "frac": ("<f8", (n, P)),
+                "excl": ("<f8", (n, P, 16)), "incl": ("<f8", (n, P, 16))}
+        dt = {"<i4": torch.int32, "|u1": torch.uint8, "<f8": torch.float64}
+        return {k: torch.as_tensor(_DevArray(getattr(v, k), shape, ts), device=dev) if n else
+                torch.empty(shape, dtype=dt[ts], device=dev) for k, (ts, shape) in spec.items()}
+
+    def to_numpy(self) -> dict:
+        out = {k: x.cpu().numpy() for k, x in self.tensors().items()}
+        for k in ("parent", "site", "node", "first_child", "n_children"):
+            out[k] = out[k].astype(np.int32).view(np.uint32)
+        out["n"], out["n_profiles"] = self.n, self.n_profiles
+        return out
+
+    def free(self):
+        if self._h is not None:
+            _lib.gpa_free_cct_multi(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def reconstruct_cct_per_profile(s: Structure, prof_func_hist, prof_call_weight, n_profiles: int,
+                                mode: int = WEIGHTS_SAMPLES, max_contexts: int = (1 << 63) - 1, stream=None):
+    """An approximate CCT per profile unified by call path (reading R30) from
+    per-profile S_f [>= n_profiles, n_func, 16] and w [>= n_profiles, n_call] (u64 device tensors).
+    Returns a CctMulti (or the unified context count when max_contexts == 0)."""
+    h = _vp()
+    n = _u64()
+    P = int(n_profiles)
+    _check(_lib.gpa_reconstruct_cct_per_profile(
+        s.handle, _ptr(prof_func_hist, "prof_func_hist", 128 * P * s.info["n_func"]),
+        _ptr(prof_call_weight, "prof_call_weight", 8 * P * s.info["n_call"]), P, mode, max_contexts,
+        ctypes.byref(h), ctypes.byref(n), _stream_ptr(stream, prof_func_hist.device)),
+        "gpa_reconstruct_cct_per_profile")
+    if max_contexts == 0:
+        return n.value
+    return CctMulti(h, s.device)
