@@ -1568,12 +1568,12 @@ gpa_status gpa_reconstruct_cct_per_profile(gpa_structure s, const uint64_t *d_pr
   for (uint32_t p = 0; p < P; p++)
     CU(launch_cct_propagate(s, d_prof_func_hist + (uint64_t)p * nf * SLOTS, w + (uint64_t)p * nc, fact + (uint64_t)p * nf,
                             dact + (uint64_t)p * nd, W + (uint64_t)p * nd, d_cnt, mode == GPA_WEIGHTS_EXACT, false, st));
-  // the union tree: activity and weighted edges of any profile (Step 2 on these is a no-op)
-  CU(launch_union_inputs(P, nf, nc, fact, w, S_u, w_u, st));
+  // the union tree: activity and weighted edges of any profile (structure only: sample weights)
+  CU(launch_union_inputs(s, P, fact, dact, w, S_u, w_u, st));
   gpa_cct sup = nullptr;
   uint64_t n_sup = 0;
   // the union tree holds every profile's tree; count-only calls still need it built
-  CHECK(reconstruct(s, false, nullptr, S_u, w_u, mode, max_contexts ? max_contexts : kScanMaxWords, &sup, &n_sup,
+  CHECK(reconstruct(s, false, nullptr, S_u, w_u, GPA_WEIGHTS_SAMPLES, max_contexts ? max_contexts : kScanMaxWords, &sup, &n_sup,
                     stream));
   struct SupGuard {
     gpa_cct c;

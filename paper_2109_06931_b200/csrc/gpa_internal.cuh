@@ -278,8 +278,8 @@ cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStre
 cudaError_t launch_prof_call_weights(const AttrTables &T, const uint32_t *inst_call, const gpa_sample *d_samples,
                                      uint64_t n, uint32_t n_prof, uint32_t n_call, unsigned long long *wp,
                                      int sm_count, cudaStream_t st);
-cudaError_t launch_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, const uint8_t *fact, const uint64_t *w,
-                                uint64_t *S_u, uint64_t *w_u, cudaStream_t st);
+cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint8_t *fact, const uint8_t *dact,
+                                const uint64_t *w, uint64_t *S_u, uint64_t *w_u, cudaStream_t st);
 cudaError_t launch_multi_tree(const gpa_structure_s *s, const gpa_cct_s *sup, uint32_t P, const uint64_t *Sp,
                               const uint64_t *w, const uint64_t *W, const uint8_t *dact, uint8_t *pres, double *frac,
                               uint32_t *flag, uint32_t *scan_scratch, unsigned long long *d_total, cudaStream_t st);

@@ -41,14 +41,19 @@ __global__ void k_prof_call_weights(AttrTables T, const uint32_t *__restrict__ i
   }
 }
 
-// union inputs: slot 0 of S = 1 for functions active in some profile (activity is all the union
-// tree needs), w = 1 for edges with weight in some profile (after each profile's Step 2)
-__global__ void k_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, const uint8_t *__restrict__ fact,
-                               const uint64_t *__restrict__ w, uint64_t *__restrict__ S_u, uint64_t *__restrict__ w_u) {
+// union inputs: slot 0 of S = 1 for functions active in some profile or whose DAG node is (the
+// guard of R12 activates a caller's DAG node without its function), w = 1 for edges with weight
+// in some profile (after each profile's Step 2).  Step 2 only adds weight and activity, so the
+// union tree contains every profile's tree (possibly more paths, which no profile marks present)
+__global__ void k_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, uint32_t n_dag,
+                               const uint32_t *__restrict__ scc_of, const uint8_t *__restrict__ fact,
+                               const uint8_t *__restrict__ dact, const uint64_t *__restrict__ w,
+                               uint64_t *__restrict__ S_u, uint64_t *__restrict__ w_u) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_func) {
+    const uint32_t X = scc_of[t];
     uint8_t a = 0;
-    for (uint32_t p = 0; p < P; p++) a |= fact[(uint64_t)p * n_func + t];
+    for (uint32_t p = 0; p < P; p++) a |= fact[(uint64_t)p * n_func + t] | dact[(uint64_t)p * n_dag + X];
     for (int r = 0; r < GPA_SLOTS; r++) S_u[(uint64_t)t * GPA_SLOTS + r] = (r == 0 && a) ? 1ull : 0ull;
   }
   if (t < n_call) {
@@ -204,11 +209,13 @@ cudaError_t launch_prof_call_weights(const AttrTables &T, const uint32_t *inst_c
   return cudaGetLastError();
 }
 
-cudaError_t launch_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, const uint8_t *fact, const uint64_t *w,
-                                uint64_t *S_u, uint64_t *w_u, cudaStream_t st) {
+cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint8_t *fact, const uint8_t *dact,
+                                const uint64_t *w, uint64_t *S_u, uint64_t *w_u, cudaStream_t st) {
+  const uint32_t n_func = s->info.n_func, n_call = s->info.n_call;
   const uint32_t m = n_func > n_call ? n_func : n_call;
   if (m == 0) return cudaSuccess;
-  k_union_inputs<<<(m + 255) / 256, 256, 0, st>>>(P, n_func, n_call, fact, w, S_u, w_u);
+  k_union_inputs<<<(m + 255) / 256, 256, 0, st>>>(P, n_func, n_call, s->info.n_dag, s->d_scc_of, fact, dact, w, S_u,
+                                                  w_u);
   count_launches(1);
   return cudaGetLastError();
 }
