@@ -84,6 +84,29 @@ def f1():
                       "inst_records_per_s": n / ms_inst * 1e3, "inst_GBps": 16 * n / ms_inst / 1e6,
                       "inst_stats_ms": ms_inst_stats, "contexts": c.n, "cct_profiles_ms": ms_cct,
                       "cct_stats_ms": ms_cct_stats}), flush=True)
+    # a tree per profile unified by call path (R30): call-site weights from the records + build
+    del E, I
+    PW = torch.zeros((P + 1, max(s.info["n_call"], 1)), dtype=torch.int64, device="cuda")
+
+    def run_w():
+        PW.zero_()
+        gpa.profile_call_weights(s, rec, P, PW)
+
+    ms_w = timed(run_w)
+    holder = []
+
+    def run_multi():
+        while holder:
+            holder.pop().free()
+        holder.append(gpa.reconstruct_cct_per_profile(s, PH, PW, P))
+
+    ms_multi = timed(run_multi)
+    print(json.dumps({"row": "f1-cct-per-profile", "workload": "C4", "profiles": P,
+                      "call_weights_ms": ms_w, "call_weights_GBps": 16 * n / ms_w / 1e6,
+                      "call_weights_frac": 16 * n / ms_w / 1e6 / PEAK,
+                      "unified_contexts": holder[0].n, "aggregate_contexts": c.n,
+                      "reconstruct_per_profile_ms": ms_multi}), flush=True)
+    holder.pop().free()
 
 
 def f3(s, PH, P):
