@@ -1559,17 +1559,17 @@ gpa_status gpa_reconstruct_cct_per_profile(gpa_structure s, const uint64_t *d_pr
   unsigned long long *d_cnt = nullptr;
   CU(mem.get(&w, (uint64_t)P * nc));
   CU(mem.get(&W, (uint64_t)P * nd));
-  CU(mem.get(&fact, (uint64_t)P * nf));
-  CU(mem.get(&dact, (uint64_t)P * nd));
+  const uint64_t fs = (nf + 7ull) & ~7ull, ds = (nd + 7ull) & ~7ull;
+  CU(mem.get(&fact, (uint64_t)P * fs));
+  CU(mem.get(&dact, (uint64_t)P * ds));
   CU(mem.get(&S_u, (uint64_t)nf * SLOTS));
   CU(mem.get(&w_u, nc));
   CU(mem.get(&d_cnt, 4));
   if (nc) CU(cudaMemcpyAsync(w, d_prof_call_weight, sizeof(uint64_t) * P * nc, cudaMemcpyDeviceToDevice, st));
-  for (uint32_t p = 0; p < P; p++)
-    CU(launch_cct_propagate(s, d_prof_func_hist + (uint64_t)p * nf * SLOTS, w + (uint64_t)p * nc, fact + (uint64_t)p * nf,
-                            dact + (uint64_t)p * nd, W + (uint64_t)p * nd, d_cnt, mode == GPA_WEIGHTS_EXACT, false, st));
+  // one block per profile (fact / dact rows padded to 8 bytes: the byte flags are set with word atomics)
+  CU(launch_cct_propagate(s, d_prof_func_hist, w, fact, dact, W, d_cnt, mode == GPA_WEIGHTS_EXACT, false, st, P, fs, ds));
   // the union tree: activity and weighted edges of any profile (structure only: sample weights)
-  CU(launch_union_inputs(s, P, fact, dact, w, S_u, w_u, st));
+  CU(launch_union_inputs(s, P, fact, fs, dact, ds, w, S_u, w_u, st));
   gpa_cct sup = nullptr;
   uint64_t n_sup = 0;
   // the union tree holds every profile's tree; count-only calls still need it built
@@ -1599,7 +1599,7 @@ gpa_status gpa_reconstruct_cct_per_profile(gpa_structure s, const uint64_t *d_pr
   CU(mem.get(&frac, n_sup * P));
   CU(mem.get(&uid, n_sup + 1));
   CU(mem.get(&scan_scratch, kScanScratchWords));
-  CU(launch_multi_tree(s, sup, P, d_prof_func_hist, w, W, dact, pres, frac, uid, scan_scratch, d_cnt + 1, st));
+  CU(launch_multi_tree(s, sup, P, d_prof_func_hist, w, W, dact, ds, pres, frac, uid, scan_scratch, d_cnt + 1, st));
   unsigned long long n_u = 0;
   CU(cudaMemcpyAsync(&n_u, d_cnt + 1, sizeof(n_u), cudaMemcpyDeviceToHost, st));
   // unified level starts: the scan value at every union-level start

@@ -203,7 +203,8 @@ cudaError_t launch_cct_weights(const gpa_structure_s *s, const uint64_t *d_hist,
                                cudaStream_t st);
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
-                                 unsigned long long *d_count, bool exact, bool count, cudaStream_t st);
+                                 unsigned long long *d_count, bool exact, bool count, cudaStream_t st,
+                                 uint32_t n_batch = 0, uint64_t fstride = 0, uint64_t dstride = 0);
 // per-profile function histograms and cross-profile statistics (k_prof.cu)
 cudaError_t launch_attribute_profiles(const AttrTables &T, const uint32_t *d_inst_func, const uint32_t *d_gfunc,
                                       uint32_t n_func,
@@ -278,11 +279,12 @@ cudaError_t launch_cct_incl_level(gpa_cct_s *c, uint64_t a, uint64_t b, cudaStre
 cudaError_t launch_prof_call_weights(const AttrTables &T, const uint32_t *inst_call, const gpa_sample *d_samples,
                                      uint64_t n, uint32_t n_prof, uint32_t n_call, unsigned long long *wp,
                                      int sm_count, cudaStream_t st);
-cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint8_t *fact, const uint8_t *dact,
-                                const uint64_t *w, uint64_t *S_u, uint64_t *w_u, cudaStream_t st);
+cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint8_t *fact, uint64_t fs,
+                                const uint8_t *dact, uint64_t ds, const uint64_t *w, uint64_t *S_u, uint64_t *w_u,
+                                cudaStream_t st);
 cudaError_t launch_multi_tree(const gpa_structure_s *s, const gpa_cct_s *sup, uint32_t P, const uint64_t *Sp,
-                              const uint64_t *w, const uint64_t *W, const uint8_t *dact, uint8_t *pres, double *frac,
-                              uint32_t *flag, uint32_t *scan_scratch, unsigned long long *d_total, cudaStream_t st);
+                              const uint64_t *w, const uint64_t *W, const uint8_t *dact, uint64_t ds, uint8_t *pres,
+                              double *frac, uint32_t *flag, uint32_t *scan_scratch, unsigned long long *d_total, cudaStream_t st);
 cudaError_t launch_multi_compact(const gpa_cct_s *sup, uint32_t P, const uint8_t *pres, const uint32_t *uid,
                                  const double *frac, gpa_cct_multi_s *m, cudaStream_t st);
 cudaError_t launch_multi_values(const gpa_structure_s *s, gpa_cct_multi_s *m, const uint64_t *Sp, cudaStream_t st);

@@ -53,6 +53,8 @@ struct PropArgs {
   uint32_t *q0, *q1;  // worklists, max(n_func, n_dag) entries each
   uint32_t n_ext;     // external call sites (din_e entries)
   uint32_t stage_dp;  // SM only: the DP's static tables fit behind the mutable state
+  uint32_t batch;     // gridDim.x problems (R30): block b works on problem b's slices
+  uint64_t fstride, dstride, pstride;  // activity bytes per problem (func, DAG); paths + q u64 per problem
 };
 
 // set byte flag[i] to 1; true if it was 0 (byte flags live in 32-bit words: atomicOr)
@@ -69,7 +71,19 @@ __device__ __forceinline__ bool set_flag(volatile uint8_t *flag, uint32_t i) {
 // whole kernel (every fixpoint round then costs shared-memory, not L2, latency) and is
 // written back at the end; the read-only graph tables stay in global memory (L1-cached).
 template <bool SM>
-__global__ void __launch_bounds__(1024) k_propagate(PropArgs A) {
+__global__ void __launch_bounds__(1024) k_propagate(PropArgs A0) {
+  PropArgs A = A0;
+  if (A.batch) {  // one independent problem per block (per-profile trees, R30)
+    const uint64_t b = blockIdx.x;
+    A.S_f += b * A.n_func * GPA_SLOTS;
+    A.w += b * A.n_call;
+    A.W += b * A.n_dag;
+    A.fact += b * A.fstride;
+    A.dact += b * A.dstride;
+    A.paths += b * A.pstride;
+    A.q0 = reinterpret_cast<uint32_t *>(A.paths + A.n_dag + 1);
+    A.q1 = A.q0 + (A.pstride - A.n_dag - 1);
+  }
   __shared__ int changed;
   __shared__ unsigned long long red[32];
   extern __shared__ __align__(16) uint8_t psm[];
@@ -971,14 +985,21 @@ constexpr size_t kPropSmem = 200 * 1024;
 
 cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f, uint64_t *d_w,
                                  uint8_t *d_func_active, uint8_t *d_dag_active, uint64_t *d_W,
-                                 unsigned long long *d_count, bool exact, bool count, cudaStream_t st) {
-  // paths[] scratch lives behind W in the caller's allocation? keep it separate and simple:
+                                 unsigned long long *d_count, bool exact, bool count, cudaStream_t st,
+                                 uint32_t n_batch, uint64_t fstride, uint64_t dstride) {
   static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
+  if (n_batch && count) return cudaErrorInvalidValue;  // the path count is a single-problem output
   uint64_t *paths = nullptr;
   const size_t nq = std::max<size_t>(s->info.n_func, s->info.n_dag) + 1;
-  cudaError_t e = pool_alloc((void **)&paths, sizeof(uint64_t) * (s->info.n_dag + 1) + 8 * nq, st);
+  const uint64_t pstride = (s->info.n_dag + 1) + nq;  // u64 words: paths, then two u32 worklists of nq
+  const uint32_t nb = n_batch ? n_batch : 1;
+  cudaError_t e = pool_alloc((void **)&paths, sizeof(uint64_t) * pstride * nb, st);
   if (e != cudaSuccess) return e;
   PropArgs A;
+  A.batch = n_batch ? 1u : 0u;
+  A.fstride = fstride;
+  A.dstride = dstride;
+  A.pstride = pstride;
   A.n_func = s->info.n_func; A.n_dag = s->info.n_dag; A.n_lev = s->info.dag_levels; A.exact = exact ? 1 : 0; A.do_count = count ? 1 : 0;
   A.S_f = d_S_f; A.fin_ptr = s->d_fin_ptr; A.fin_e = s->d_fin_e; A.caller = s->d_call_caller;
   A.scc_of = s->d_scc_of; A.din_ptr = s->d_din_ptr; A.din_e = s->d_din_e; A.dmem_ptr = s->d_dmem_ptr;
@@ -998,9 +1019,9 @@ cudaError_t launch_cct_propagate(const gpa_structure_s *s, const uint64_t *d_S_f
         (e = cudaFuncSetAttribute(k_propagate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPropSmem)) !=
             cudaSuccess)
       return e;
-    k_propagate<true><<<1, 1024, sm, st>>>(A);
+    k_propagate<true><<<nb, 1024, sm, st>>>(A);
   } else {
-    k_propagate<false><<<1, 1024, 0, st>>>(A);
+    k_propagate<false><<<nb, 1024, 0, st>>>(A);
   }
   count_launches(1);
   e = cudaGetLastError();

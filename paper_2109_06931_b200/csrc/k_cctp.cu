@@ -45,7 +45,7 @@ __global__ void k_prof_call_weights(AttrTables T, const uint32_t *__restrict__ i
 // guard of R12 activates a caller's DAG node without its function), w = 1 for edges with weight
 // in some profile (after each profile's Step 2).  Step 2 only adds weight and activity, so the
 // union tree contains every profile's tree (possibly more paths, which no profile marks present)
-__global__ void k_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, uint32_t n_dag,
+__global__ void k_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, uint64_t fs, uint64_t ds,
                                const uint32_t *__restrict__ scc_of, const uint8_t *__restrict__ fact,
                                const uint8_t *__restrict__ dact, const uint64_t *__restrict__ w,
                                uint64_t *__restrict__ S_u, uint64_t *__restrict__ w_u) {
@@ -53,7 +53,7 @@ __global__ void k_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, uin
   if (t < n_func) {
     const uint32_t X = scc_of[t];
     uint8_t a = 0;
-    for (uint32_t p = 0; p < P; p++) a |= fact[(uint64_t)p * n_func + t] | dact[(uint64_t)p * n_dag + X];
+    for (uint32_t p = 0; p < P; p++) a |= fact[p * fs + t] | dact[p * ds + X];
     for (int r = 0; r < GPA_SLOTS; r++) S_u[(uint64_t)t * GPA_SLOTS + r] = (r == 0 && a) ? 1ull : 0ull;
   }
   if (t < n_call) {
@@ -68,7 +68,8 @@ struct MultiArgs {
   const uint32_t *parent, *site, *node;  // union tree
   const uint8_t *kind;
   const uint64_t *w, *W;                 // per profile after Step 2: [P][n_call], [P][n_dag]
-  const uint8_t *dact;                   // [P][n_dag]
+  const uint8_t *dact;                   // [P][ds]
+  uint64_t ds;
   uint8_t *pres;                         // [n][P]
   double *frac;                          // [n][P]
 };
@@ -83,7 +84,7 @@ __global__ void k_multi_frac(MultiArgs A, uint64_t a, uint64_t b) {
     uint8_t pr = 0;
     double f = 0.0;
     if (pc == NONE) {  // a root: active in p (roots are the DAG nodes without external in-edges, R15)
-      pr = A.dact[(uint64_t)p * A.n_dag + A.node[c]];
+      pr = A.dact[p * A.ds + A.node[c]];
       f = 1.0;
     } else if (A.pres[(uint64_t)pc * A.P + p]) {
       const double fp = A.frac[(uint64_t)pc * A.P + p];
@@ -209,21 +210,22 @@ cudaError_t launch_prof_call_weights(const AttrTables &T, const uint32_t *inst_c
   return cudaGetLastError();
 }
 
-cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint8_t *fact, const uint8_t *dact,
-                                const uint64_t *w, uint64_t *S_u, uint64_t *w_u, cudaStream_t st) {
+cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint8_t *fact, uint64_t fs,
+                                const uint8_t *dact, uint64_t ds, const uint64_t *w, uint64_t *S_u, uint64_t *w_u,
+                                cudaStream_t st) {
   const uint32_t n_func = s->info.n_func, n_call = s->info.n_call;
   const uint32_t m = n_func > n_call ? n_func : n_call;
   if (m == 0) return cudaSuccess;
-  k_union_inputs<<<(m + 255) / 256, 256, 0, st>>>(P, n_func, n_call, s->info.n_dag, s->d_scc_of, fact, dact, w, S_u,
-                                                  w_u);
+  k_union_inputs<<<(m + 255) / 256, 256, 0, st>>>(P, n_func, n_call, fs, ds, s->d_scc_of, fact, dact, w, S_u, w_u);
   count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_multi_tree(const gpa_structure_s *s, const gpa_cct_s *sup, uint32_t P, const uint64_t *Sp,
-                              const uint64_t *w, const uint64_t *W, const uint8_t *dact, uint8_t *pres, double *frac,
+                              const uint64_t *w, const uint64_t *W, const uint8_t *dact, uint64_t ds, uint8_t *pres,
+                              double *frac,
                               uint32_t *flag, uint32_t *scan_scratch, unsigned long long *d_total, cudaStream_t st) {
-  MultiArgs A{P, s->info.n_call, s->info.n_dag, sup->parent, sup->site, sup->node, sup->kind, w, W, dact, pres, frac};
+  MultiArgs A{P, s->info.n_call, s->info.n_dag, sup->parent, sup->site, sup->node, sup->kind, w, W, dact, ds, pres, frac};
   for (size_t L = 0; L + 1 < sup->level_start.size(); L++) {
     const uint64_t a = sup->level_start[L], b = sup->level_start[L + 1];
     if (b > a) {
