@@ -652,6 +652,30 @@ static void free_cct(gpa_cct_s *c) {
   pool_trim(dev);  // whatever the stream has already released beyond the pool's threshold
 }
 
+// several arrays carved from ONE stream-ordered allocation (each 256-B aligned): a CCT call's
+// dozen buffers cost one pool call instead of twelve (host time that small trees pay in full)
+struct Carve {
+  void **p;
+  size_t bytes;
+};
+template <class T>
+static Carve carve(T **p, size_t n) {
+  return Carve{reinterpret_cast<void **>(p), sizeof(T) * (n ? n : 1)};
+}
+static cudaError_t alloc_block(gpa_cct_s *c, std::initializer_list<Carve> parts) {
+  size_t tot = 0;
+  for (const Carve &q : parts) tot += (q.bytes + 255) & ~(size_t)255;
+  uint8_t *b = nullptr;
+  cudaError_t e = pool_alloc((void **)&b, tot, c->stream);
+  if (e != cudaSuccess) return e;
+  c->allocs.push_back(b);
+  for (const Carve &q : parts) {
+    *q.p = b;
+    b += (q.bytes + 255) & ~(size_t)255;
+  }
+  return cudaSuccess;
+}
+
 template <class T>
 static cudaError_t calloc_dev(gpa_cct_s *c, T **p, size_t n) {
   *p = nullptr;
@@ -831,7 +855,7 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
       HC(pool_alloc(&plan_mem, plan_bytes(s->attr, variant), st));
       plan_mem_err = plan_mem;
       HC(plan_build(s->attr, variant, reinterpret_cast<const uint4 *>(buf[b]), m, plan_mem, &plan, sm_count(s->device), st));
-      HC(plan_begin(plan, &acc, st));
+      HC(plan_begin(plan, &acc, sm_count(s->device), st));
     }
     if (planned)
       HC(plan_run(s->attr, plan, acc, reinterpret_cast<const uint4 *>(buf[b]), m, nullptr, sm_count(s->device), st));
@@ -883,12 +907,8 @@ static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d
       return ret;                                                                         \
     }                                                                                     \
   } while (0)
-  CC(calloc_dev(c, &c->w, I.n_call));
-  CC(calloc_dev(c, &c->S_f, (size_t)I.n_func * SLOTS));
-  CC(calloc_dev(c, &c->func_active, I.n_func));
-  CC(calloc_dev(c, &c->dag_active, I.n_dag));
-  CC(calloc_dev(c, &c->W, I.n_dag));
-  CC(calloc_dev(c, &d_cnt, 4));
+  CC(alloc_block(c, {carve(&c->w, I.n_call), carve(&c->S_f, (size_t)I.n_func * SLOTS), carve(&c->func_active, I.n_func),
+                      carve(&c->dag_active, I.n_dag), carve(&c->W, I.n_dag), carve(&d_cnt, 4)}));
   // Step 1: edge weights and per-function samples S_f (the FUNC roll-up), or the caller's
   // (copied: Step 2 rewrites w)
   if (from_hist) {
@@ -911,17 +931,10 @@ static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d
                             false, st));
     const uint64_t nb = small_static ? I.cct_path_bound : kSmallContexts;
     c->n = nb;
-    CC(calloc_dev(c, &c->parent, nb));
-    CC(calloc_dev(c, &c->site, nb));
-    CC(calloc_dev(c, &c->node, nb));
-    CC(calloc_dev(c, &c->first_child, nb));
-    CC(calloc_dev(c, &c->n_children, nb));
-    CC(calloc_dev(c, &c->kind, nb));
-    CC(calloc_dev(c, &c->frac, nb));
-    CC(calloc_dev(c, &c->excl, nb * SLOTS));
-    CC(calloc_dev(c, &c->incl, nb * SLOTS));
     uint32_t *d_lev = nullptr;
-    CC(calloc_dev(c, &d_lev, 1100));
+    CC(alloc_block(c, {carve(&c->parent, nb), carve(&c->site, nb), carve(&c->node, nb), carve(&c->first_child, nb),
+                       carve(&c->n_children, nb), carve(&c->kind, nb), carve(&c->frac, nb), carve(&c->excl, nb * SLOTS),
+                       carve(&c->incl, nb * SLOTS), carve(&d_lev, 1100)}));
     c->d_lev = d_lev; c->lev_fmt = 1; c->lev_len = 1100;
     CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
     CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -968,15 +981,9 @@ static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d
     return fail(GPA_ERR_CAPACITY, "%llu contexts exceed the u32 context index", (unsigned long long)n);
   }
   c->n = n;
-  CC(calloc_dev(c, &c->parent, n));
-  CC(calloc_dev(c, &c->site, n));
-  CC(calloc_dev(c, &c->node, n));
-  CC(calloc_dev(c, &c->first_child, n));
-  CC(calloc_dev(c, &c->n_children, n));
-  CC(calloc_dev(c, &c->kind, n));
-  CC(calloc_dev(c, &c->frac, n));
-  CC(calloc_dev(c, &c->excl, n * SLOTS));
-  CC(calloc_dev(c, &c->incl, n * SLOTS));
+  CC(alloc_block(c, {carve(&c->parent, n), carve(&c->site, n), carve(&c->node, n), carve(&c->first_child, n),
+                     carve(&c->n_children, n), carve(&c->kind, n), carve(&c->frac, n), carve(&c->excl, n * SLOTS),
+                     carve(&c->incl, n * SLOTS)}));
   if (cct_small_ok(s, n)) {  // one CTA builds the whole tree: no per-level launches or syncs
     uint32_t *d_lev = nullptr;
     CC(calloc_dev(c, &d_lev, 1100));
@@ -1480,7 +1487,7 @@ gpa_status gpa_attribute_samples_planned(gpa_structure s, gpa_attr_plan p, const
   cudaStream_t st = (cudaStream_t)stream;
   const int sm = sm_count(s->device);
   AttrAcc a;
-  CU(plan_begin(p->p, &a, st));
+  CU(plan_begin(p->p, &a, sm, st));
   cudaError_t e = plan_run(s->attr, p->p, a, reinterpret_cast<const uint4 *>(d_samples), n, d_rec_inst, sm, st);
   cudaError_t e2 = plan_end(s->attr, p->p, &a, (unsigned long long *)d_inst_hist,
                             (unsigned long long *)d_unattributed, sm, st);

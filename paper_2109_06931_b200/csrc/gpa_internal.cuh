@@ -168,11 +168,13 @@ struct AttrPlan {
 struct AttrAcc {
   unsigned long long *acc = nullptr, *Hg = nullptr;
   unsigned int *ctr = nullptr;  // dynamic tile counter (reset before every launch)
+  uint32_t *dump = nullptr;     // one slab of shared-table words per CTA (flushed by store, folded into acc)
+  int slabs = 0;
 };
 size_t plan_bytes(const AttrTables &T, int variant);
 cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,
                        int sm_count, cudaStream_t st);
-cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, cudaStream_t st);
+cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, int sm_count, cudaStream_t st);
 cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
                      uint32_t *ri, int sm_count, cudaStream_t st);
 cudaError_t plan_end(const AttrTables &T, const AttrPlan &p, AttrAcc *a, unsigned long long *H, unsigned long long *U,

@@ -385,6 +385,13 @@ static_assert((size_t)kHotBins * 4 + 2 * 31 * 64 * 16 + 64 <= 227 * 1024, "GPA_H
 using RingBins = Ring<31, 2, 2>;
 constexpr int kLookBins = 1;
 
+// cnt[key] += 1 for every lane whose key != NONE, one atomic per distinct key of the warp (all 32
+// lanes must call it: the sample loops run whole warps, chunks x kSampleChunk being a multiple of 32)
+__device__ __forceinline__ void sample_add(uint32_t *cnt, uint32_t key) {
+  const unsigned peers = __match_any_sync(FULL, key);
+  if (key != NONE && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(cnt + key, (uint32_t)__popc(peers));
+}
+
 // `chunks` runs of kSampleChunk records, evenly spaced over the call's records
 __global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint64_t n, uint32_t chunks,
                               uint32_t *__restrict__ scnt) {
@@ -395,7 +402,9 @@ __global__ void k_sample_bins(AttrTables T, const uint4 *__restrict__ rec, uint6
     uint4 v = ld_stream(rec + k);
     uint32_t i = lookup<0>(T, ((uint64_t)v.y << 32) | v.x);
     uint32_t stall = v.w & 0xFFFFu;
-    if (i != NONE && stall < GPA_VALID_SLOTS) atomicAdd(scnt + (uint64_t)i * kHotSlots + stall, 1u);
+    // sampled runs are bursts of one kernel: lanes often share a bin, so one atomic per distinct bin
+    // and warp (a hot bin's counter would otherwise serialise thousands of same-address atomics)
+    sample_add(scnt, i != NONE && stall < GPA_VALID_SLOTS ? i * kHotSlots + stall : NONE);
   }
 }
 
@@ -428,12 +437,6 @@ __global__ void k_codemap_bins(const uint32_t *__restrict__ gmap, uint64_t n_gra
     uint32_t m = gmap[g];
     code[g] = m == NONE ? 0xFFFFFFFFull : ((unsigned long long)hot_info[m] << 32 | (m << 4));
   }
-}
-
-__device__ __forceinline__ void repay(unsigned long long *H, const uint32_t *bin_of, uint32_t idx,
-                                      unsigned long long v) {
-  uint32_t b = __ldg(bin_of + idx);
-  if (b != NONE) red_add_u64(H + b, v);
 }
 
 __device__ __forceinline__ uint32_t ldg_keep_u32(const uint32_t *p, uint64_t pol) {
@@ -648,6 +651,128 @@ cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsig
   return e != cudaSuccess ? e : e2;
 }
 
+// ---- store flush of a CTA's byte-counter table ----------------------------------------------------
+// At the end of K_attr_probe / K_attr_code32 every CTA stores its table of packed byte counters to a
+// slab of its own (coalesced 16-B stores) instead of one L2 reduction per non-zero counter (up to
+// 98 k per CTA, ~15 M per launch, ~75 us at the measured 1.9e11 reductions/s).  k_fold_all then
+// sums the slabs byte-wise into acc (byte j of word x = counter 4x + j).
+// Words [nw, NWALL) of the slab (table words this plan leaves unused, never zeroed in shared memory)
+// are stored as 0.  NWALL is a multiple of 4.
+template <uint32_t NWALL>
+__device__ __forceinline__ void dump_table(const uint32_t *tab, uint32_t nw, uint32_t *slab, uint32_t nthr) {
+  static_assert(NWALL % 4 == 0, "slab rows are stored as 16-B vectors");
+  for (uint32_t x = threadIdx.x; x < NWALL / 4; x += nthr) {
+    uint4 v = reinterpret_cast<const uint4 *>(tab)[x];
+    if (4 * x + 4 > nw) {
+      v.x = 4 * x + 0 < nw ? v.x : 0u;
+      v.y = 4 * x + 1 < nw ? v.y : 0u;
+      v.z = 4 * x + 2 < nw ? v.z : 0u;
+      v.w = 4 * x + 3 < nw ? v.w : 0u;
+    }
+    reinterpret_cast<uint4 *>(slab)[x] = v;
+  }
+}
+
+// The end of a call in one launch.  Blocks [0, tb): table words, kFoldParts x 32 threads per 32
+// words: the CTA slabs of the last launch are summed byte-wise (byte j of word x = counter 4x + j;
+// two bytes at a time in 16-bit lanes, <= 256 slabs of 255 per lane before a spill), the parts
+// combined in shared memory, then either added to acc (fin == 0: a chunk of a multi-launch call;
+// the dynamic tile counter is reset for the next launch) or, with acc, reduced into H through the
+// plan (fin == 1: K_attr_probe entry -> granule -> instruction; K_attr_code32 bin -> (instruction,
+// slot)).  Blocks [tb, grid) (fin == 1 only): the granule scratch Hg -> H / U (gap granules and
+// the out-of-module row -> U).
+constexpr int kFoldParts = 8;
+struct FoldArgs {
+  const uint32_t *dump;
+  uint32_t nw, tb;
+  int slabs, fin, variant;
+  unsigned long long *acc;
+  unsigned int *ctr;
+  const unsigned long long *best;       // 7
+  const uint32_t *bin_of, *thr;         // 8
+  const uint32_t *gmap;
+  const unsigned long long *Hg;
+  uint64_t n_gran;
+  unsigned long long *H, *U;
+};
+
+__global__ void __launch_bounds__(kFoldParts * 32) k_fold_all(FoldArgs F) {
+  __shared__ uint32_t part[kFoldParts][32][4];
+  if (blockIdx.x >= F.tb) {  // Hg -> H / U, 16 lanes per granule row
+    const uint64_t nb = gridDim.x - F.tb;
+    for (uint64_t t = (uint64_t)(blockIdx.x - F.tb) * blockDim.x + threadIdx.x; t < (F.n_gran + 1) * 16; t += nb * blockDim.x) {
+      const unsigned long long v = F.Hg[t];
+      if (!v) continue;
+      const uint64_t g = t >> 4;
+      const uint32_t sl = (uint32_t)(t & 15), i = g < F.n_gran ? __ldg(F.gmap + g) : NONE;
+      red_add_u64(i == NONE ? F.U + sl : F.H + ((uint64_t)i << 4 | sl), v);
+    }
+    return;
+  }
+  const uint32_t wl = threadIdx.x & 31, pt = threadIdx.x >> 5;
+  const uint32_t x = blockIdx.x * 32 + wl;
+  if (!F.fin && blockIdx.x == 0 && threadIdx.x == 0 && F.ctr) *F.ctr = 0;  // the next launch's tile counter
+  uint32_t s4[4] = {0, 0, 0, 0};
+  if (x < F.nw) {
+    for (int c0 = pt; c0 < F.slabs; c0 += kFoldParts * 256) {
+      uint32_t ev = 0, od = 0;  // bytes 0, 2 / 1, 3 in 16-bit lanes
+      const int c1 = min(F.slabs, c0 + kFoldParts * 256);
+#pragma unroll 8
+      for (int c = c0; c < c1; c += kFoldParts) {
+        const uint32_t w = __ldcs(F.dump + (size_t)c * F.nw + x);
+        ev += w & 0x00FF00FFu;
+        od += (w >> 8) & 0x00FF00FFu;
+      }
+      s4[0] += ev & 0xFFFFu;
+      s4[1] += od & 0xFFFFu;
+      s4[2] += ev >> 16;
+      s4[3] += od >> 16;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) part[pt][wl][j] = s4[j];
+  __syncthreads();
+  if (pt >= 4 || x >= F.nw) return;
+  unsigned long long t = 0;
+#pragma unroll
+  for (int q = 0; q < kFoldParts; q++) t += part[q][wl][pt];
+  const uint32_t bin = 4 * x + pt;  // this thread alone owns the counter (the main kernel's repayments are done)
+  if (!F.fin) {
+    if (t) F.acc[bin] += t;
+    return;
+  }
+  t += F.acc[bin];
+  if (!t) return;
+  if (F.variant == 7) {  // acc index = 12 e + slot
+    const uint32_t e = bin / GPA_VALID_SLOTS, sl = bin - e * GPA_VALID_SLOTS;
+    const unsigned long long b = F.best[e];
+    if (!b) return;
+    const uint32_t i = F.gmap[0xFFFFFFFFu - (uint32_t)b];  // placed granules are mapped (k_sample_gran)
+    red_add_u64(F.H + ((uint64_t)i << 4 | sl), t);
+  } else {
+    if (bin >= F.thr[1]) return;
+    const uint32_t b = F.bin_of[bin];
+    if (b != NONE) red_add_u64(F.H + b, t);
+  }
+}
+
+// fill n 32-bit words at each of up to 4 ranges with a value (16-B aligned ranges)
+struct FillSet {
+  uint32_t *p[4];
+  uint64_t n[4];
+  uint32_t v[4];
+};
+__global__ void k_fill(FillSet F) {
+  const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const uint32_t v = F.v[j];
+    const uint4 v4 = make_uint4(v, v, v, v);
+    for (uint64_t x = gt; x < F.n[j] / 4; x += gs) reinterpret_cast<uint4 *>(F.p[j])[x] = v4;
+    for (uint64_t x = F.n[j] / 4 * 4 + gt; x < F.n[j]; x += gs) F.p[j][x] = v;
+  }
+}
+
 // ---- K_attr_probe: granule-keyed rows of byte counters, no global load in the record loop ---------
 // Each CTA holds a 2-way set-associative table of kProbeM granules (the key is the granule index
 // itself; set = (g ^ g >> 12) mod 4096, one 64-bit shared load returns both ways) and, per entry,
@@ -658,7 +783,7 @@ cudaError_t launch_bins(const AttrTables &T, const uint4 *rec, uint64_t n, unsig
 // outside the module into the extra row Hg[n_gran], which folds into U).  So the per-record path
 // reads the record from the TMA ring, probes the table and issues one shared atomic or one L2
 // reduction: no gather, no wait on global memory; the kernel is issue-bound, so the record path
-// is written for a small instruction count.  k_fold_probe / k_fold_gran then add acc and Hg into
+// is written for a small instruction count.  k_fold_all then adds the slabs, acc and Hg into
 // H (instruction = gmap[g]; gap granules -> U).  The table is chosen per call from a sample:
 // each set keeps its two most-sampled granules.
 constexpr int kProbeSetsLog = 12, kProbeSets = 1 << kProbeSetsLog;  // 4096 sets x 2 ways
@@ -688,7 +813,7 @@ __global__ void k_sample_gran(AttrTables T, const uint4 *__restrict__ rec, uint6
     uint64_t k = c * (n - kSampleChunk) / (chunks - 1) + o;
     uint4 v = ld_stream(rec + k);
     uint64_t g = ((((uint64_t)v.y << 32) | v.x) - T.base) >> T.gshift;
-    if (g < T.n_gran && (v.w & 0xFFFFu) < GPA_VALID_SLOTS && __ldg(T.gmap + g) != NONE) atomicAdd(gcnt + g, 1u);
+    sample_add(gcnt, g < T.n_gran && (v.w & 0xFFFFu) < GPA_VALID_SLOTS && __ldg(T.gmap + g) != NONE ? (uint32_t)g : NONE);
   }
 }
 
@@ -757,7 +882,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_probe(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint4 *__restrict__ rec, uint64_t n,
                  unsigned long long *__restrict__ Hg, uint32_t *__restrict__ rec_inst,
                  const unsigned long long *__restrict__ best, unsigned long long *__restrict__ acc,
-                 unsigned int *__restrict__ tile_ctr) {
+                 unsigned int *__restrict__ tile_ctr, uint32_t *__restrict__ dump) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane;
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
@@ -811,40 +936,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
-  for (uint32_t x = threadIdx.x; x < kProbeWords; x += NC * 32) {  // word x: bytes 4x .. 4x+3 = acc[4x ..]
-    const uint32_t word = cnt8[x];
-    if (!word) continue;
-#pragma unroll
-    for (int jb = 0; jb < 4; jb++) {
-      const uint32_t val = (word >> (8 * jb)) & 0xFFu;
-      if (val) red_add_u64_keep(acc + 4 * x + jb, val, keep);
-    }
-  }
-}
-
-// acc (per table entry x slot) -> H via the entry's granule and its instruction
-__global__ void k_fold_probe(const unsigned long long *__restrict__ acc, const unsigned long long *__restrict__ best,
-                             const uint32_t *__restrict__ gmap, unsigned long long *__restrict__ H) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (uint32_t)kProbeM * GPA_VALID_SLOTS) return;
-  const uint32_t e = t / GPA_VALID_SLOTS, s = t - e * GPA_VALID_SLOTS;
-  const unsigned long long v = acc[t];
-  const uint32_t g = best_gran(best[e]);
-  if (!v || g == kEmpty) return;
-  const uint32_t i = gmap[g];  // placed granules are mapped (k_sample_gran)
-  red_add_u64(H + ((uint64_t)i << 4 | s), v);
-}
-
-// Hg (granule x slot) -> H (gap granules and the out-of-module row n_gran -> U); 16 lanes per row
-__global__ void k_fold_gran(const unsigned long long *__restrict__ Hg, uint64_t n_gran, const uint32_t *__restrict__ gmap,
-                            unsigned long long *__restrict__ H, unsigned long long *__restrict__ U) {
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (n_gran + 1) * 16; t += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long v = Hg[t];
-    if (!v) continue;
-    const uint64_t g = t >> 4;
-    const uint32_t s = (uint32_t)(t & 15), i = g < n_gran ? __ldg(gmap + g) : NONE;
-    red_add_u64(i == NONE ? U + s : H + ((uint64_t)i << 4 | s), v);
-  }
+  dump_table<kProbeWords>(cnt8, kProbeWords, dump + (size_t)blockIdx.x * kProbeWords, NC * 32);  // word x: bytes = acc[4x ..]
 }
 
 // module span < 2^32 inside one aligned 4 GiB window (32-bit granule arithmetic)
@@ -873,7 +965,7 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     k_attr_code32(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint32_t *__restrict__ code,
                   const uint4 *__restrict__ rec, uint64_t n, unsigned long long *__restrict__ Hg,
                   uint32_t *__restrict__ rec_inst, unsigned long long *__restrict__ acc, const uint32_t *__restrict__ thr,
-                  unsigned int *__restrict__ tile_ctr) {
+                  unsigned int *__restrict__ tile_ctr, uint32_t *__restrict__ dump) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane, D = LOOK + 1;
   // PACK 0: bin idx in word idx % NW, byte idx / NW (NW a power of two: the consecutive bins of one
@@ -965,13 +1057,17 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   }
 done:
   asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
-  for (uint32_t x = threadIdx.x; x < nw; x += NC * 32) {
-    const uint32_t word = tab[x];
+  if (PACK) {
+    dump_table<NW>(tab, nw, dump + (size_t)blockIdx.x * NW, NC * 32);  // word x: bytes = acc[4x ..]
+  } else {
+    for (uint32_t x = threadIdx.x; x < nw; x += NC * 32) {
+      const uint32_t word = tab[x];
 #pragma unroll
-    for (int p = 0; p < 4; p++) {
-      const uint32_t val = (word >> (8 * p)) & 0xFFu;
-      const uint32_t bin = PACK ? 4 * x + p : (uint32_t)p * NW + x;
-      if (val && bin < nb) red_add_u64_keep(acc + bin, val, keep);
+      for (int p = 0; p < 4; p++) {
+        const uint32_t val = (word >> (8 * p)) & 0xFFu;
+        const uint32_t bin = (uint32_t)p * NW + x;
+        if (val && bin < nb) red_add_u64_keep(acc + bin, val, keep);
+      }
     }
   }
 }
@@ -1007,12 +1103,16 @@ using RingCode = Ring<GPA_CODE_NC, GPA_CODE_R, GPA_CODE_NST>;
 // chunks: the result is exact for every plan, only the speed depends on how well it fits ------------
 constexpr uint32_t kCodeK = (uint32_t)GPA_CODE_NW * 4;  // K_attr_code32 byte bins
 
-// records sampled to build a plan: n/256, at least 2^18, at most 2^21 for the probe table (7) and
+// records sampled to build a plan: n/256, at least 2^17, at most 2^21 for the probe table (7) and
 // 2^22 for the 131 072 byte bins of 8, whose ranking needs the finer counts (C5: 12.77 -> 12.7 ms;
 // C4 with 7 got slower with 2^22)
+// floor 2^17 (C2 1e7 records: 0.087 -> 0.083 ms against 2^18; 2^16 0.089; C3 0.324 -> 0.319 ms)
+#ifndef GPA_SAMPLE_MIN_LOG
+#define GPA_SAMPLE_MIN_LOG 17
+#endif
 static uint64_t plan_sample(uint64_t n, int variant) {
   const int cap = variant == 8 ? GPA_SAMPLE_MAX_LOG + 1 : GPA_SAMPLE_MAX_LOG;
-  return std::min<uint64_t>(1ull << cap, std::max<uint64_t>(1ull << 18, n / GPA_SAMPLE_DIV));
+  return std::min<uint64_t>(1ull << cap, std::max<uint64_t>(1ull << GPA_SAMPLE_MIN_LOG, n / GPA_SAMPLE_DIV));
 }
 
 size_t plan_bytes(const AttrTables &T, int variant) {
@@ -1020,66 +1120,169 @@ size_t plan_bytes(const AttrTables &T, int variant) {
   return ((size_t)kCodeK + 4 + T.n_gran) * 4;                                     // bin_of[K] | thr[4] | code[n_gran]
 }
 
-cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,
-                       int sm_count, cudaStream_t st) {
+// ---- host side of a call: few API calls (a mid-size call, C2's 1e7 records, is otherwise paced by
+// the host: ~20 allocations / memsets / launches took longer to issue than the GPU work they held) --
+static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+static uint32_t table_words(int variant) { return variant == 7 ? (uint32_t)kProbeWords : (uint32_t)GPA_CODE_NW; }
+
+// transient scratch of a plan build: gcnt[n_gran] (7) | scnt[n_inst*12] hot_info[n_inst] V[4096] (8)
+static size_t build_bytes(const AttrTables &T, int variant) {
+  if (variant == 7) return al256((size_t)T.n_gran * 4);
+  return al256(((size_t)T.n_inst * kHotSlots + T.n_inst + kVBins) * 4);
+}
+
+// accumulators of one call (or of all chunks of a host-records call): acc (per shared counter) |
+// Hg (granule x slot, + the out-of-module row) | one table slab per CTA | the dynamic tile counter
+static size_t acc_bytes(const AttrPlan &p, int sm_count) {
+  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  const size_t nh = (size_t)(p.n_gran + 1) * 128;
+  return al256(na + nh) + al256((size_t)sm_count * table_words(p.variant) * 4) + 256;
+}
+
+static void plan_ptrs(const AttrTables &T, int variant, void *mem, AttrPlan *p) {
   p->variant = variant;
   p->n_gran = T.n_gran;
-  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, plan_sample(n, variant) / kSampleChunk);
-  cudaError_t e;
   if (variant == 7) {
     p->best = reinterpret_cast<unsigned long long *>(mem);
-    uint32_t *gcnt = nullptr;
-    if ((e = pool_alloc((void **)&gcnt, T.n_gran * 4, st)) != cudaSuccess) return e;
-    cudaMemsetAsync(gcnt, 0, T.n_gran * 4, st);
-    cudaMemsetAsync(p->best, 0, (size_t)kProbeM * 8, st);
+  } else {
+    p->bin_of = reinterpret_cast<uint32_t *>(mem);
+    p->thr = p->bin_of + kCodeK;
+    p->code = p->thr + 4;
+  }
+}
+
+static void acc_ptrs(const AttrPlan &p, void *mem, int sm_count, AttrAcc *a) {
+  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  const size_t nh = (size_t)(p.n_gran + 1) * 128;
+  uint8_t *b = reinterpret_cast<uint8_t *>(mem);
+  a->acc = reinterpret_cast<unsigned long long *>(b);
+  a->Hg = a->acc + na / 8;
+  a->dump = reinterpret_cast<uint32_t *>(b + al256(na + nh));
+  a->slabs = sm_count;
+  a->ctr = reinterpret_cast<unsigned int *>(b + al256(na + nh) + al256((size_t)sm_count * table_words(p.variant) * 4));
+}
+
+struct Fills {
+  FillSet F{};
+  int k = 0;
+  void add(void *p, size_t words, uint32_t v) {
+    F.p[k] = reinterpret_cast<uint32_t *>(p);
+    F.n[k] = words;
+    F.v[k] = v;
+    k++;
+  }
+  cudaError_t launch(int sm_count, cudaStream_t st) {
+    k_fill<<<sm_count * 8, 256, 0, st>>>(F);
+    count_launches(1);
+    return cudaGetLastError();
+  }
+};
+
+static void build_fills(const AttrTables &T, const AttrPlan &p, void *w, Fills &f) {
+  if (p.variant == 7) {
+    f.add(w, T.n_gran, 0u);                      // gcnt
+    f.add(p.best, (size_t)kProbeM * 2, 0u);      // best
+  } else {
+    f.add(w, (size_t)T.n_inst * kHotSlots + T.n_inst + kVBins, 0u);  // scnt | hot_info | V
+    f.add(p.bin_of, kCodeK, 0xFFFFFFFFu);         // unassigned bins map to NONE
+  }
+}
+
+static void acc_fills(const AttrPlan &p, const AttrAcc &a, Fills &f) {
+  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  f.add(a.acc, (na + (size_t)(p.n_gran + 1) * 128) / 4, 0u);  // acc | Hg (the slabs are stored whole)
+  f.add(a.ctr, 4, 0u);
+}
+
+// the sample -> table kernels (scratch zeroed)
+static cudaError_t build_kernels(const AttrTables &T, const AttrPlan &p, const uint4 *rec, uint64_t n, void *w,
+                                 int sm_count, cudaStream_t st) {
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, plan_sample(n, p.variant) / kSampleChunk);
+  if (p.variant == 7) {
+    uint32_t *gcnt = reinterpret_cast<uint32_t *>(w);
     const unsigned gb = (unsigned)std::min<uint64_t>((T.n_gran + 255) / 256, (uint64_t)sm_count * 8);
     k_sample_gran<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, gcnt);
-    k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 0, p->best);
-    k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 1, p->best);
+    k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 0, p.best);
+    k_place<<<gb, 256, 0, st>>>(gcnt, T.n_gran, 1, p.best);
     count_launches(3);
-    e = cudaGetLastError();
-    cudaError_t e2 = cudaFreeAsync(gcnt, st);
-    return e != cudaSuccess ? e : e2;
+    return cudaGetLastError();
   }
-  // variant 8: scnt[n_inst*12] | hot_info[n_inst] | V[4096] transient; bin_of | thr | code kept
-  p->bin_of = reinterpret_cast<uint32_t *>(mem);
-  p->thr = p->bin_of + kCodeK;
-  p->code = p->thr + 4;
   const size_t ni = T.n_inst, nbins = ni * kHotSlots;
-  uint32_t *w = nullptr;
-  if ((e = pool_alloc((void **)&w, (nbins + ni + kVBins) * 4, st)) != cudaSuccess) return e;
-  uint32_t *scnt = w, *hot_info = w + nbins, *V = hot_info + ni;
-  cudaMemsetAsync(scnt, 0, nbins * 4, st);
-  cudaMemsetAsync(V, 0, kVBins * 4, st);
-  cudaMemsetAsync(p->bin_of, 0xFF, (size_t)kCodeK * 4, st);
+  uint32_t *scnt = reinterpret_cast<uint32_t *>(w), *hot_info = scnt + nbins, *V = hot_info + ni;
   k_sample_bins<<<sm_count * 4, 256, 0, st>>>(T, rec, n, chunks, scnt);
   k_vhist<<<sm_count, 1024, 0, st>>>(scnt, (uint32_t)nbins, V);
-  k_pick<<<1, 1024, 0, st>>>(V, p->thr, kCodeK);
-  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, p->thr, hot_info, p->bin_of, kCodeK);
-  k_codemap32<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, p->code);
+  k_pick<<<1, 1024, 0, st>>>(V, p.thr, kCodeK);
+  k_assign_bins<<<sm_count * 2, 256, 0, st>>>(scnt, (uint32_t)ni, p.thr, hot_info, p.bin_of, kCodeK);
+  k_codemap32<<<sm_count * 4, 256, 0, st>>>(T.gmap, T.n_gran, hot_info, p.code);
   count_launches(5);
-  e = cudaGetLastError();
+  return cudaGetLastError();
+}
+
+cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,
+                       int sm_count, cudaStream_t st) {
+  plan_ptrs(T, variant, mem, p);
+  void *w = nullptr;
+  cudaError_t e = pool_alloc(&w, build_bytes(T, variant), st);
+  if (e != cudaSuccess) return e;
+  Fills f;
+  build_fills(T, *p, w, f);
+  e = f.launch(sm_count, st);
+  if (e == cudaSuccess) e = build_kernels(T, *p, rec, n, w, sm_count, st);
   cudaError_t e2 = cudaFreeAsync(w, st);
   return e != cudaSuccess ? e : e2;
 }
 
-// accumulators of one call (or of all chunks of a host-records call): acc (per shared counter) |
-// Hg (granule x slot, + the out-of-module row), zeroed
-cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, cudaStream_t st) {
-  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
-  const size_t nh = (size_t)(p.n_gran + 1) * 128;
-  cudaError_t e = pool_alloc((void **)&a->acc, na + nh + 16, st);
+cudaError_t plan_begin(const AttrPlan &p, AttrAcc *a, int sm_count, cudaStream_t st) {
+  void *mem = nullptr;
+  cudaError_t e = pool_alloc(&mem, acc_bytes(p, sm_count), st);
   if (e != cudaSuccess) return e;
-  a->Hg = a->acc + na / 8;
-  a->ctr = reinterpret_cast<unsigned int *>(a->Hg + nh / 8);
-  return cudaMemsetAsync(a->acc, 0, na + nh, st);
+  acc_ptrs(p, mem, sm_count, a);
+  Fills f;
+  acc_fills(p, *a, f);
+  return f.launch(sm_count, st);
 }
 
-cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
-                     uint32_t *ri, int sm_count, cudaStream_t st) {
+// cudaFuncSetAttribute once per kernel and device (it costs a few microseconds of host time per call)
+template <class K>
+static cudaError_t smem_attr_once(K kern, size_t smem, int slot) {
+  static std::atomic<uint64_t> done[4];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done[slot].load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[slot].fetch_or(bit, std::memory_order_relaxed);
+  return e;
+}
+
+static FoldArgs fold_args(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, int slabs, int fin,
+                          unsigned long long *H, unsigned long long *U) {
+  FoldArgs F{};
+  F.dump = a.dump;
+  F.nw = table_words(p.variant);
+  F.tb = (F.nw + 31) / 32;
+  F.slabs = slabs;
+  F.fin = fin;
+  F.variant = p.variant;
+  F.acc = a.acc;
+  F.ctr = a.ctr;
+  F.best = p.best;
+  F.bin_of = p.bin_of;
+  F.thr = p.thr;
+  F.gmap = T.gmap;
+  F.Hg = a.Hg;
+  F.n_gran = T.n_gran;
+  F.H = H;
+  F.U = U;
+  return F;
+}
+
+// one launch of the main kernel; fold != 0: its slabs -> acc (and the tile counter reset) right away,
+// as every launch of a multi-launch call must; a single-launch call leaves them to plan_end
+static cudaError_t plan_launch(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
+                               uint32_t *ri, int sm_count, cudaStream_t st, bool fold) {
   if (n == 0) return cudaSuccess;
-  cudaError_t e0 = cudaMemsetAsync(a.ctr, 0, sizeof(unsigned int), st);  // the dynamic tile counter of this launch
-  if (e0 != cudaSuccess) return e0;
   const ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift,
                     (uint32_t)T.n_gran, (uint32_t)g_ring_stress.load(std::memory_order_relaxed)};
   cudaError_t e;
@@ -1087,51 +1290,72 @@ cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, c
     using RG = RingProbe;
     auto kern = ri ? k_attr_probe<RG, true> : k_attr_probe<RG, false>;
     const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
-    // dynamic tile order for the probe kernel (C4: 2.82 -> 2.71 ms)
-    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, p.best, a.acc, a.ctr);
+    if ((e = smem_attr_once(kern, smem, ri ? 1 : 0)) != cudaSuccess) return e;
+    // dynamic tile order for the probe kernel (C4: 2.82 -> 2.71 ms); the counter is zero here
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, p.best, a.acc, a.ctr, a.dump);
   } else {
     using RG = RingCode;
     auto kern = ri ? k_attr_code32<RG, GPA_CODE_NW, GPA_CODE_PACK, true, GPA_CODE_LOOK>
                    : k_attr_code32<RG, GPA_CODE_NW, GPA_CODE_PACK, false, GPA_CODE_LOOK>;
     const size_t smem = RG::kBytes + (size_t)GPA_CODE_NW * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    if ((e = smem_attr_once(kern, smem, ri ? 3 : 2)) != cudaSuccess) return e;
     // static tile order for the code-map kernel (C5: 12.54 ms vs 13.16 ms with the dynamic order)
-    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, p.code, rec, n, a.Hg, ri, a.acc, p.thr, nullptr);
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, p.code, rec, n, a.Hg, ri, a.acc, p.thr, nullptr, a.dump);
   }
+  count_launches(1);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (fold && (p.variant == 7 || GPA_CODE_PACK)) {
+    const FoldArgs F = fold_args(T, p, a, sm_count, 0, nullptr, nullptr);
+    k_fold_all<<<F.tb, kFoldParts * 32, 0, st>>>(F);
+    count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t plan_run(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, const uint4 *rec, uint64_t n,
+                     uint32_t *ri, int sm_count, cudaStream_t st) {
+  return plan_launch(T, p, a, rec, n, ri, sm_count, st, true);
+}
+
+// fold the accumulators (+ `slabs` table slabs not yet folded) into H / U in one launch
+static cudaError_t plan_fold_final(const AttrTables &T, const AttrPlan &p, const AttrAcc &a, int slabs,
+                                   unsigned long long *H, unsigned long long *U, int sm_count, cudaStream_t st) {
+  const FoldArgs F = fold_args(T, p, a, slabs, 1, H, U);
+  const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
+  k_fold_all<<<F.tb + (unsigned)b2, kFoldParts * 32, 0, st>>>(F);
   count_launches(1);
   return cudaGetLastError();
 }
 
-// fold the accumulators into H / U and release them
 cudaError_t plan_end(const AttrTables &T, const AttrPlan &p, AttrAcc *a, unsigned long long *H, unsigned long long *U,
                      int sm_count, cudaStream_t st) {
-  if (p.variant == 7) k_fold_probe<<<(kProbeM * GPA_VALID_SLOTS + 255) / 256, 256, 0, st>>>(a->acc, p.best, T.gmap, H);
-  else k_fold_acc<<<(kCodeK + 255) / 256, 256, 0, st>>>(a->acc, p.bin_of, p.thr, kCodeK, H);
-  const uint64_t b2 = std::min<uint64_t>(((T.n_gran + 1) * 16 + 255) / 256, (uint64_t)sm_count * 16);
-  k_fold_gran<<<(unsigned)b2, 256, 0, st>>>(a->Hg, T.n_gran, T.gmap, H, U);
-  count_launches(2);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = plan_fold_final(T, p, *a, 0, H, U, sm_count, st);
   cudaError_t e2 = cudaFreeAsync(a->acc, st);
   a->acc = a->Hg = nullptr;
   return e != cudaSuccess ? e : e2;
 }
 
-// one call with a transient plan built from the call's own records
+// one call with a transient plan built from the call's own records: one allocation, one fill, the
+// plan kernels, the main kernel and one fold
 cudaError_t launch_planned(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, unsigned long long *H,
                            unsigned long long *U, uint32_t *ri, int sm_count, cudaStream_t st) {
-  void *mem = nullptr;
-  cudaError_t e = pool_alloc(&mem, plan_bytes(T, variant), st);
-  if (e != cudaSuccess) return e;
   AttrPlan p;
+  p.variant = variant;
+  p.n_gran = T.n_gran;
+  const size_t b0 = al256(plan_bytes(T, variant)), b1 = build_bytes(T, variant), b2 = acc_bytes(p, sm_count);
+  uint8_t *mem = nullptr;
+  cudaError_t e = pool_alloc((void **)&mem, b0 + b1 + b2, st);
+  if (e != cudaSuccess) return e;
+  plan_ptrs(T, variant, mem, &p);
   AttrAcc a;
-  e = plan_build(T, variant, rec, n, mem, &p, sm_count, st);
-  if (e == cudaSuccess) e = plan_begin(p, &a, st);
-  if (e == cudaSuccess) {
-    e = plan_run(T, p, a, rec, n, ri, sm_count, st);
-    cudaError_t e3 = plan_end(T, p, &a, H, U, sm_count, st);
-    if (e == cudaSuccess) e = e3;
-  }
+  acc_ptrs(p, mem + b0 + b1, sm_count, &a);
+  Fills f;
+  build_fills(T, p, mem + b0, f);
+  acc_fills(p, a, f);
+  e = f.launch(sm_count, st);
+  if (e == cudaSuccess) e = build_kernels(T, p, rec, n, mem + b0, sm_count, st);
+  if (e == cudaSuccess) e = plan_launch(T, p, a, rec, n, ri, sm_count, st, false);
+  if (e == cudaSuccess) e = plan_fold_final(T, p, a, (p.variant == 7 || GPA_CODE_PACK) ? sm_count : 0, H, U, sm_count, st);
   cudaError_t e2 = cudaFreeAsync(mem, st);
   return e != cudaSuccess ? e : e2;
 }

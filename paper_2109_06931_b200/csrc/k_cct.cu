@@ -766,6 +766,57 @@ __global__ void k_block_counts(uint32_t n_blocks, const uint32_t *__restrict__ s
 //   B  block 0 scans the per-block totals -> the next level's size
 //   C  every block writes its chunk's children at b + block offset + local offset
 // then excl for every context, then incl level by level from the deepest.
+// Dataflow incl fold (no level barriers).  The excl pass computes excl for every (context, slot)
+// and zeroes the context's arrival counter; then the 16 lanes (slots) of each leaf context store
+// incl = excl and climb: after their stores they count their context in at the parent (fence +
+// one atomic per context); the child that arrives last (count == the parent's n_children)
+// computes the parent's incl = excl + the children's incl in index order -- the same fp64
+// operations in the same order as the level fold and the oracle, so the result is bit-identical --
+// and climbs on.  No thread ever waits for another, so there is no deadlock; the critical path is
+// one store-fence-atomic-load round trip per tree level instead of a barrier plus the level's loads.
+// Threads x = 16 c + r: the 16 lanes of a half-warp hold one context (blockDim and strides are
+// multiples of 16).
+__device__ __forceinline__ double excl_of(const LevelArgs &A, const uint64_t *__restrict__ S_f, uint64_t c, int r) {
+  const uint8_t k = A.kind[c];
+  if (k == GPA_CTX_SCC) return 0.0;  // excl (R14)
+  const uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
+  return __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
+}
+
+// climb from context c (lane r of its half-warp) with incl(c) = v; returns when this half-warp is
+// not the last arrival at an ancestor, or after storing a root's incl
+__device__ __forceinline__ void fold_climb(const LevelArgs &A, const double *__restrict__ excl, double *incl,
+                                           uint32_t *arrived, uint32_t c, uint32_t r, double v) {
+  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
+  for (;;) {
+    const uint32_t p = A.parent[c];
+    uint32_t nc = 0, d0 = 0;
+    if (p != NONE) {
+      nc = A.n_children[p];
+      d0 = A.first_child[p];
+    }
+    __stcg(incl + (uint64_t)c * GPA_SLOTS + r, v);
+    if (p == NONE) return;
+    __threadfence();
+    __syncwarp(hmask);
+    uint32_t last = 0;
+    if (r == 0) last = atomicAdd(arrived + p, 1u) + 1u == nc;
+    last = __shfl_sync(hmask, last, 0, 16);
+    if (!last) return;
+    __threadfence();  // every sibling's incl is visible (each fenced before its context was counted in)
+    v = __ldcg(excl + (uint64_t)p * GPA_SLOTS + r);
+    const double *ci = incl + (uint64_t)d0 * GPA_SLOTS + r;
+    uint32_t d = 0;
+    for (; d + 4 <= nc; d += 4) {  // four loads in flight, added in index order
+      const double a0 = __ldcg(ci + (uint64_t)d * GPA_SLOTS), a1 = __ldcg(ci + (uint64_t)(d + 1) * GPA_SLOTS);
+      const double a2 = __ldcg(ci + (uint64_t)(d + 2) * GPA_SLOTS), a3 = __ldcg(ci + (uint64_t)(d + 3) * GPA_SLOTS);
+      v = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(v, a0), a1), a2), a3);
+    }
+    for (; d < nc; d++) v = __dadd_rn(v, __ldcg(ci + (uint64_t)d * GPA_SLOTS));
+    c = p;
+  }
+}
+
 namespace cg = cooperative_groups;
 constexpr int kCoopThreads = 512;
 
@@ -834,19 +885,12 @@ __global__ void __launch_bounds__(kCoopThreads) k_cct_coop(LevelArgs A, uint32_t
     grid.sync();
   }
   const uint64_t gt = (uint64_t)bi * nt + t, gs = (uint64_t)B * nt;
-  for (uint64_t x = gt; x < n_total * GPA_SLOTS; x += gs) {  // excl (R14)
-    uint64_t c = x >> 4;
-    int r = (int)(x & 15);
-    uint8_t k = A.kind[c];
-    double v = 0.0;
-    if (k != GPA_CTX_SCC) {
-      uint32_t g = k == GPA_CTX_SCC_MEMBER ? A.node[c] : A.dmem[A.dmem_ptr[A.node[c]]];
-      v = __dmul_rn(A.frac[c], __ull2double_rn(S_f[(uint64_t)g * GPA_SLOTS + r]));
-    }
-    excl[x] = v;
-  }
+  for (uint64_t x = gt; x < n_total * GPA_SLOTS; x += gs) excl[x] = excl_of(A, S_f, x >> 4, (int)(x & 15));
   grid.sync();
-  for (int l = (int)L - 1; l >= 0; l--) {  // incl: deepest level first, children in order
+  // incl: deepest level first, children in order.  (The dataflow fold of the small trees, fold_climb,
+  // measured 4.4x slower here: with millions of contexts each thread walks hundreds of leaves, and
+  // every climb step is a serial store-fence-atomic round trip, while a level pass is bandwidth-bound.)
+  for (int l = (int)L - 1; l >= 0; l--) {
     for (uint64_t x = (uint64_t)lev[l] * GPA_SLOTS + gt; x < (uint64_t)lev[l + 1] * GPA_SLOTS; x += gs) {
       uint64_t c = x >> 4;
       int r = (int)(x & 15);
@@ -927,6 +971,25 @@ __global__ void __launch_bounds__(1024) k_cct_fold_cl(LevelArgs A, const uint32_
     }
     cl.sync();
   }
+}
+
+__global__ void k_cct_excl_lev(LevelArgs A, const uint32_t *__restrict__ lev, const uint64_t *__restrict__ S_f,
+                               double *__restrict__ excl, uint32_t *__restrict__ arrived) {
+  const uint64_t n = lev[1 + lev[0]];
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n * GPA_SLOTS; x += (uint64_t)gridDim.x * blockDim.x) {
+    excl[x] = excl_of(A, S_f, x >> 4, (int)(x & 15));
+    if ((x & 15) == 0) arrived[x >> 4] = 0;
+  }
+}
+
+__global__ void k_cct_fold_up(LevelArgs A, const uint32_t *__restrict__ lev, const double *__restrict__ excl,
+                              double *incl, uint32_t *arrived) {
+  const uint64_t n = lev[1 + lev[0]];
+  const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n * GPA_SLOTS) return;
+  const uint32_t c = (uint32_t)(x >> 4);
+  if (A.n_children[c] != 0) return;
+  fold_climb(A, excl, incl, arrived, c, (uint32_t)(x & 15), excl[x]);
 }
 
 unsigned grid_for(uint64_t work, unsigned threads) {
@@ -1109,6 +1172,17 @@ cudaError_t launch_cct_small(const gpa_structure_s *s, gpa_cct_s *c, uint32_t *d
   const uint32_t *lev = d_lev;
   const uint64_t *S_f = c->S_f;
   double *excl = c->excl, *incl = c->incl;
+  static const bool level_fold = getenv("GPA_CCT_LEVEL_FOLD") != nullptr;  // A/B switch: the cluster level fold
+  if (!level_fold) {  // dataflow fold over every (context, slot) of the capacity c->n
+    uint32_t *arrived = nullptr;
+    if ((e = pool_alloc((void **)&arrived, c->n * 4, st)) != cudaSuccess) return e;
+    k_cct_excl_lev<<<grid_for(c->n * GPA_SLOTS, 256), 256, 0, st>>>(A, lev, S_f, excl, arrived);
+    k_cct_fold_up<<<(unsigned)((c->n * GPA_SLOTS + 255) / 256), 256, 0, st>>>(A, lev, excl, incl, arrived);
+    count_launches(2);
+    e = cudaGetLastError();
+    cudaError_t e2 = cudaFreeAsync(arrived, st);
+    return e != cudaSuccess ? e : e2;
+  }
   // largest cluster the device accepts for k_cct_fold_cl (16, else 8); 0 = none (cooperative grid)
   static std::atomic<int> cluster{-1};
   int cs0 = cluster.load(std::memory_order_relaxed);

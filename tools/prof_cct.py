@@ -34,3 +34,16 @@ for r in range(reps):
     torch.cuda.synchronize()
     print(f"rep {r}: {c.n} contexts, gpu {e0.elapsed_time(e1):.3f} ms, host {(time.perf_counter() - t0) * 1e3:.3f} ms")
     c.free()
+if os.environ.get("TRACE"):
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        c = gpa.reconstruct_cct(s, H)
+        cm = torch.empty((max(c.n, 1), 33), dtype=torch.float64, device="cuda")
+        gpa.derive_metrics(s, "CCT_EXCL", cct=c, metrics=cm)
+        gpa.derive_metrics(s, "CCT_INCL", cct=c, metrics=cm)
+        torch.cuda.synchronize()
+    ev = sorted((e for e in prof.events() if e.device_type.name == "CUDA"), key=lambda e: e.time_range.start)
+    t0 = ev[0].time_range.start if ev else 0
+    for e in ev:
+        print(f"  {e.time_range.start - t0:9.1f} us  {e.time_range.end - e.time_range.start:8.1f} us  {e.name[:90]}")
+    c.free()
