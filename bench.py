@@ -299,41 +299,78 @@ def run_gpa(args):
                 dist.reduce(x.SW, dst=0)
                 if rank == 0:
                     cct = gpa.reconstruct_cct_inputs(s, x.SF, x.CW, stream=B)
+            elif rank == 0 and async_cct:
+                cct = gpa.reconstruct_cct_async(s, x.H, stream=B)   # no host synchronization
             elif rank == 0:
                 cct = gpa.reconstruct_cct(s, x.H, stream=B)
             if cct is not None:
-                cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+                if cct.pending:  # metrics rows = the capacity; the kernels read the size on the device
+                    if cm_async[0] is None or cm_async[0].shape[0] < cct.capacity:
+                        cm_async[0] = torch.empty((cct.capacity, gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+                    cm = cm_async[0]
+                else:
+                    cm = torch.empty((max(cct.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
                 gpa.derive_metrics(s, "CCT_EXCL", cct=cct, metrics=cm, stream=B)
                 gpa.derive_metrics(s, "CCT_INCL", cct=cct, metrics=cm, stream=B)
                 if timed:
                     ce = torch.cuda.Event(enable_timing=True)
                     ce.record(B)
                     ev_c1.append(ce)
-                nctx = cct.n
+                nctx = cct if cct.pending else cct.n
             if do_scopes:
                 B.wait_stream(side)
             if results is not None:      # e2e: read the batch's results back to the host
                 for dst, src in results(x):
                     dst.copy_(src, non_blocking=True)
             x.freed.record(B)
-            if cct is not None:
+            if cct is not None and not cct.pending:
                 cct.free()               # stream-ordered on B
         return nctx
 
     pipeline = args.pipeline
+    # CCT without a host round trip inside the step (gpa_reconstruct_cct_async); --sync-cct for
+    # the synchronous call
+    async_cct = world == 1 and not args.sync_cct
+    cm_async = [None]
 
     def run_steps(k: int, timed: bool, host=None, results=None):
-        """k batches; pipelined: attribution of i + 1 is enqueued before the analysis of i."""
-        nctx = 0
+        """k batches; pipelined: attribution of i + 1 is enqueued before the analysis of i.
+        An asynchronous tree is finished when the next batch's attribution is already queued (the
+        host waits for the tree while the GPU attributes; a tree the one-launch build could not
+        hold is rebuilt there and its metrics derived again, on B, inside the timed region)."""
+        nctx, last = 0, None
+
+        def settle():
+            nonlocal last
+            n = 0
+            if last is not None:
+                c, last = last, None
+                if c.finish():
+                    for sc in ("CCT_EXCL", "CCT_INCL"):
+                        m = torch.empty((max(c.n, 1), gpa.NUM_DERIVED), dtype=torch.float64, device=dev)
+                        gpa.derive_metrics(s, sc, cct=c, metrics=m, stream=B)
+                n = c.n
+                c.free()
+            return n
+
+        def keep(r):
+            nonlocal last
+            if isinstance(r, gpa.Cct):
+                last = r
+                return 0
+            return r
+
         for i in range(k):
             enqueue_attr(i, timed, host)
+            nctx = settle() or nctx
             if not pipeline:
-                nctx = analyse(i, timed, results)
+                nctx = keep(analyse(i, timed, results))
             elif i > 0:
-                nctx = analyse(i - 1, timed, results)
+                nctx = keep(analyse(i - 1, timed, results))
         if pipeline and k > 0:
-            nctx = analyse(k - 1, timed, results)
-        return nctx
+            nctx = settle() or nctx
+            nctx = keep(analyse(k - 1, timed, results))
+        return settle() or nctx
 
     nctx = run_steps(args.warmup, False)
     torch.cuda.synchronize()
@@ -530,6 +567,7 @@ def main():
     ap.add_argument("--combine", default="scatter", choices=["scatter", "reduce"],
                     help="N > 1: reduce-scatter + per-rank roll-ups (default) or reduce to rank 0")
     ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
+    ap.add_argument("--sync-cct", action="store_true", help="synchronous gpa_reconstruct_cct (A/B of the async tree)")
     ap.add_argument("--pipeline", action="store_true",
                     help="enqueue batch i+1's attribution before batch i's analysis (measured slower; DESIGN.md §7)")
     ap.add_argument("--e2e-steps", type=int, default=0)

@@ -362,6 +362,22 @@ GPA_API gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_h
  * clipped).  Enqueue-only. */
 GPA_API gpa_status gpa_block_counts(gpa_structure s, uint32_t n_blocks, const uint32_t *d_block_start,
                                     const uint64_t *d_counts, uint64_t *d_inst_hist, gpa_stream_t stream);
+/* The same tree without a host synchronization (for a pipeline of batches: P:711-714 statistics
+ * generated per batch while the next batch is attributed).  The tree is built in one launch into
+ * *capacity context slots (the static path bound when it is small, else 2^16); its size stays on
+ * the device.  Until gpa_cct_finish: gpa_derive_metrics with GPA_SCOPE_CCT_EXCL / _INCL writes the
+ * rows of the built contexts only (d_metrics must hold *capacity rows; none when the build did
+ * not fit); gpa_get_cct_view and gpa_cct_profiles fail with GPA_ERR_INVALID_ARG.  d_inst_hist must
+ * stay unchanged until gpa_cct_finish (an overflowing build is redone from it).  Enqueue-only,
+ * except structures whose trees the one-launch build cannot hold at all: then as
+ * gpa_reconstruct_cct (synchronizes; *capacity = the context count, the tree finished). */
+GPA_API gpa_status gpa_reconstruct_cct_async(gpa_structure s, const uint64_t *d_inst_hist, gpa_weight_mode mode,
+                                             gpa_cct *out, uint64_t *capacity, gpa_stream_t stream);
+/* Completes an asynchronous tree: synchronizes its stream and sets *n_contexts.  If the one-launch
+ * build did not fit its capacity the tree is rebuilt with the counted path (synchronously, same
+ * result as gpa_reconstruct_cct) and *rebuilt = 1 (may be NULL): CCT metrics derived before must
+ * be derived again.  A finished or synchronous tree: *n_contexts = its size, *rebuilt = 0. */
+GPA_API gpa_status gpa_cct_finish(gpa_cct c, uint64_t *n_contexts, int *rebuilt);
 GPA_API gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *out);
 /* Releases the tree's device memory in stream order on the stream gpa_reconstruct_cct was
  * called with (no device synchronization); work on other streams that still reads the views

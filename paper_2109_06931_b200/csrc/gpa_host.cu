@@ -880,9 +880,10 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
 
 // Steps 1-4 from the instruction histogram (d_inst_hist) or from precomputed Step-1
 // inputs (d_func_hist = S_f, d_call_weight = w; gpa_reconstruct_cct_inputs)
+// async_: the one-launch build is left pending (no synchronization; gpa_cct_finish reads the size)
 static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d_inst_hist, const uint64_t *d_func_hist,
                               const uint64_t *d_call_weight, gpa_weight_mode mode, uint64_t max_contexts, gpa_cct *out,
-                              uint64_t *n_contexts, gpa_stream_t stream) {
+                              uint64_t *n_contexts, gpa_stream_t stream, bool async_ = false) {
   if (!s || !n_contexts || (max_contexts && !out)) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
   if (mode != GPA_WEIGHTS_SAMPLES && mode != GPA_WEIGHTS_EXACT) return fail(GPA_ERR_INVALID_ARG, "mode %d", (int)mode);
   if (out) *out = nullptr;
@@ -937,6 +938,16 @@ static gpa_status reconstruct(gpa_structure s, bool from_hist, const uint64_t *d
                        carve(&c->incl, nb * SLOTS), carve(&d_lev, 1100)}));
     c->d_lev = d_lev; c->lev_fmt = 1; c->lev_len = 1100;
     CC(launch_cct_small(s, c, d_lev, d_cnt + 1, sm_count(s->device), st));
+    if (async_) {  // gpa_reconstruct_cct_async: size (and a fall-back rebuild) left to gpa_cct_finish
+      c->pending = true;
+      c->d_built = d_cnt + 1;
+      c->src = s;
+      c->src_hist = d_inst_hist;
+      c->src_mode = (int)mode;
+      *n_contexts = nb;
+      *out = c;
+      return GPA_OK;
+    }
     CC(cudaMemcpyAsync(h_cnt + 1, d_cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CC(cudaStreamSynchronize(st));
     if (h_cnt[1] > nb && small_static) {
@@ -1132,6 +1143,7 @@ static gpa_status cct_levels(gpa_cct_s *c) {
 gpa_status gpa_cct_profiles(gpa_structure s, gpa_cct cct, const uint64_t *d_prof_hist, uint32_t n_profiles,
                             double *d_prof_excl, double *d_prof_incl, gpa_stream_t stream) {
   if (!s || !cct) return fail(GPA_ERR_INVALID_ARG, "NULL handle");
+  if (cct->pending) return fail(GPA_ERR_INVALID_ARG, "asynchronous tree: call gpa_cct_finish first");
   if (cct->n == 0) return GPA_OK;
   if (!d_prof_hist || !d_prof_excl || !d_prof_incl) return fail(GPA_ERR_INVALID_ARG, "NULL buffer");
   if (n_profiles > 65536) return fail(GPA_ERR_INVALID_ARG, "n_profiles %u > 65536", n_profiles);
@@ -1377,8 +1389,49 @@ gpa_status gpa_reconstruct_cct(gpa_structure s, const uint64_t *d_inst_hist, gpa
   return reconstruct(s, true, d_inst_hist, nullptr, nullptr, mode, max_contexts, out, n_contexts, stream);
 }
 
+gpa_status gpa_reconstruct_cct_async(gpa_structure s, const uint64_t *d_inst_hist, gpa_weight_mode mode, gpa_cct *out,
+                                     uint64_t *capacity, gpa_stream_t stream) {
+  if (s && !d_inst_hist && s->info.n_inst) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist is NULL");
+  if ((uintptr_t)d_inst_hist & 15) return fail(GPA_ERR_INVALID_ARG, "d_inst_hist must be 16-byte aligned");
+  if (!out || !capacity) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  return reconstruct(s, true, d_inst_hist, nullptr, nullptr, mode, ~0ull, out, capacity, stream, true);
+}
+
+gpa_status gpa_cct_finish(gpa_cct c, uint64_t *n_contexts, int *rebuilt) {
+  if (!c || !n_contexts) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if (rebuilt) *rebuilt = 0;
+  if (!c->pending) {
+    *n_contexts = c->n;
+    return GPA_OK;
+  }
+  DeviceGuard g(c->device);
+  CU(g.err);
+  unsigned long long built = 0;
+  CU(cudaMemcpyAsync(&built, c->d_built, sizeof built, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (built <= c->n) {
+    c->n = built;
+    c->pending = false;
+    *n_contexts = built;
+    return GPA_OK;
+  }
+  if (c->src->info.cct_path_bound <= c->n)
+    return fail(GPA_ERR_INTERNAL, "tree exceeds the static bound %llu", (unsigned long long)c->n);
+  // the one-launch build did not fit its capacity: the counted build, on the same inputs and stream
+  gpa_cct c2 = nullptr;
+  uint64_t n2 = 0;
+  CHECK(reconstruct(c->src, true, c->src_hist, nullptr, nullptr, (gpa_weight_mode)c->src_mode, ~0ull, &c2, &n2,
+                    c->stream));
+  std::swap(*c, *c2);
+  free_cct(c2);  // the arrays of the pending build
+  *n_contexts = c->n;
+  if (rebuilt) *rebuilt = 1;
+  return GPA_OK;
+}
+
 gpa_status gpa_get_cct_view(gpa_cct c, gpa_cct_view *v) {
   if (!c || !v) return fail(GPA_ERR_INVALID_ARG, "NULL argument");
+  if (c->pending) return fail(GPA_ERR_INVALID_ARG, "asynchronous tree: call gpa_cct_finish first");
   v->n = c->n;
   v->parent = c->parent; v->site = c->site; v->node = c->node; v->kind = c->kind;
   v->first_child = c->first_child; v->n_children = c->n_children;
@@ -1403,7 +1456,9 @@ gpa_status gpa_derive_metrics(gpa_structure s, gpa_scope scope, const uint64_t *
     if (!cct) return fail(GPA_ERR_INVALID_ARG, "CCT scope without a cct");
     if (d_scope_hist || d_scope_mix) return fail(GPA_ERR_INVALID_ARG, "CCT rows have no u64 histogram or mix");
     if (!d_metrics || cct->n == 0) return GPA_OK;
-    CU(launch_derive_f64(scope == GPA_SCOPE_CCT_EXCL ? cct->excl : cct->incl, cct->n, d_metrics, st));
+    // a pending (asynchronous) tree: rows = the size on the device, d_metrics holds the capacity
+    CU(launch_derive_f64(scope == GPA_SCOPE_CCT_EXCL ? cct->excl : cct->incl, cct->n, d_metrics, st,
+                         cct->pending ? cct->d_built : nullptr));
     return GPA_OK;
   }
   int k = scope == GPA_SCOPE_LINE ? ROLL_LINE : scope == GPA_SCOPE_LOOP ? ROLL_LOOP

@@ -138,6 +138,13 @@ struct gpa_cct_s {
   int lev_fmt = 0;
   uint32_t lev_len = 0;
   std::vector<void *> allocs;
+  // gpa_reconstruct_cct_async: built into n (= capacity) slots, the size still on the device
+  // (*d_built: contexts, or ~0 when the one-launch build did not fit) until gpa_cct_finish
+  bool pending = false;
+  unsigned long long *d_built = nullptr;
+  gpa_structure src = nullptr;       // the inputs a counted rebuild needs (overflow only)
+  const uint64_t *src_hist = nullptr;
+  int src_mode = 0;
 };
 
 // ---- kernel launch accounting (gpa_kernel_launches) ------------------------------------------
@@ -192,7 +199,8 @@ cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_h
 // w_e = sum_{r<12} H[call_inst[e]][r] for the call sites whose call instruction lies in [lo, hi)
 cudaError_t launch_cct_weights_range(const gpa_structure_s *s, const uint64_t *d_hist, uint32_t lo, uint32_t hi,
                                      uint64_t *d_w, cudaStream_t st);
-cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st);
+cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st,
+                              const unsigned long long *d_rows = nullptr);
 // all scope kinds in one launch: INST rows [ident_lo, ident_lo + n_ident) and merged chunks [c0, c1),
 // multi rows [m0, m1); outputs indexed by gpa_scope (0 INST .. 4 FUNC), NULL = not produced
 cudaError_t launch_rollup_multi(const MultiRoll &M, uint32_t c0, uint32_t c1, uint32_t m0, uint32_t m1, uint32_t ident_lo,

@@ -38,6 +38,15 @@
 #include "gpa_internal.cuh"
 #include "kern_common.cuh"
 
+// record paths: predicated atomics instead of hot / cold branches (1) or branches (0); K_attr_code32
+// measured 12.25 / 12.12 ms with branches against 12.38 / 12.40 ms predicated (C5, same box)
+#ifndef GPA_CODE_PRED
+#define GPA_CODE_PRED 0
+#endif
+#ifndef GPA_PROBE_PRED
+#define GPA_PROBE_PRED 0
+#endif
+
 namespace gpa {
 namespace {
 
@@ -855,6 +864,13 @@ __device__ __forceinline__ void probe_record(const ProbeArgs &A, uint4 v, bool l
   const uint32_t baddr = set * (2 * kProbeRowBytes) + (w1 ? (uint32_t)kProbeRowBytes : 0u) + st16;
   const uint32_t sh = (baddr << 3) & 24u;
   const uint32_t delta = cnt << sh;
+  if (GPA_PROBE_PRED) {  // straight-line: predicated shared atomic / L2 reduction, a carry (rare) branches
+    const uint32_t old = atoms_add_if(hot, cnt_s + (baddr & ~3u), delta, 0u);
+    const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
+    red_add_u64_if(live && !hot, Hg + ((uint64_t)g * GPA_SLOTS + slot), cnt, keep);
+    if (hot && ((old >> sh) & 0xFFu) + cnt > 255u) repay_carries<8, 1>(acc + (baddr & ~3u), 0, old, delta, keep);
+    return;
+  }
   if (hot) {
     const uint32_t old = atoms_add(cnt_s + (baddr & ~3u), delta);
     // the byte's old value + cnt > 255: a carry left the byte (maybe further): repay through acc
@@ -1041,7 +1057,14 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
         const uint32_t word = PACK ? idx >> 2 : idx & (NW - 1);
         const uint32_t sh = PACK ? (idx & 3u) << 3 : (idx >> kLogNW) << 3;
         const uint32_t delta = cnt << sh;
-        if (hot) {
+        if (PACK && GPA_CODE_PRED) {
+          // straight-line: a predicated shared atomic (hot) and a predicated L2 reduction (the rest),
+          // no divergent branches; only a carry (rare) branches
+          const uint32_t old = atoms_add_if(hot, tab_s + word * 4, delta, 0u);
+          const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
+          red_add_u64_if(live && !hot, Hg + ((uint64_t)gq * GPA_SLOTS + slot), cnt, keep);
+          if (hot && ((old >> sh) & 0xFFu) + cnt > 255u) repay_carries<8, 1>(acc + 4 * word, 0, old, delta, keep);
+        } else if (hot) {
           const uint32_t old = atoms_add(tab_s + word * 4, delta);
           if (((old >> sh) & 0xFFu) + cnt > 255u) {
             if (PACK) repay_carries<8, 1>(acc + 4 * word, 0, old, delta, keep);  // bins 4 word .. 4 word + 3

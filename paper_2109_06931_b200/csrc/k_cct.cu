@@ -797,13 +797,15 @@ __device__ __forceinline__ void fold_climb(const LevelArgs &A, const double *__r
     }
     __stcg(incl + (uint64_t)c * GPA_SLOTS + r, v);
     if (p == NONE) return;
-    __threadfence();
+    // release: this lane's incl is visible device-wide before the context is counted in (acq_rel,
+    // not __threadfence: that is fence.sc plus an L1 invalidation; every load here goes to L2)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     __syncwarp(hmask);
     uint32_t last = 0;
     if (r == 0) last = atomicAdd(arrived + p, 1u) + 1u == nc;
     last = __shfl_sync(hmask, last, 0, 16);
     if (!last) return;
-    __threadfence();  // every sibling's incl is visible (each fenced before its context was counted in)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: every sibling's incl is visible
     v = __ldcg(excl + (uint64_t)p * GPA_SLOTS + r);
     const double *ci = incl + (uint64_t)d0 * GPA_SLOTS + r;
     uint32_t d = 0;

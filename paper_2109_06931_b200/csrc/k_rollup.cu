@@ -219,8 +219,15 @@ __global__ void __launch_bounds__(256) k_rollup_fin_multi(const uint2 *__restric
 }
 
 // CCT rows: fp64 vectors; S and the latency sum fold slots left to right (R3, R4).
+// d_rows (asynchronous trees): the row count on the device; above `rows` (~0: the build did not
+// fit) means no row
 __global__ void __launch_bounds__(256) k_derive_f64(const double *__restrict__ V, uint64_t rows,
-                                                    double *__restrict__ metrics) {
+                                                    double *__restrict__ metrics,
+                                                    const unsigned long long *__restrict__ d_rows) {
+  if (d_rows) {
+    const unsigned long long r = *d_rows;
+    rows = r > rows ? 0 : r;
+  }
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
     const double2 *p = reinterpret_cast<const double2 *>(V + r * GPA_SLOTS);
     double v[16];
@@ -329,11 +336,12 @@ cudaError_t launch_rollup_multi(const MultiRoll &M, uint32_t c0, uint32_t c1, ui
   return e;
 }
 
-cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st) {
+cudaError_t launch_derive_f64(const double *d_v, uint64_t rows, double *d_metrics, cudaStream_t st,
+                              const unsigned long long *d_rows) {
   if (rows == 0) return cudaSuccess;
   uint64_t blocks = (rows + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_derive_f64<<<(unsigned)blocks, 256, 0, st>>>(d_v, rows, d_metrics);
+  k_derive_f64<<<(unsigned)blocks, 256, 0, st>>>(d_v, rows, d_metrics, d_rows);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -90,6 +90,8 @@ def _load():
         "gpa_attribute_samples_host": ([_vp, _vp, _u64, _vp, _vp, _vp], S),
         "gpa_reconstruct_cct": ([_vp, _vp, ctypes.c_int, _u64, ctypes.POINTER(_vp), ctypes.POINTER(_u64), _vp], S),
         "gpa_get_cct_view": ([_vp, ctypes.POINTER(CctView)], S),
+        "gpa_reconstruct_cct_async": ([_vp, _vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_u64), _vp], S),
+        "gpa_cct_finish": ([_vp, ctypes.POINTER(_u64), ctypes.POINTER(ctypes.c_int)], S),
         "gpa_free_cct": ([_vp], None),
         "gpa_derive_metrics": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], S),
         "gpa_kernel_launches": ([], ctypes.c_uint64),
@@ -370,13 +372,28 @@ class Cct:
                "first_child": ("<i4", 1), "n_children": ("<i4", 1), "frac": ("<f8", 1), "excl": ("<f8", 16),
                "incl": ("<f8", 16)}
 
-    def __init__(self, h, device):
+    def __init__(self, h, device, pending_capacity: int | None = None):
         self._h = h
         self.device = device
+        if pending_capacity is not None:  # gpa_reconstruct_cct_async: size unknown until finish()
+            self.pending, self.capacity, self.n, self._v = True, int(pending_capacity), None, None
+            return
+        self._load_view()
+
+    def _load_view(self):
         v = CctView()
-        _check(_lib.gpa_get_cct_view(h, ctypes.byref(v)), "gpa_get_cct_view")
+        _check(_lib.gpa_get_cct_view(self._h, ctypes.byref(v)), "gpa_get_cct_view")
         self._v = v
         self.n = v.n
+        self.pending, self.capacity = False, v.n
+
+    def finish(self) -> bool:
+        """gpa_cct_finish: synchronize, learn the size; True if the tree had to be rebuilt (CCT
+        metrics derived while it was pending must then be derived again)."""
+        n, r = _u64(), ctypes.c_int()
+        _check(_lib.gpa_cct_finish(self.handle, ctypes.byref(n), ctypes.byref(r)), "gpa_cct_finish")
+        self._load_view()
+        return bool(r.value)
 
     @property
     def handle(self):
@@ -513,6 +530,21 @@ def reconstruct_cct(s: Structure, inst_hist, mode: int = WEIGHTS_SAMPLES, max_co
     if max_contexts == 0:
         return n.value
     return Cct(h, s.device)
+
+
+def reconstruct_cct_async(s: Structure, inst_hist, mode: int = WEIGHTS_SAMPLES, stream=None) -> Cct:
+    """a-6..a-9 without a host synchronization: a pending Cct (capacity known, size after finish())."""
+    h = _vp()
+    cap = _u64()
+    _check(_lib.gpa_reconstruct_cct_async(s.handle, _ptr(inst_hist, "inst_hist", 128 * s.info["n_inst"]), mode,
+                                          ctypes.byref(h), ctypes.byref(cap), _stream_ptr(stream, inst_hist.device)),
+           "gpa_reconstruct_cct_async")
+    c = Cct(h, s.device, pending_capacity=cap.value)
+    # a structure the one-launch build cannot hold: built synchronously, already finished (the view
+    # is refused only while the tree is pending)
+    if _lib.gpa_get_cct_view(h, ctypes.byref(CctView())) == 0:
+        c._load_view()
+    return c
 
 
 def derive_metrics(s: Structure, scope: str, inst_hist=None, cct: Cct | None = None, scope_hist=None,
