@@ -190,19 +190,21 @@ GPA_API uint64_t gpa_kernel_launches(void);
  * shared-memory heavy-hitter bins (u32), 4 ... heavy-hitter rows, 5 / 6 ... bins packed four /
  * two per 32-bit word (carries repaid exactly), 7 TMA ring with a shared-memory probe table of
  * granule rows (no per-record gather), 8 byte-packed bins found through a 32-bit code map with
- * a granule-indexed scratch for the rest (3-8 only where applicable: granule map, >= 2^21
- * records, >= 1024 instructions; 7 and 8 also need the module inside one aligned 4 GiB window;
- * otherwise automatic).  Automatic = 7 (structures up to 2^18 granules) or 8 from
- * max(4e6, 8 x n_inst) records on (granule map), else 1 (2 for binary-search structures above
- * 4096 records).  Also settable by the environment variable GPA_ATTR_VARIANT before the first
- * call.  DESIGN.md §7 describes the kernels. */
+ * a granule-indexed scratch for the rest, 9 every granule's row of byte counters in shared memory
+ * (no plan; modules of up to ~13.8 k granules) (3-8 only where applicable: granule map, >= 2^21
+ * records, >= 1024 instructions; 7, 8 and 9 also need the module inside one aligned 4 GiB window
+ * and < 2^27 granules; otherwise automatic).  Automatic = 9 from 2^20 records on where it
+ * applies, else 7 (structures up to 2^18 granules) or 8 from max(4e6, 8 x n_inst) records on
+ * (granule map), else 1 (2 for binary-search structures above 4096 records).  Also settable by
+ * the environment variable GPA_ATTR_VARIANT before the first call.  DESIGN.md §7 describes the
+ * kernels. */
 GPA_API gpa_status gpa_set_attr_kernel(int which);
-/* Testing only: level L in 1..64 makes the TMA-ring kernels (7, 8) sleep pseudo-random times up to
+/* Testing only: level L in 1..64 makes the TMA-ring kernels (7, 8, 9) sleep pseudo-random times up to
  * L/2 us before each stage's bulk copy (producer) and before reading each stage (consumers), so
  * producer-ahead and consumer-ahead orders of the ring protocol are exercised; results must not
  * change.  0 (default) = off.  Process-wide. */
 GPA_API gpa_status gpa_set_ring_stress(int level);
-/* The kernel (1..8, numbering above) gpa_attribute_samples runs for a call of n records on s
+/* The kernel (1..9, numbering above) gpa_attribute_samples runs for a call of n records on s
  * under the current setting.  Host-only; *which is written on GPA_OK. */
 GPA_API gpa_status gpa_attr_kernel_choice(gpa_structure s, uint64_t n, int *which);
 /* Validate a structure description on the host only (no device touched).  Same checks and

@@ -691,7 +691,7 @@ const char *gpa_last_error(void) { return g_err.c_str(); }
 uint64_t gpa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 gpa_status gpa_set_attr_kernel(int which) {
-  if (which < 0 || which > 8) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-8)", which);
+  if (which < 0 || which > 9) return fail(GPA_ERR_INVALID_ARG, "attribution kernel %d (0 auto, 1-9)", which);
   gpa::set_attr_kernel(which);
   return GPA_OK;
 }
@@ -840,7 +840,7 @@ gpa_status gpa_attribute_samples_host(gpa_structure s, const gpa_sample *h_sampl
   // the kernel is chosen for the whole call; a large-call kernel builds its plan once, from the
   // first chunk, accumulates every chunk and folds into H / U once at the end
   const int variant = attr_choice(s->attr, n);
-  const bool planned = variant == 7 || variant == 8;
+  const bool planned = variant == 7 || variant == 8 || variant == 9;
   AttrPlan plan;
   AttrAcc acc;
   void *plan_mem = nullptr;
@@ -1499,7 +1499,7 @@ gpa_status gpa_attr_plan_create(gpa_structure s, const gpa_sample *d_samples, ui
   // the structure's large-call kernel (gpa_set_attr_kernel numbering); none for small samples or
   // structures without one (planned calls then run gpa_attribute_samples)
   const int v = attr_choice(s->attr, ~0ull >> 8);
-  if ((v == 7 || v == 8) && n >= 4096) {
+  if ((v == 7 || v == 8 || v == 9) && n >= 4096) {
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMalloc(&pl->mem, plan_bytes(s->attr, v));
     if (e == cudaSuccess) e = plan_build(s->attr, v, reinterpret_cast<const uint4 *>(d_samples), n, pl->mem, &pl->p,

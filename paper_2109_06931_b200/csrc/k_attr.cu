@@ -43,8 +43,21 @@
 #ifndef GPA_CODE_PRED
 #define GPA_CODE_PRED 0
 #endif
+// K_attr_probe: predicated (C4 2.69 -> 2.59 ms, 0.91 -> 0.94 of peak; C3 unchanged)
 #ifndef GPA_PROBE_PRED
-#define GPA_PROBE_PRED 0
+#define GPA_PROBE_PRED 1
+#endif
+// K_attr_code32: unconditional code gather (sentinel entry) and 32-bit scratch row offsets
+#ifndef GPA_DIRECT_MIN  // records from which K_attr_direct runs (structures it holds whole)
+#define GPA_DIRECT_MIN (1 << 20)
+#endif
+#ifndef GPA_CODE_LEAN
+#define GPA_CODE_LEAN 1
+#endif
+// L2 evict-last hint on the code gathers: off (C5 12.01 -> 11.95 ms without it: the hint's policy
+// register is re-staged into uniform registers per gather)
+#ifndef GPA_CODE_HINT
+#define GPA_CODE_HINT 0
 #endif
 
 namespace gpa {
@@ -758,6 +771,11 @@ __global__ void __launch_bounds__(kFoldParts * 32) k_fold_all(FoldArgs F) {
     if (!b) return;
     const uint32_t i = F.gmap[0xFFFFFFFFu - (uint32_t)b];  // placed granules are mapped (k_sample_gran)
     red_add_u64(F.H + ((uint64_t)i << 4 | sl), t);
+  } else if (F.variant == 9) {  // acc index = 12 g + slot; gap granules -> U
+    const uint32_t g = bin / GPA_VALID_SLOTS, sl = bin - g * GPA_VALID_SLOTS;
+    if (g >= F.n_gran) return;
+    const uint32_t i = F.gmap[g];
+    red_add_u64(i == NONE ? F.U + sl : F.H + ((uint64_t)i << 4 | sl), t);
   } else {
     if (bin >= F.thr[1]) return;
     const uint32_t b = F.bin_of[bin];
@@ -867,7 +885,7 @@ __device__ __forceinline__ void probe_record(const ProbeArgs &A, uint4 v, bool l
   if (GPA_PROBE_PRED) {  // straight-line: predicated shared atomic / L2 reduction, a carry (rare) branches
     const uint32_t old = atoms_add_if(hot, cnt_s + (baddr & ~3u), delta, 0u);
     const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
-    red_add_u64_if(live && !hot, Hg + ((uint64_t)g * GPA_SLOTS + slot), cnt, keep);
+    red_add_u64_if(live && !hot, Hg + (g * GPA_SLOTS + slot), cnt, keep);  // 32-bit row offset (probe_ok)
     if (hot && ((old >> sh) & 0xFFu) + cnt > 255u) repay_carries<8, 1>(acc + (baddr & ~3u), 0, old, delta, keep);
     return;
   }
@@ -955,11 +973,99 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   dump_table<kProbeWords>(cnt8, kProbeWords, dump + (size_t)blockIdx.x * kProbeWords, NC * 32);  // word x: bytes = acc[4x ..]
 }
 
-// module span < 2^32 inside one aligned 4 GiB window (32-bit granule arithmetic)
+// module span < 2^32 inside one aligned 4 GiB window (32-bit granule arithmetic; < 2^27 granules, so
+// a granule-scratch row offset 16 g + slot fits 32 bits)
 bool probe_ok(const AttrTables &T) {
   const uint64_t span = T.n_gran << T.gshift;
-  return T.mode == 0 && T.n_gran < (1ull << 31) && span < (1ull << 32) && (T.base >> 32) == ((T.base + span - 1) >> 32);
+  return T.mode == 0 && T.n_gran < (1ull << 27) && span < (1ull << 32) && (T.base >> 32) == ((T.base + span - 1) >> 32);
 }
+
+
+// ---- K_attr_direct: every granule's row of byte counters in shared memory (small structures) ------
+// When the whole module fits (n_gran x 12 byte counters next to a 2-stage ring: up to ~13.8 k
+// granules, C2's 12 129), the CTA table is indexed by the granule itself: no plan (no sample,
+// no placement), no probe, no gather.  A record with a valid slot and count < 256 in the module is
+// one shared byte add (carries repaid through acc as in K_attr_probe); every other record (invalid
+// slot, count >= 256, outside the module) is reduced into the granule scratch Hg.  Gap granules are
+// counted like the rest and go to U in the fold (gmap[g] = NONE).
+using RingDirect = Ring<31, 2, 2>;
+constexpr size_t kDirectSmemMax = 232448;  // the opt-in dynamic shared memory of one sm_100 CTA
+
+__host__ __device__ inline uint32_t direct_words(uint64_t n_gran) {  // table words, a multiple of 4
+  return (uint32_t)(((n_gran * GPA_VALID_SLOTS + 3) / 4 + 3) & ~3ull);
+}
+__host__ __device__ inline size_t direct_smem(uint64_t n_gran) {
+  return RingDirect::kBytes + (size_t)direct_words(n_gran) * 4 + 2 * RingDirect::kStages * 8 + 4 * RingDirect::kStages;
+}
+
+template <class RG, bool REC>
+__global__ void __launch_bounds__(RG::kThreads, 1)
+    k_attr_direct(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint4 *__restrict__ rec, uint64_t n,
+                  unsigned long long *__restrict__ Hg, uint32_t *__restrict__ rec_inst,
+                  unsigned long long *__restrict__ acc, unsigned int *__restrict__ tile_ctr, uint32_t *__restrict__ dump,
+                  uint32_t tw) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(tab + tw);
+  uint64_t *empty = full + NST;
+  uint32_t *tile_of = reinterpret_cast<uint32_t *>(empty + NST);
+  uint32_t tab_s = smem_u32(tab);
+  asm volatile("mov.b32 %0, %0;" : "+r"(tab_s));
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty), tile_s = smem_u32(tile_of);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ntiles = (uint32_t)((n + S - 1) / S);
+  for (uint32_t x = threadIdx.x; x < tw / 4; x += blockDim.x) reinterpret_cast<uint4 *>(tab)[x] = make_uint4(0, 0, 0, 0);
+  ring_init(full, empty, NST, NC);
+  __syncthreads();
+  if (warp == NC) {
+    if (lane == 0) ring_produce_dyn<RG>(ring, full, empty, tile_of, rec, n, ntiles, tile_ctr, A.stress);
+    return;
+  }
+  uint64_t keep;  // L2 evict-last for Hg / acc (the record stream is evict-first)
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  const uint32_t ring_s = smem_u32(ring) + (warp * 32 + lane) * 16;
+  const uint32_t last_m = (uint32_t)(n - (uint64_t)(ntiles - 1) * S);
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t st = it % NST, ph = (it / NST) & 1;
+    mbar_wait_s(full_s + st * 8, ph);
+    const uint32_t tile = ld_shared_u32(tile_s + st * 4);
+    if (tile >= ntiles) break;
+    stress_sleep(A.stress, it, warp);
+    uint4 v[R];
+#pragma unroll
+    for (int u = 0; u < R; u++) v[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);  // beyond the tile end: masked
+    __syncwarp();
+    if (lane == 0) ring_release_s(empty_s + st * 8);
+    const bool partial = tile == ntiles - 1 && last_m != (uint32_t)S;
+#pragma unroll
+    for (int u = 0; u < R; u++) {
+      const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+      const bool live = !partial || j < last_m;
+      const uint32_t dlo = v[u].x - A.base_lo;
+      const uint32_t g = (v[u].y == A.base_hi && dlo < A.span) ? dlo >> A.gshift : A.n_gran;
+      const uint32_t cnt = v[u].z, st16 = v[u].w & 0xFFFFu;
+      if (REC && live) rec_inst[(uint64_t)tile * S + j] = g == A.n_gran ? NONE : __ldg(gmap + g);
+      const bool hot = live && g < A.n_gran && st16 < (uint32_t)GPA_VALID_SLOTS && cnt < 256u;
+      const uint32_t baddr = g * GPA_VALID_SLOTS + st16;
+      const uint32_t sh = (baddr & 3u) << 3, delta = cnt << sh;
+      if (hot) {
+        const uint32_t old = atoms_add(tab_s + (baddr & ~3u), delta);
+        if (((old >> sh) & 0xFFu) + cnt > 255u) repay_carries<8, 1>(acc + (baddr & ~3u), 0, old, delta, keep);
+      } else if (live) {
+        const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
+        red_add_u64(Hg + (g * GPA_SLOTS + slot), cnt);
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+  uint32_t *slab = dump + (size_t)blockIdx.x * tw;
+  for (uint32_t x = threadIdx.x; x < tw / 4; x += NC * 32)
+    reinterpret_cast<uint4 *>(slab)[x] = reinterpret_cast<const uint4 *>(tab)[x];
+}
+
+bool direct_ok(const AttrTables &T) { return probe_ok(T) && direct_smem(T.n_gran) <= kDirectSmemMax; }
 
 // ---- K_attr_code32: packed bins located through a 32-bit per-granule code ------------------------
 // The byte-packed bins of K_attr_bins<8> (131 072 bins in 128 KiB), but the per-call code map holds
@@ -970,8 +1076,8 @@ bool probe_ok(const AttrTables &T) {
 // H / U after the kernel.
 __global__ void k_codemap32(const uint32_t *__restrict__ gmap, uint64_t n_gran, const uint32_t *__restrict__ hot_info,
                             uint32_t *__restrict__ code) {
-  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_gran; g += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t m = gmap[g];
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= n_gran; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t m = g < n_gran ? gmap[g] : NONE;
     code[g] = m == NONE ? 0u : hot_info[m];
   }
 }
@@ -993,7 +1099,9 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
   uint64_t *empty = full + NST;
   uint32_t *tile_of = reinterpret_cast<uint32_t *>(empty + NST);
   uint4 *ring = reinterpret_cast<uint4 *>(smem);
-  const uint32_t tab_s = smem_u32(tab), full_s = smem_u32(full), empty_s = smem_u32(empty), tile_s = smem_u32(tile_of);
+  uint32_t tab_s = smem_u32(tab);
+  if (GPA_CODE_LEAN) asm volatile("mov.b32 %0, %0;" : "+r"(tab_s));  // a plain register, not re-derived per use
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty), tile_s = smem_u32(tile_of);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t ntiles = (uint32_t)((n + S - 1) / S);
   const uint32_t nb = min(thr[1], (uint32_t)NW * 4);
@@ -1029,7 +1137,8 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
     for (int u = 0; u < R; u++) {
       const uint32_t dlo = vv[u].x - A.base_lo;
       gg[u] = (vv[u].y == A.base_hi && dlo < A.span) ? dlo >> A.gshift : A.n_gran;
-      cc[u] = gg[u] < A.n_gran ? ldg_keep_u32(code + gg[u], keep) : 0u;
+      if (GPA_CODE_LEAN) cc[u] = GPA_CODE_HINT ? ldg_keep_u32(code + gg[u], keep) : __ldg(code + gg[u]);  // code[n_gran] = 0
+      else cc[u] = gg[u] < A.n_gran ? ldg_keep_u32(code + gg[u], keep) : 0u;
     }
   };
 #pragma unroll
@@ -1072,7 +1181,8 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
           }
         } else if (live) {
           const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
-          red_add_u64(Hg + ((uint64_t)gq * GPA_SLOTS + slot), cnt);
+          if (GPA_CODE_LEAN) red_add_u64(Hg + (gq * GPA_SLOTS + slot), cnt);  // 32-bit row offset: n_gran < 2^27
+          else red_add_u64(Hg + ((uint64_t)gq * GPA_SLOTS + slot), cnt);
         }
       }
       tid[q] = ntiles;  // consumed
@@ -1139,17 +1249,25 @@ static uint64_t plan_sample(uint64_t n, int variant) {
 }
 
 size_t plan_bytes(const AttrTables &T, int variant) {
+  if (variant == 9) return 16;                                                   // none
   if (variant == 7) return (size_t)kProbeM * 8;                                  // best[M]
-  return ((size_t)kCodeK + 4 + T.n_gran) * 4;                                     // bin_of[K] | thr[4] | code[n_gran]
+  return ((size_t)kCodeK + 4 + T.n_gran + 1) * 4;  // bin_of[K] | thr[4] | code[n_gran + 1] (code[n_gran] = 0: out of module)
 }
 
 // ---- host side of a call: few API calls (a mid-size call, C2's 1e7 records, is otherwise paced by
 // the host: ~20 allocations / memsets / launches took longer to issue than the GPU work they held) --
 static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
-static uint32_t table_words(int variant) { return variant == 7 ? (uint32_t)kProbeWords : (uint32_t)GPA_CODE_NW; }
+static uint32_t table_words(const AttrPlan &p) {
+  return p.variant == 7 ? (uint32_t)kProbeWords : p.variant == 9 ? direct_words(p.n_gran) : (uint32_t)GPA_CODE_NW;
+}
+// per-counter accumulators (acc): one per shared byte counter (7, 9) or bin (8)
+static size_t acc_count(const AttrPlan &p) {
+  return p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : p.variant == 9 ? (size_t)table_words(p) * 4 : (size_t)kCodeK;
+}
 
 // transient scratch of a plan build: gcnt[n_gran] (7) | scnt[n_inst*12] hot_info[n_inst] V[4096] (8)
 static size_t build_bytes(const AttrTables &T, int variant) {
+  if (variant == 9) return 0;
   if (variant == 7) return al256((size_t)T.n_gran * 4);
   return al256(((size_t)T.n_inst * kHotSlots + T.n_inst + kVBins) * 4);
 }
@@ -1157,9 +1275,9 @@ static size_t build_bytes(const AttrTables &T, int variant) {
 // accumulators of one call (or of all chunks of a host-records call): acc (per shared counter) |
 // Hg (granule x slot, + the out-of-module row) | one table slab per CTA | the dynamic tile counter
 static size_t acc_bytes(const AttrPlan &p, int sm_count) {
-  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  const size_t na = acc_count(p) * 8;
   const size_t nh = (size_t)(p.n_gran + 1) * 128;
-  return al256(na + nh) + al256((size_t)sm_count * table_words(p.variant) * 4) + 256;
+  return al256(na + nh) + al256((size_t)sm_count * table_words(p) * 4) + 256;
 }
 
 static void plan_ptrs(const AttrTables &T, int variant, void *mem, AttrPlan *p) {
@@ -1175,14 +1293,14 @@ static void plan_ptrs(const AttrTables &T, int variant, void *mem, AttrPlan *p) 
 }
 
 static void acc_ptrs(const AttrPlan &p, void *mem, int sm_count, AttrAcc *a) {
-  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  const size_t na = acc_count(p) * 8;
   const size_t nh = (size_t)(p.n_gran + 1) * 128;
   uint8_t *b = reinterpret_cast<uint8_t *>(mem);
   a->acc = reinterpret_cast<unsigned long long *>(b);
   a->Hg = a->acc + na / 8;
   a->dump = reinterpret_cast<uint32_t *>(b + al256(na + nh));
   a->slabs = sm_count;
-  a->ctr = reinterpret_cast<unsigned int *>(b + al256(na + nh) + al256((size_t)sm_count * table_words(p.variant) * 4));
+  a->ctr = reinterpret_cast<unsigned int *>(b + al256(na + nh) + al256((size_t)sm_count * table_words(p) * 4));
 }
 
 struct Fills {
@@ -1202,6 +1320,7 @@ struct Fills {
 };
 
 static void build_fills(const AttrTables &T, const AttrPlan &p, void *w, Fills &f) {
+  if (p.variant == 9) return;  // no plan
   if (p.variant == 7) {
     f.add(w, T.n_gran, 0u);                      // gcnt
     f.add(p.best, (size_t)kProbeM * 2, 0u);      // best
@@ -1212,7 +1331,7 @@ static void build_fills(const AttrTables &T, const AttrPlan &p, void *w, Fills &
 }
 
 static void acc_fills(const AttrPlan &p, const AttrAcc &a, Fills &f) {
-  const size_t na = (p.variant == 7 ? (size_t)kProbeM * GPA_VALID_SLOTS : (size_t)kCodeK) * 8;
+  const size_t na = acc_count(p) * 8;
   f.add(a.acc, (na + (size_t)(p.n_gran + 1) * 128) / 4, 0u);  // acc | Hg (the slabs are stored whole)
   f.add(a.ctr, 4, 0u);
 }
@@ -1220,6 +1339,7 @@ static void acc_fills(const AttrPlan &p, const AttrAcc &a, Fills &f) {
 // the sample -> table kernels (scratch zeroed)
 static cudaError_t build_kernels(const AttrTables &T, const AttrPlan &p, const uint4 *rec, uint64_t n, void *w,
                                  int sm_count, cudaStream_t st) {
+  if (p.variant == 9) return cudaSuccess;  // no plan
   const uint32_t chunks = (uint32_t)std::max<uint64_t>(2, plan_sample(n, p.variant) / kSampleChunk);
   if (p.variant == 7) {
     uint32_t *gcnt = reinterpret_cast<uint32_t *>(w);
@@ -1244,6 +1364,7 @@ static cudaError_t build_kernels(const AttrTables &T, const AttrPlan &p, const u
 cudaError_t plan_build(const AttrTables &T, int variant, const uint4 *rec, uint64_t n, void *mem, AttrPlan *p,
                        int sm_count, cudaStream_t st) {
   plan_ptrs(T, variant, mem, p);
+  if (variant == 9) return cudaSuccess;  // no plan
   void *w = nullptr;
   cudaError_t e = pool_alloc(&w, build_bytes(T, variant), st);
   if (e != cudaSuccess) return e;
@@ -1283,7 +1404,7 @@ static FoldArgs fold_args(const AttrTables &T, const AttrPlan &p, const AttrAcc 
                           unsigned long long *H, unsigned long long *U) {
   FoldArgs F{};
   F.dump = a.dump;
-  F.nw = table_words(p.variant);
+  F.nw = table_words(p);
   F.tb = (F.nw + 31) / 32;
   F.slabs = slabs;
   F.fin = fin;
@@ -1309,7 +1430,19 @@ static cudaError_t plan_launch(const AttrTables &T, const AttrPlan &p, const Att
   const ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift,
                     (uint32_t)T.n_gran, (uint32_t)g_ring_stress.load(std::memory_order_relaxed)};
   cudaError_t e;
-  if (p.variant == 7) {
+  if (p.variant == 9) {
+    using RG = RingDirect;
+    auto kern = ri ? k_attr_direct<RG, true> : k_attr_direct<RG, false>;
+    const size_t smem = direct_smem(T.n_gran);
+    // the table size varies per structure: set the attribute whenever this structure needs more
+    static std::atomic<size_t> set_for[2];
+    if (smem > set_for[ri ? 1 : 0].load(std::memory_order_relaxed)) {
+      if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirectSmemMax)) != cudaSuccess)
+        return e;
+      set_for[ri ? 1 : 0].store(kDirectSmemMax, std::memory_order_relaxed);
+    }
+    kern<<<sm_count, RG::kThreads, smem, st>>>(A, T.gmap, rec, n, a.Hg, ri, a.acc, a.ctr, a.dump, table_words(p));
+  } else if (p.variant == 7) {
     using RG = RingProbe;
     auto kern = ri ? k_attr_probe<RG, true> : k_attr_probe<RG, false>;
     const size_t smem = RG::kBytes + (size_t)kProbeSets * 8 + (size_t)kProbeWords * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
@@ -1327,7 +1460,7 @@ static cudaError_t plan_launch(const AttrTables &T, const AttrPlan &p, const Att
   }
   count_launches(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (fold && (p.variant == 7 || GPA_CODE_PACK)) {
+  if (fold && (p.variant != 8 || GPA_CODE_PACK)) {
     const FoldArgs F = fold_args(T, p, a, sm_count, 0, nullptr, nullptr);
     k_fold_all<<<F.tb, kFoldParts * 32, 0, st>>>(F);
     count_launches(1);
@@ -1378,7 +1511,7 @@ cudaError_t launch_planned(const AttrTables &T, int variant, const uint4 *rec, u
   e = f.launch(sm_count, st);
   if (e == cudaSuccess) e = build_kernels(T, p, rec, n, mem + b0, sm_count, st);
   if (e == cudaSuccess) e = plan_launch(T, p, a, rec, n, ri, sm_count, st, false);
-  if (e == cudaSuccess) e = plan_fold_final(T, p, a, (p.variant == 7 || GPA_CODE_PACK) ? sm_count : 0, H, U, sm_count, st);
+  if (e == cudaSuccess) e = plan_fold_final(T, p, a, (p.variant != 8 || GPA_CODE_PACK) ? sm_count : 0, H, U, sm_count, st);
   cudaError_t e2 = cudaFreeAsync(mem, st);
   return e != cudaSuccess ? e : e2;
 }
@@ -1475,9 +1608,11 @@ int attr_choice(const AttrTables &T, uint64_t n) {
   // sampled records (C3, C4: ~0.92), else the byte bins found through the 32-bit code map (C5)
   //
   const bool bins_auto = hot_ok && n >= 4000000ull && n >= 8ull * T.n_inst;
+  // the whole module in shared memory (K_attr_direct, no plan): from GPA_DIRECT_MIN records on
+  if ((var == 0 && n >= (uint64_t)GPA_DIRECT_MIN || var == 9) && direct_ok(T)) return 9;
   if (var == 0 && bins_auto) return probe_ok(T) ? (T.n_gran <= (1ull << 18) ? 7 : 8) : 3;
   if (var >= 3 && var <= 6 && hot_ok) return var;
-  if (var >= 7 && hot_ok && probe_ok(T)) return var;
+  if ((var == 7 || var == 8) && hot_ok && probe_ok(T)) return var;
   return (var == 1 || n < 4096 || (var == 0 && T.mode == 0)) ? 1 : 2;
 }
 
@@ -1487,6 +1622,7 @@ cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, u
   if (n == 0) return cudaSuccess;
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
   switch (attr_choice(T, n)) {
+    case 9:
     case 8:
     case 7: return launch_planned(T, attr_choice(T, n), rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
     case 6: return launch_bins<16>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);

@@ -154,7 +154,7 @@ def set_ring_stress(level: int) -> None:
 
 
 ATTR_KERNEL_NAMES = {1: "k_attr_stream", 2: "k_attr_tma", 3: "k_attr_bins", 4: "k_attr_hot", 5: "k_attr_bins",
-                     6: "k_attr_bins", 7: "k_attr_probe", 8: "k_attr_code32"}
+                     6: "k_attr_bins", 7: "k_attr_probe", 8: "k_attr_code32", 9: "k_attr_direct"}
 
 
 def attr_kernel_choice(s, n: int) -> int:

@@ -85,7 +85,7 @@ def test_fuzz_whole_path(gpa, seed):
     s = gpa.load_structure(st, 0)
     assert np.array_equal(s.scc_of(), oracle.cct(st, np.zeros((n_inst, 16), np.uint64))["scc_of"])
     dr = torch.from_numpy(rec.view(np.int64).reshape(-1, 2)).to(DEV)
-    for kernel in (0, 1, 2, 3, 4, 5, 6, 7, 8):
+    for kernel in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9):
         gpa.set_attr_kernel(kernel)
         H = torch.zeros((n_inst, 16), dtype=torch.int64, device=DEV)
         U = torch.zeros(16, dtype=torch.int64, device=DEV)

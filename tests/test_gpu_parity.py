@@ -321,8 +321,8 @@ def attr_kernel(gpa):
     gpa.set_attr_kernel(0)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8])
-@pytest.mark.parametrize("name,records", [("C3", 4_000_003), ("C5", 3_000_001)])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("name,records", [("C2", 3_000_001), ("C3", 4_000_003), ("C5", 3_000_001)])
 def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
     attr_kernel(kernel)
     w = gen.workload(name, records=records)
@@ -333,11 +333,11 @@ def test_attribution_each_kernel(gpa, attr_kernel, kernel, name, records):
     assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_attribution_huge_counts_exact(gpa, attr_kernel, kernel):
     """Counts near 2^32 make every shared u32 add wrap: the repaid 2^32 keeps H exact."""
     attr_kernel(kernel)
-    w = gen.workload("C3", records=2_200_000)
+    w = gen.workload("C2" if kernel == 9 else "C3", records=2_200_000)  # 9: a structure it holds whole
     rec = w.records_host()
     rng = np.random.default_rng(5)
     rec["count"] = np.where(rng.random(len(rec)) < 0.5, 0xFFFFFFF0, rng.integers(1, 1 << 31, len(rec)))
@@ -385,12 +385,12 @@ def test_profile_stats_huge_values(gpa):
     assert (So[0, 4] == 0).all()
 
 
-@pytest.mark.parametrize("kernel", [3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("kernel", [3, 4, 5, 6, 7, 8, 9])
 def test_attribution_shared_counter_overflow_patterns(gpa, attr_kernel, kernel):
     """Hot bins receive counts that drive 16- and 32-bit shared counters through many
     overflows (incl. carries between packed halves, counts of exactly 0xFFFF / 0x10000)."""
     attr_kernel(kernel)
-    w = gen.workload("C4", records=3_000_000)
+    w = gen.workload("C2" if kernel == 9 else "C4", records=3_000_000)
     rec = w.records_host()
     rng = np.random.default_rng(8)
     choices = np.array([1, 0xFFFF, 0x10000, 0x7FFF, 0xFFFE, 2 ** 31, 0xFFFFFFFF], np.uint64)
@@ -479,7 +479,7 @@ def test_f1_invalid_args(gpa):
 
 
 # ---- reusable attribution plans and the host-records path --------------------------------------
-@pytest.mark.parametrize("name", ["C3", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
 def test_attr_plan_reuse_exact(gpa, name):
     """A plan built from one batch serves other batches (and a batch from another part of the
     stream): results equal the oracle bit for bit, whatever the plan."""
@@ -487,7 +487,7 @@ def test_attr_plan_reuse_exact(gpa, name):
     s = gpa.load_structure(w.structure, 0)
     first = _device_records(w, 0, 2_000_000)
     plan = gpa.AttrPlan(s, first)
-    assert plan.variant in (7, 8)
+    assert plan.variant in (7, 8, 9)
     for k0, n in [(2_000_000, 3_999_999), (0, 2_000_000), (5_999_000, 1000)]:
         rec = _device_records(w, k0, n)
         H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device=DEV)
@@ -501,13 +501,14 @@ def test_attr_plan_reuse_exact(gpa, name):
     plan.free()
 
 
+@pytest.mark.parametrize("name", ["C2", "C4"])
 @pytest.mark.parametrize("pinned", [True, False])
-def test_host_path_many_chunks(gpa, pinned):
+def test_host_path_many_chunks(gpa, pinned, name):
     """gpa_attribute_samples_host over more than 3 x 2^22 + 17 records (several passes of the
     3-buffer staging rotation and a ragged last chunk, one plan for the whole call), pinned and
     pageable host memory."""
     n = 3 * (1 << 22) + 17 + 1_000_003
-    w = gen.workload("C4", records=n)
+    w = gen.workload(name, records=n)
     s = gpa.load_structure(w.structure, 0)
     host = torch.empty((n, 2), dtype=torch.int64, pin_memory=pinned)
     w.records_host(0, n, out=host.numpy().view(gen.RECORD_DTYPE).reshape(-1))
@@ -520,7 +521,7 @@ def test_host_path_many_chunks(gpa, pinned):
     assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
 
 
-@pytest.mark.parametrize("kernel", [7, 8])
+@pytest.mark.parametrize("kernel", [7, 8, 9])
 @pytest.mark.parametrize("stress", [1, 8])
 def test_ring_stress_exact(gpa, attr_kernel, kernel, stress):
     """Adversarial TMA-ring timing (gpa_set_ring_stress: random producer and consumer sleeps, so
@@ -529,7 +530,7 @@ def test_ring_stress_exact(gpa, attr_kernel, kernel, stress):
     attr_kernel(kernel)
     gpa.set_ring_stress(stress)
     try:
-        w = gen.workload("C4" if kernel == 7 else "C5", records=4_200_007)
+        w = gen.workload({7: "C4", 8: "C5", 9: "C2"}[kernel], records=4_200_007)
         s = gpa.load_structure(w.structure, 0)
         H, U, ri = _attribute(gpa, s, _device_records(w))
     finally:

@@ -33,7 +33,7 @@ def main():
     w = gen.workload(cfg, records=records)
     n = w.cfg.records
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "-k", "regex:k_attr_(code32|probe|bins|hot|tma|stream)", "-c", "1", "--csv",
+           "--clock-control", "none", "-k", "regex:k_attr_(code32|probe|direct|bins|hot|tma|stream)", "-c", "1", "--csv",
            sys.executable, os.path.join(ROOT, "tools", "prof_attr.py"), cfg, str(n), "1"]
     out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT).stdout
     rows = [r for r in csv.reader(io.StringIO(out)) if len(r) > 10]
