@@ -797,6 +797,11 @@ __device__ __forceinline__ void fold_climb(const LevelArgs &A, const double *__r
     }
     __stcg(incl + (uint64_t)c * GPA_SLOTS + r, v);
     if (p == NONE) return;
+    if (nc == 1) {  // an only child is trivially the last arrival: no fence, no counter (recursion chains)
+      v = __dadd_rn(__ldcg(excl + (uint64_t)p * GPA_SLOTS + r), v);
+      c = p;
+      continue;
+    }
     // release: this lane's incl is visible device-wide before the context is counted in (acq_rel,
     // not __threadfence: that is fence.sc plus an L1 invalidation; every load here goes to L2)
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
