@@ -61,7 +61,17 @@ class ClockSampler:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        time.sleep(0.3)
+        # wait for the first sample: nvidia-smi's start-up (NVML init) can stall the GPU briefly, so
+        # it must not fall inside the timed region (measured: one 16-32 ms step out of ten)
+        t_end = time.time() + 5.0
+        while self.proc and time.time() < t_end:
+            try:
+                if open(self.path).read().strip():
+                    break
+            except Exception:
+                pass
+            time.sleep(0.05)
+        time.sleep(0.15)
         return self
 
     def __exit__(self, *a):
@@ -223,10 +233,14 @@ def run_gpa(args):
         bounds = [int(x) for x in gpa.partition_structure(w.structure, world)]
         lo, hi = bounds[rank], bounds[rank + 1]
         nf, nc = s.info["n_func"], s.info["n_call"]
-    # Two batch buffers.  Default: one batch at a time (attribution on stream A, then the combine
-    # and CCT on the high-priority stream B with the scope roll-ups on a side stream).  --pipeline
-    # enqueues batch i + 1's attribution before batch i's analysis; measured slower:
-    # the persistent attribution CTAs occupy every SM, so the analysis kernels wait for them.
+    # Two batch buffers.  Default: one batch at a time (attribution, then the CCT on the
+    # high-priority stream B with the scope roll-ups on a side stream).  --pipeline enqueues batch
+    # i + 1's attribution (stream A) before batch i's analysis; with the asynchronous CCT the host
+    # never waits inside a step, so the analysis kernels fill SMs the attribution leaves idle: C5
+    # 12.56 -> 12.35 ms per step, but the attribution itself then measures 12.26 instead of 12.02 ms
+    # (0.797 instead of 0.813 of peak: the analysis competes with it), so the default keeps the
+    # kernel's own time clean.
+    pipeline = args.pipeline
     class Buf:
         pass
 
@@ -243,7 +257,7 @@ def run_gpa(args):
         x.freed.record(stream)
         bufs.append(x)
     B = stream                                       # combine + CCT (high priority)
-    A = torch.cuda.Stream(dev) if args.pipeline else B   # attribution
+    A = torch.cuda.Stream(dev) if pipeline else B        # attribution
     side = torch.cuda.Stream(dev)                    # scope roll-ups
     ev_a0, ev_a1, ev_b0, ev_b1, ev_c1 = [], [], [], [], []
 
@@ -327,7 +341,6 @@ def run_gpa(args):
                 cct.free()               # stream-ordered on B
         return nctx
 
-    pipeline = args.pipeline
     # CCT without a host round trip inside the step (gpa_reconstruct_cct_async); --sync-cct for
     # the synchronous call
     async_cct = world == 1 and not args.sync_cct
@@ -513,7 +526,8 @@ def run_gpa(args):
     # phase times on rank 0 and the secondary sum-of-counts rate
     phases = {"attr_ms": attr_ms,
               "scopes_ms_side_stream": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_b1)) / max(1, len(ev_b1)),
-              "cct_and_cct_metrics_ms": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_c1)) / max(1, len(ev_c1))}
+              "cct_and_cct_metrics_ms": sum(x.elapsed_time(y) for x, y in zip(ev_b0, ev_c1)) / max(1, len(ev_c1)),
+              "attr_ms_per_step": [round(x.elapsed_time(y), 4) for x, y in zip(ev_a0, ev_a1)]}
     observations = int(bufs[(args.steps - 1) % 2].HU.sum().item())  # sum of counts of the last batch (u64 as int64)
     line = {"metric": METRIC, "value": n_all / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -525,7 +539,9 @@ def run_gpa(args):
                            f"{args.dist_backend} reduce-scatter of H||U at function-aligned bounds, rows derived "
                            f"per rank, S_f||w reduced to rank 0 for the CCT" if scatter else
                            f"{args.dist_backend} reduce of H||U to rank 0") if world > 1 else "single GPU"),
-                       "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed"},
+                       "l2": "inputs (16 B x records) far exceed the 126 MB L2; no flush needed",
+                       "schedule": "pipelined batches (attribution of i+1 queued before the analysis of i)"
+                       if pipeline else "one batch at a time"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": gpa.ATTR_KERNEL_NAMES.get(gpa.attr_kernel_choice(s, n), "?"),
@@ -569,7 +585,8 @@ def main():
     ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
     ap.add_argument("--sync-cct", action="store_true", help="synchronous gpa_reconstruct_cct (A/B of the async tree)")
     ap.add_argument("--pipeline", action="store_true",
-                    help="enqueue batch i+1's attribution before batch i's analysis (measured slower; DESIGN.md §7)")
+                    help="enqueue batch i+1's attribution before batch i's analysis (C5: +1.7 %% throughput, "
+                         "the attribution kernel slowed by the concurrent analysis; DESIGN.md §11)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

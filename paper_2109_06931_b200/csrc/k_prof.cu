@@ -77,9 +77,24 @@ __global__ void __launch_bounds__(kThreads)
 // K "profile lanes" x n_func functions x 12 slots, lane k = profile p_first + k where p_first
 // is the profile of the CTA's first record; other records, unattributed ones and invalid
 // stalls go straight to L2.  One gather (granule -> function, built at load) per record.
-constexpr int kProfTab = 160 * 1024;  // bytes of shared counters
-using RingProf = Ring<16, 2, 4>;
-constexpr int kProfLook = 2;
+#ifndef GPA_PROF_TAB
+#define GPA_PROF_TAB (160 * 1024)
+#endif
+#ifndef GPA_PROF_NC
+#define GPA_PROF_NC 16
+#endif
+#ifndef GPA_PROF_R
+#define GPA_PROF_R 2
+#endif
+#ifndef GPA_PROF_NST
+#define GPA_PROF_NST 4
+#endif
+#ifndef GPA_PROF_LOOK
+#define GPA_PROF_LOOK 2
+#endif
+constexpr int kProfTab = GPA_PROF_TAB;  // bytes of shared counters
+using RingProf = Ring<GPA_PROF_NC, GPA_PROF_R, GPA_PROF_NST>;
+constexpr int kProfLook = GPA_PROF_LOOK;
 
 template <class RG>
 __global__ void __launch_bounds__(RG::kThreads, 1)
