@@ -33,6 +33,12 @@ for kernel in KERNELS:
             gpa.derive_metrics(s, "CCT_EXCL", cct=c, metrics=m)
             gpa.derive_metrics(s, "CCT_INCL", cct=c, metrics=m)
             c.free()
+            c = gpa.reconstruct_cct_async(s, H, mode=mode)  # device-side row count, finish
+            m = torch.empty((max(1, c.capacity), 33), dtype=torch.float64, device="cuda")
+            gpa.derive_metrics(s, "CCT_EXCL", cct=c, metrics=m)
+            gpa.derive_metrics(s, "CCT_INCL", cct=c, metrics=m)
+            c.finish()
+            c.free()
         P = 3
         PH = torch.zeros((P + 1, s.info["n_func"], 16), dtype=torch.int64, device="cuda")
         PU = torch.zeros((P + 1, 16), dtype=torch.int64, device="cuda")
