@@ -29,15 +29,23 @@ namespace {
 template <int MODE>
 __global__ void k_prof_call_weights(AttrTables T, const uint32_t *__restrict__ inst_call, const uint4 *__restrict__ rec,
                                     uint64_t n, uint32_t n_prof, uint32_t n_call, unsigned long long *__restrict__ wp) {
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint4 v = ld_stream(rec + k);
-    const uint32_t stall = v.w & 0xFFFFu, prof = v.w >> 16;
-    if (stall >= GPA_VALID_SLOTS || v.z == 0) continue;
-    const uint32_t i = lookup<MODE>(T, ((uint64_t)v.y << 32) | v.x);
-    if (i == NONE) continue;
-    const uint32_t e = __ldg(inst_call + i);
-    if (e == NONE) continue;
-    atomicAdd(wp + (uint64_t)(prof < n_prof ? prof : n_prof) * n_call + e, (unsigned long long)v.z);
+  // four records in flight per thread (the loads are independent; one at a time left HBM idle)
+  constexpr int U = 4;
+  const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += U * G) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = k0 + u * G < n ? ld_stream(rec + k0 + u * G) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t stall = v[u].w & 0xFFFFu, prof = v[u].w >> 16;
+      if (stall >= GPA_VALID_SLOTS || v[u].z == 0) continue;  // (count 0 also marks a padding lane)
+      const uint32_t i = lookup<MODE>(T, ((uint64_t)v[u].y << 32) | v[u].x);
+      if (i == NONE) continue;
+      const uint32_t e = __ldg(inst_call + i);
+      if (e == NONE) continue;
+      atomicAdd(wp + (uint64_t)(prof < n_prof ? prof : n_prof) * n_call + e, (unsigned long long)v[u].z);
+    }
   }
 }
 

@@ -1,3 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_cct_async.py tests/test_gpu_cct_per_profile.py -m gpu -x -q -k "cct or async" > gpurun_out/t11.log 2>&1; echo rc=$? >> gpurun_out/t11.log
-for c in C3 C5; do timeout 200 python tools/prof_cct.py $c 7 >> gpurun_out/cct11.log 2>&1; done
-tail -3 gpurun_out/t11.log; grep "rep [456]" gpurun_out/cct11.log
+timeout 300 python -m pytest tests/test_gpu_cct_per_profile.py -m gpu -x -q > gpurun_out/t17.log 2>&1; echo rc=$? >> gpurun_out/t17.log
+timeout 600 python tools/bench_next.py f1 > gpurun_out/next17.jsonl 2>&1
+bash tools/ab_libs.sh C5 r2s3 nc24r4 look2 pred1 > gpurun_out/ab17.log 2>&1
+tail -2 gpurun_out/t17.log; grep call_weights gpurun_out/next17.jsonl; grep -v Warn gpurun_out/ab17.log
