@@ -165,6 +165,9 @@ constexpr uint64_t kScanMaxWords = 1ull << 27;  // the largest scan_u32 input
 // ---- kernels launchers (k_*.cu) -----------------------------------------------------------
 namespace gpa {
 int attr_choice(const AttrTables &T, uint64_t n);  // kernel a call of n records runs (gpa_attr_kernel_choice)
+bool prof_code_ok(const AttrTables &T, uint64_t n);  // f1 instruction rows through a call plan's hot bins
+cudaError_t launch_prof_inst_code(const AttrTables &T, const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
+                                  unsigned long long *PH, unsigned long long *PU, int sm_count, cudaStream_t st);
 // attribution plans of the large-call kernels 7 (probe table) and 8 (code map + byte bins), k_attr.cu
 struct AttrPlan {
   int variant = 0;

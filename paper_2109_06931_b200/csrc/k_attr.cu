@@ -1067,6 +1067,139 @@ __global__ void __launch_bounds__(RG::kThreads, 1)
 
 bool direct_ok(const AttrTables &T) { return probe_ok(T) && direct_smem(T.n_gran) <= kDirectSmemMax; }
 
+// ---- f1 at instruction level with K_attr_code32's hot bins ------------
+// The per-profile cube PH[(P+1)][n_inst][16] (profile = the record's stream field, P = overflow).
+// A CTA takes a contiguous range of tiles (one profile's records are contiguous in the stream, so it
+// meets a few profiles in turn) and counts the current profile's records that fall into the call
+// plan's hot (instruction, slot) bins in K_attr_code32's byte-packed shared table; every other
+// record is one L2 reduction into the cube (instruction = gmap[g]).  When a whole tile belongs to
+// another profile, the consumer warps meet at a named barrier, flush the table into the old
+// profile's rows (bin -> (instruction, slot) through the plan's bin_of) and continue with the new
+// profile.  A byte carry is repaid in the cube directly (+256 at the bin, -1 at the next byte's bin,
+// unassigned bins skipped on both sides, so they cancel).  Exact for any plan.
+__device__ __forceinline__ void prof_repay(unsigned long long *row, const uint32_t *__restrict__ bin_of, uint32_t nb,
+                                           uint32_t word, uint32_t old, uint32_t delta) {
+  const unsigned long long s = (unsigned long long)old + delta;
+  const uint32_t cin = old ^ delta ^ (uint32_t)s;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const bool cross = j < 3 ? ((cin >> (8 * (j + 1))) & 1u) : (uint32_t)(s >> 32);
+    if (!cross) continue;
+    const uint32_t b0 = 4 * word + j, t0 = b0 < nb ? __ldg(bin_of + b0) : NONE;
+    if (t0 != NONE) red_add_u64(row + t0, 256ull);
+    if (j < 3) {
+      const uint32_t t1 = b0 + 1 < nb ? __ldg(bin_of + b0 + 1) : NONE;
+      if (t1 != NONE) red_add_u64(row + t1, ~0ull);  // -1 (mod 2^64)
+    }
+  }
+}
+
+template <class RG, int NW>
+__global__ void __launch_bounds__(RG::kThreads, 1)
+    k_attr_prof_code(ProbeArgs A, const uint32_t *__restrict__ gmap, const uint32_t *__restrict__ code,
+                     const uint32_t *__restrict__ bin_of, const uint32_t *__restrict__ thr, const uint4 *__restrict__ rec,
+                     uint64_t n, uint32_t n_inst, uint32_t n_prof, unsigned long long *__restrict__ PH,
+                     unsigned long long *__restrict__ PU) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int S = RG::kTile, NST = RG::kStages, NC = RG::kConsumers, R = RG::kPerLane;
+  uint4 *ring = reinterpret_cast<uint4 *>(smem);
+  uint32_t *tab = reinterpret_cast<uint32_t *>(smem + RG::kBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + RG::kBytes + (size_t)NW * 4);
+  uint64_t *empty = full + NST;
+  uint32_t *tile_of = reinterpret_cast<uint32_t *>(empty + NST);
+  uint32_t tab_s = smem_u32(tab);
+  asm volatile("mov.b32 %0, %0;" : "+r"(tab_s));
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty), tile_s = smem_u32(tile_of);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ntiles = (uint32_t)((n + S - 1) / S);
+  const uint32_t t0 = (uint32_t)((uint64_t)ntiles * blockIdx.x / gridDim.x);
+  const uint32_t t1 = (uint32_t)((uint64_t)ntiles * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t nb = min(thr[1], (uint32_t)NW * 4);
+  for (uint32_t x = threadIdx.x; x < NW; x += blockDim.x) tab[x] = 0;
+  ring_init(full, empty, NST, NC);
+  __syncthreads();
+  if (warp == NC) {
+    if (lane == 0) ring_produce<RG>(ring, full, empty, rec, n, t0, 1, t1);
+    return;
+  }
+  const uint32_t ring_s = smem_u32(ring) + (warp * 32 + lane) * 16;
+  const uint32_t last_m = (uint32_t)(n - (uint64_t)(ntiles - 1) * S);
+  const uint64_t rows = (uint64_t)n_inst * GPA_SLOTS;  // u64 per profile
+  // the profile the table counts: the CTA's first record's (clamped to the overflow profile)
+  uint32_t pcur = n_prof;
+  if (t0 < t1) {
+    const uint32_t s0 = __ldg(reinterpret_cast<const uint32_t *>(rec + (uint64_t)t0 * S) + 3) >> 16;
+    pcur = s0 < n_prof ? s0 : n_prof;
+  }
+  auto flush = [&](uint32_t p) {  // table -> PH[p], zeroed; all consumer warps
+    asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+    unsigned long long *row = PH + (uint64_t)p * rows;
+    for (uint32_t x = threadIdx.x; x < NW; x += NC * 32) {
+      const uint32_t word = tab[x];
+      if (!word) continue;
+      tab[x] = 0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t val = (word >> (8 * q)) & 0xFFu, b = 4 * x + q;
+        if (val && b < nb) {
+          const uint32_t t = __ldg(bin_of + b);
+          if (t != NONE) red_add_u64(row + t, val);
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+  };
+  for (uint32_t it = 0; t0 + it < t1; ++it) {
+    const uint32_t tile = t0 + it;
+    const uint32_t st = it % NST, ph = (it / NST) & 1;
+    mbar_wait_s(full_s + st * 8, ph);
+    const bool last = tile == ntiles - 1;
+    const uint32_t m = last ? last_m : (uint32_t)S;
+    // a tile wholly of another profile: switch the table to it (uniform: every warp reads the same words)
+    const uint32_t pa = ld_shared_u32(smem_u32(ring) + (st * S) * 16 + 12) >> 16;
+    const uint32_t pz = ld_shared_u32(smem_u32(ring) + (st * S + m - 1) * 16 + 12) >> 16;
+    const uint32_t qa = pa < n_prof ? pa : n_prof, qz = pz < n_prof ? pz : n_prof;
+    uint4 v[R];
+#pragma unroll
+    for (int u = 0; u < R; u++) v[u] = lds128(ring_s + (st * S + u * NC * 32) * 16);
+    __syncwarp();
+    if (lane == 0) ring_release_s(empty_s + st * 8);
+    if (qa == qz && qa != pcur) {
+      flush(pcur);
+      pcur = qa;
+    }
+    uint32_t g[R], c[R];
+#pragma unroll
+    for (int u = 0; u < R; u++) {
+      const uint32_t dlo = v[u].x - A.base_lo;
+      g[u] = (v[u].y == A.base_hi && dlo < A.span) ? dlo >> A.gshift : A.n_gran;
+      c[u] = __ldg(code + g[u]);  // code[n_gran] = 0
+    }
+    unsigned long long *row = PH + (uint64_t)pcur * rows;
+#pragma unroll
+    for (int u = 0; u < R; u++) {
+      const uint32_t j = (uint32_t)(u * NC + warp) * 32 + lane;
+      const bool live = j < m;
+      const uint32_t cnt = v[u].z, st16 = v[u].w & 0xFFFFu, sid = v[u].w >> 16;
+      const uint32_t p = sid < n_prof ? sid : n_prof;
+      const uint32_t mask = c[u] & 0xFFFu;
+      const bool hot = live && p == pcur && st16 < (uint32_t)GPA_VALID_SLOTS && ((mask >> st16) & 1u) && cnt < 256u;
+      const uint32_t idx = (c[u] >> 12) + __popc(mask & ((1u << st16) - 1u));
+      const uint32_t word = idx >> 2, sh = (idx & 3u) << 3, delta = cnt << sh;
+      if (hot) {
+        const uint32_t old = atoms_add(tab_s + word * 4, delta);
+        if (((old >> sh) & 0xFFu) + cnt > 255u) prof_repay(row, bin_of, nb, word, old, delta);
+      } else if (live && cnt) {
+        const uint32_t slot = st16 < (uint32_t)GPA_VALID_SLOTS ? st16 : (uint32_t)GPA_SLOT_INVALID;
+        const uint32_t i = g[u] < A.n_gran ? __ldg(gmap + g[u]) : NONE;
+        red_add_u64(i == NONE ? PU + ((uint64_t)p << 4 | slot) : PH + (uint64_t)p * rows + ((uint64_t)i << 4 | slot), cnt);
+      }
+    }
+  }
+  flush(pcur);
+}
+
+
 // ---- K_attr_code32: packed bins located through a 32-bit per-granule code ------------------------
 // The byte-packed bins of K_attr_bins<8> (131 072 bins in 128 KiB), but the per-call code map holds
 // only the hot information of the granule's instruction (base << 12 | 12-bit hot-slot mask; 0 =
@@ -1616,6 +1749,56 @@ int attr_choice(const AttrTables &T, uint64_t n) {
   return (var == 1 || n < 4096 || (var == 0 && T.mode == 0)) ? 1 : 2;
 }
 
+// CTAs of the persistent attribution kernels: all SMs, or fewer (environment GPA_ATTR_CTAS) so that
+// kernels of other streams (a previous batch's analysis) find free SMs while a batch is attributed
+int attr_ctas(int sm_count) {
+  static const int v = [] {
+    const char *e = getenv("GPA_ATTR_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  return v > 0 && v < sm_count ? v : sm_count;
+}
+
+// f1 instruction level with the hot bins of a call plan (k_attr_prof_code); false: not applicable
+bool prof_code_ok(const AttrTables &T, uint64_t n) {
+  return probe_ok(T) && n >= 4000000ull && T.n_inst >= 1024 && getenv("GPA_PROF_INST_L2") == nullptr;
+}
+
+cudaError_t launch_prof_inst_code(const AttrTables &T, const gpa_sample *d_samples, uint64_t n, uint32_t n_prof,
+                                  unsigned long long *PH, unsigned long long *PU, int sm_count, cudaStream_t st) {
+  const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
+  AttrPlan p;
+  p.variant = 8;
+  p.n_gran = T.n_gran;
+  const size_t b0 = al256(plan_bytes(T, 8)), b1 = build_bytes(T, 8);
+  uint8_t *mem = nullptr;
+  cudaError_t e = pool_alloc((void **)&mem, b0 + b1, st);
+  if (e != cudaSuccess) return e;
+  plan_ptrs(T, 8, mem, &p);
+  Fills f;
+  build_fills(T, p, mem + b0, f);
+  e = f.launch(sm_count, st);
+  if (e == cudaSuccess) e = build_kernels(T, p, rec, n, mem + b0, sm_count, st);
+  if (e == cudaSuccess) {
+    using RG = RingCode;
+    auto kern = k_attr_prof_code<RG, GPA_CODE_NW>;
+    const size_t smem = RG::kBytes + (size_t)GPA_CODE_NW * 4 + 2 * RG::kStages * 8 + 4 * RG::kStages;
+    e = smem_attr_once(kern, smem, 3);
+    const ProbeArgs A{(uint32_t)T.base, (uint32_t)(T.base >> 32), (uint32_t)(T.n_gran << T.gshift), T.gshift,
+                      (uint32_t)T.n_gran, 0u};
+    const uint64_t ntiles = (n + RG::kTile - 1) / RG::kTile;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count);
+    if (e == cudaSuccess) {
+      kern<<<blocks, RG::kThreads, smem, st>>>(A, T.gmap, p.code, p.bin_of, p.thr, rec, n, (uint32_t)T.n_inst, n_prof,
+                                               PH, PU);
+      count_launches(1);
+      e = cudaGetLastError();
+    }
+  }
+  cudaError_t e2 = cudaFreeAsync(mem, st);
+  return e != cudaSuccess ? e : e2;
+}
+
 cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, uint64_t n,
                              unsigned long long *d_hist, unsigned long long *d_unattr, uint32_t *d_rec_inst,
                              int sm_count, cudaStream_t st) {
@@ -1624,7 +1807,7 @@ cudaError_t launch_attribute(const AttrTables &T, const gpa_sample *d_samples, u
   switch (attr_choice(T, n)) {
     case 9:
     case 8:
-    case 7: return launch_planned(T, attr_choice(T, n), rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
+    case 7: return launch_planned(T, attr_choice(T, n), rec, n, d_hist, d_unattr, d_rec_inst, attr_ctas(sm_count), st);
     case 6: return launch_bins<16>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
     case 5: return launch_bins<8>(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);
     case 4: return launch_hot(T, rec, n, d_hist, d_unattr, d_rec_inst, sm_count, st);

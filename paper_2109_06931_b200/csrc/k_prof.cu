@@ -282,6 +282,8 @@ cudaError_t launch_attribute_profiles_inst(const AttrTables &T, uint32_t n_inst,
                                            unsigned long long *d_pu, int sm_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const uint4 *rec = reinterpret_cast<const uint4 *>(d_samples);
+  // large calls: the current profile's hot (instruction, slot) bins in shared memory (k_attr.cu)
+  if (prof_code_ok(T, n)) return launch_prof_inst_code(T, d_samples, n, n_prof, d_ph, d_pu, sm_count, st);
   if (T.mode == 0 && n >= 4096) {  // TMA ring, granule -> instruction, one u64 L2 reduction per record
     using RG = RingProf;
     const size_t smem = RG::kBytes + 2 * RG::kStages * 8;

@@ -403,7 +403,8 @@ def test_attribution_shared_counter_overflow_patterns(gpa, attr_kernel, kernel):
 
 
 # ---- f1 at instruction and CCT level ------------------------------------------------------------
-@pytest.mark.parametrize("name,records,n_prof", [("C2", 2_000_000, 5), ("C4", 1_000_003, 64), ("C1", 1000, 0)])
+@pytest.mark.parametrize("name,records,n_prof", [("C2", 2_000_000, 5), ("C4", 1_000_003, 64), ("C1", 1000, 0),
+                                                 ("C4", 6_000_011, 48), ("C3", 4_500_001, 7), ("C5", 5_000_003, 3)])
 def test_profiles_inst_parity(gpa, name, records, n_prof):
     w = gen.workload(name, records=records)
     s = gpa.load_structure(w.structure, 0)
@@ -419,6 +420,23 @@ def test_profiles_inst_parity(gpa, name, records, n_prof):
     assert np.array_equal(u64(PH), Hp) and np.array_equal(u64(PU), Up)
     So = oracle.profile_stats(Hp, n_prof)
     assert np.array_equal(stats.cpu().numpy().view(np.uint64), So.view(np.uint64))
+
+
+def test_profiles_inst_carries_exact(gpa):
+    """Large calls count the current profile's hot bins in shared byte counters: counts of 128-255
+    overflow a byte every one or two records, and the carries are repaid in the cube directly."""
+    w = gen.workload("C5", records=4_400_007)
+    rec = w.records_host()
+    rng = np.random.default_rng(11)
+    rec["count"] = np.where(rng.random(len(rec)) < 0.9, rng.integers(128, 256, len(rec)), rec["count"])
+    s = gpa.load_structure(w.structure, 0)
+    ni, n_prof = s.info["n_inst"], 2
+    PH = torch.zeros((n_prof + 1, ni, 16), dtype=torch.int64, device=DEV)
+    PU = torch.zeros((n_prof + 1, 16), dtype=torch.int64, device=DEV)
+    gpa.attribute_profiles_inst(s, torch.from_numpy(rec.view(np.int64).reshape(-1, 2)).to(DEV), n_prof, PH, PU)
+    torch.cuda.synchronize()
+    Hp, Up = oracle.attribute_profiles_inst(w.structure, rec, n_prof)
+    assert np.array_equal(u64(PH), Hp) and np.array_equal(u64(PU), Up)
 
 
 @pytest.mark.parametrize("name,records,n_prof", [("C4", 2_000_000, 48), ("C3", 3_000_000, 3), ("C2", 500_000, 1)])
