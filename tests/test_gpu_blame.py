@@ -99,3 +99,20 @@ def test_invalid_inputs(gpa):
     tr["n_scopes"] = 2
     with pytest.raises(gpa.GpaError):
         _run(gpa, tr)
+
+
+# ---- larger random ranks: many merge tiles per rank, equal times across and inside lines --------
+@pytest.mark.parametrize("seed", range(8))
+def test_random_large_ranks(gpa, seed):
+    """Ranks of up to 16 lines and up to 60 k change points (several merge tiles per run and
+    merge round), with equal times across lines (t_max small against the event count)."""
+    rng = np.random.default_rng(3000 + seed)
+    _compare(gpa, random_trace(rng, int(rng.integers(1, 4)), max_lines=(8, 9), t_max=int(rng.choice([3000, 200_000])),
+                               max_events=int(rng.choice([300, 4000]))))
+
+
+def test_many_equal_times(gpa):
+    """3000 change points at one timestamp in a line (one merge tile is all ties)."""
+    gpu = [[t, 1 if i % 2 else None] for i, t in enumerate([0] + [10] * 3000 + [20, 30])]
+    cpu = [[0, 0], [5, 1], [15, 0], [25, None], [40, None]]
+    _compare(gpa, from_lines([(2, [("gpu", gpu), ("cpu", cpu), ("cpu", [[1, 1], [35, None]])])]))
