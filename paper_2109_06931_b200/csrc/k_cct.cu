@@ -874,20 +874,22 @@ __global__ void __launch_bounds__(kCoopThreads) k_cct_coop(LevelArgs A, uint32_t
     }
     if (t == 0) bsum[bi] = run;
     grid.sync();
-    if (bi == 0) {  // B: scan the block totals
-      uint32_t running = 0;
-      for (uint32_t base = 0; base < B; base += nt) {
-        uint32_t i = base + t;
-        uint32_t v = i < B ? bsum[i] : 0, tot;
-        uint32_t ex = block_exscan(v, &tot);
-        if (i < B) bsum[i] = running + ex;
-        running += tot;
+    {  // B: every block sums the totals of the blocks before it (block 0 also the level size),
+       // instead of block 0 scanning them behind one more grid barrier
+      uint32_t v = 0, vall = 0, tot, tot2;
+      for (uint32_t i = t; i < B; i += nt) {
+        const uint32_t x = __ldcg(bsum + i);
+        if (i < bi) v += x;
+        vall += x;
       }
-      if (t == 0) lev[L + 2] = b + running;
+      block_exscan(v, &tot);
+      block_exscan(vall, &tot2);
+      if (t == 0) {
+        s_off = tot;
+        if (bi == 0) lev[L + 2] = b + tot2;
+      }
     }
-    grid.sync();
-    if (t == 0) s_off = bsum[bi];  // C: write the children
-    __syncthreads();
+    __syncthreads();  // C: write the children
     for (uint32_t c = c0 + t; c < c1; c += nt) write_children(A, c, (uint64_t)b + s_off + tmp[c - a]);
     grid.sync();
   }
