@@ -1,6 +1,5 @@
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_bt_tile -c 1 -o gpurun_out/bt -f python tools/prof_blame.py 1 > /dev/null 2>&1
-ncu -i gpurun_out/bt.ncu-rep --page source --csv > gpurun_out/bt_src.csv 2>&1
-ncu -i gpurun_out/bt.ncu-rep --page details --csv > gpurun_out/bt_det.csv 2>&1
-ncu -i gpurun_out/bt.ncu-rep --page raw --csv > gpurun_out/bt_raw.csv 2>&1
-rm -f gpurun_out/bt.ncu-rep
-python tools/src_top.py gpurun_out/bt_src.csv 30
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/fin_gputest.log 2>&1; echo rc=$? >> gpurun_out/fin_gputest.log
+timeout 200 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/fin_smoke.log 2>&1
+timeout 600 python bench.py > gpurun_out/fin_bench.log 2>&1
+tail -1 gpurun_out/fin_bench.log > gpurun_out/fin_bench_C5.json
+tail -2 gpurun_out/fin_gputest.log; tail -1 gpurun_out/fin_smoke.log; cat gpurun_out/fin_bench_C5.json
