@@ -84,7 +84,6 @@ __global__ void __launch_bounds__(1024) k_propagate(PropArgs A0) {
     A.q0 = reinterpret_cast<uint32_t *>(A.paths + A.n_dag + 1);
     A.q1 = A.q0 + (A.pstride - A.n_dag - 1);
   }
-  __shared__ int changed;
   __shared__ unsigned long long red[32];
   extern __shared__ __align__(16) uint8_t psm[];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
