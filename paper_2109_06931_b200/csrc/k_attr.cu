@@ -3,8 +3,11 @@
 // and a count"; §4.5 P:475-479 raw metric = sum; §5 P:614-617 disjoint relocated ranges).
 //
 // attr_choice() picks the kernel of a call (numbering of gpa_set_attr_kernel):
-// from max(4e6, 8 x n_inst) records on (granule-map structures) a large-call kernel with a
-// per-call plan (sample -> shared-memory hot set), below that register streaming (1).
+// from 2^20 records K_attr_direct (9) where the whole module fits shared memory (C2); else from
+// max(4e6, 8 x n_inst) records on (granule-map structures) a large-call kernel with a per-call
+// plan (sample -> shared-memory hot set); below that register streaming (1).  A call is one pool
+// allocation, one fill kernel, the plan kernels, the main kernel and one fold (k_fold_all: the
+// CTAs' tables are stored as slabs and summed byte-wise, acc and the granule scratch folded).
 //
 // Why privatise: measured on B200 (tools/microbench.cu), u64 reductions into L2 cost ~1.3 SM
 // cycles of LSU issue per lane (~1.9e11/s at spread addresses), far below the ~4.1e11 records/s
@@ -18,10 +21,12 @@
 //     granules in shared memory (key = the granule) with a row of 12 byte counters each: the record
 //     path has no global load at all (probe, shared atomic or L2 reduction into a granule-indexed
 //     scratch); k_sample_gran / k_place choose the table per plan.
-//  8 K_attr_code32 (larger structures, C5): 131 072 byte-packed (instruction, slot) bins found
+//  8 K_attr_code32 (larger structures, C5): 102 400 byte-packed (instruction, slot) bins found
 //     through a 32-bit per-granule code (base << 12 | hot-slot mask); non-hot records go to the
 //     granule-indexed scratch.  k_sample_bins / k_vhist / k_pick / k_assign_bins / k_codemap32
 //     choose the bins per plan.
+//  9 K_attr_direct (modules of up to ~13.8 k granules, C2): every granule's 12 byte counters in
+//     shared memory, no plan; also k_attr_prof_code (f1 instruction rows with a plan's hot bins).
 //  Byte / half-word counters: a carry out of a packed counter is visible in the atomic's old value
 //  and repaid exactly in L2 (acc), so any count is exact.  Plans are reusable (gpa_attr_plan_*).
 //  3 / 5 / 6 K_attr_bins<32 / 8 / 16>: the round-1 kernel (64-bit code map: instruction + hot
