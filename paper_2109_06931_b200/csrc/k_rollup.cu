@@ -11,6 +11,13 @@
 
 #include "gpa_internal.cuh"
 
+// Blocks per SM of the roll-up grids: short-lived blocks (a few items each) rather than one
+// resident wave, so that the CCT's kernels on the high-priority stream find an SM as soon as a
+// roll-up block retires while the scopes are rolled up concurrently on the side stream.
+#ifndef GPA_ROLL_BLOCKS_PER_SM
+#define GPA_ROLL_BLOCKS_PER_SM 64
+#endif
+
 namespace gpa {
 namespace {
 
@@ -278,7 +285,7 @@ cudaError_t launch_rollup(const RollSet *set, uint32_t rows, const uint64_t *d_h
     cudaMemsetAsync(scratch, 0, (size_t)n_multi * 32 * 8, st);
   }
   uint64_t want = ((uint64_t)items * 4 + 255) / 256;
-  uint64_t cap = (uint64_t)sm_count * 8;
+  uint64_t cap = (uint64_t)sm_count * GPA_ROLL_BLOCKS_PER_SM;
   unsigned blocks = (unsigned)(want < cap ? want : cap);
   k_rollup<<<blocks, 256, 0, st>>>(identity ? nullptr : set->d_chunk + 3ull * c0, identity ? nullptr : set->d_inst,
                                    items, identity ? 1 : 0, identity ? nullptr : set->d_multi_slot, d_hist, d_class,
@@ -318,7 +325,7 @@ cudaError_t launch_rollup_multi(const MultiRoll &M, uint32_t c0, uint32_t c1, ui
     cudaMemsetAsync(scratch, 0, (size_t)n_multi * 32 * 8, st);
   }
   uint64_t want = ((uint64_t)items * 4 + 255) / 256;
-  uint64_t cap = (uint64_t)sm_count * 8;
+  uint64_t cap = (uint64_t)sm_count * GPA_ROLL_BLOCKS_PER_SM;
   unsigned blocks = (unsigned)(want < cap ? want : cap);
   k_rollup_multi<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4 *>(M.d_chunk) + c0, n_chunk, ident_lo, n_ident,
                                          M.d_lst, d_hist, d_class, O, scratch ? scratch - (size_t)m0 * 32 : nullptr);
