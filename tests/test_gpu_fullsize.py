@@ -95,3 +95,41 @@ def test_full_size_histogram_bit_exact(gpa, name):
         assert np.array_equal(sh.cpu().numpy().view(np.uint64)[:k], hist), scope
         assert np.array_equal(sm.cpu().numpy().view(np.uint64)[:k], mix), scope
         assert np.array_equal(fm.cpu().numpy()[:k].view(np.uint64), oracle.derive_u64(hist, mix).view(np.uint64)), scope
+
+
+def test_full_size_profiles_c4(gpa):
+    """f1 at C4's full size in bench_next's launch configuration (1e9 records, 384 profiles, one
+    call each): every profile's instruction rows summed over profiles equal the aggregate H of
+    the same records (integers, exact at any size); four sampled profiles (contiguous record
+    ranges of the stream field) bit-exact against the oracle at instruction and function level."""
+    w = gen.workload("C4")
+    n = w.cfg.records
+    s = gpa.load_structure(w.structure, 0)
+    rec = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+    for k in range(0, n, 1 << 28):
+        w.records_device(rec[k:k + (1 << 28)], k, min(1 << 28, n - k))
+    P, ni, nf = 384, s.info["n_inst"], s.info["n_func"]
+    H = torch.zeros((ni, 16), dtype=torch.int64, device="cuda")
+    U = torch.zeros(16, dtype=torch.int64, device="cuda")
+    gpa.attribute_samples(s, rec, H, U)
+    PH = torch.zeros((P + 1, nf, 16), dtype=torch.int64, device="cuda")
+    PU = torch.zeros((P + 1, 16), dtype=torch.int64, device="cuda")
+    gpa.attribute_profiles(s, rec, P, PH, PU)
+    PI = torch.zeros((P + 1, ni, 16), dtype=torch.int64, device="cuda")
+    PUI = torch.zeros((P + 1, 16), dtype=torch.int64, device="cuda")
+    gpa.attribute_profiles_inst(s, rec, P, PI, PUI)
+    torch.cuda.synchronize()
+    assert torch.equal(PI.sum(0), H) and torch.equal(PUI.sum(0), U)   # int64 sums wrap like u64
+    assert torch.equal(PU, PUI)
+    del rec
+    sfb = w.tables["stream_first_burst"].astype(np.int64)
+    bounds = np.concatenate([np.minimum(sfb << int(w.tables["burst_shift"]), n), [n]])
+    rng = np.random.default_rng(12)
+    for p in [0, P - 1] + [int(x) for x in rng.integers(1, P - 1, 2)]:
+        k0, k1 = int(bounds[p]), int(bounds[p + 1])
+        Ho, Uo, _ = oracle.attribute(w.structure, w.records_host(k0, k1 - k0, threads=len(os.sched_getaffinity(0))),
+                                     threads=len(os.sched_getaffinity(0)))
+        assert np.array_equal(PI[p].cpu().numpy().view(np.uint64), Ho), p
+        assert np.array_equal(PUI[p].cpu().numpy().view(np.uint64), Uo), p
+        Fo, _ = oracle.scope_hist(w.structure, Ho, "FUNC")
+        assert np.array_equal(PH[p].cpu().numpy().view(np.uint64), Fo), p
