@@ -57,18 +57,28 @@ __global__ void k_union_inputs(uint32_t P, uint32_t n_func, uint32_t n_call, uin
                                const uint32_t *__restrict__ scc_of, const uint8_t *__restrict__ fact,
                                const uint8_t *__restrict__ dact, const uint64_t *__restrict__ w,
                                uint64_t *__restrict__ S_u, uint64_t *__restrict__ w_u) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per function / call site, its lanes striding the profiles
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t < n_func) {
     const uint32_t X = scc_of[t];
-    uint8_t a = 0;
-    for (uint32_t p = 0; p < P; p++) a |= fact[p * fs + t] | dact[p * ds + X];
-    for (int r = 0; r < GPA_SLOTS; r++) S_u[(uint64_t)t * GPA_SLOTS + r] = (r == 0 && a) ? 1ull : 0ull;
+    uint32_t a = 0;
+    for (uint32_t p = lane; p < P; p += 32) a |= fact[p * fs + t] | dact[p * ds + X];
+    a = __any_sync(0xFFFFFFFFu, a != 0);
+    if (lane < GPA_SLOTS) S_u[(uint64_t)t * GPA_SLOTS + lane] = (lane == 0 && a) ? 1ull : 0ull;
   }
   if (t < n_call) {
     bool any = false;
-    for (uint32_t p = 0; p < P; p++) any = any || w[(uint64_t)p * n_call + t] != 0;
-    w_u[t] = any ? 1ull : 0ull;
+    for (uint32_t p = lane; p < P; p += 32) any = any || w[(uint64_t)p * n_call + t] != 0;
+    any = __any_sync(0xFFFFFFFFu, any);
+    if (lane == 0) w_u[t] = any ? 1ull : 0ull;
   }
+}
+
+// does any profile mark union context c present?  (all lanes of the warp, the result in all)
+__device__ __forceinline__ bool warp_any_present(const uint8_t *__restrict__ pres, uint64_t c, uint32_t P) {
+  uint32_t a = 0;
+  for (uint32_t p = threadIdx.x & 31; p < P; p += 32) a |= pres[c * P + p];
+  return __any_sync(0xFFFFFFFFu, a != 0);
 }
 
 struct MultiArgs {
@@ -114,10 +124,10 @@ __global__ void k_multi_frac(MultiArgs A, uint64_t a, uint64_t b) {
 
 // any-profile flag per union context (the scan input)
 __global__ void k_multi_any(const uint8_t *__restrict__ pres, uint64_t n, uint32_t P, uint32_t *__restrict__ flag) {
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t a = 0;
-    for (uint32_t p = 0; p < P; p++) a |= pres[c * P + p];
-    flag[c] = a ? 1u : 0u;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;  // one warp per context
+  for (uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n; c += nw) {
+    const bool a = warp_any_present(pres, c, P);
+    if ((threadIdx.x & 31) == 0) flag[c] = a ? 1u : 0u;
   }
 }
 
@@ -134,30 +144,32 @@ struct CompactArgs {
 };
 
 __global__ void k_multi_compact(CompactArgs A) {
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < A.n; c += (uint64_t)gridDim.x * blockDim.x) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;  // one warp per context
+  for (uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < A.n; c += nw) {
+    if (!warp_any_present(A.pres, c, A.P)) continue;
     const uint32_t u = A.uid[c];
-    bool any = false;
-    for (uint32_t p = 0; p < A.P; p++) any = any || A.pres[c * A.P + p];
-    if (!any) continue;
-    const uint32_t pc = A.parent[c];
-    A.u_parent[u] = pc == NONE ? NONE : A.uid[pc];
-    A.u_site[u] = A.site[c];
-    A.u_node[u] = A.node[c];
-    A.u_kind[u] = A.kind[c];
-    for (uint32_t p = 0; p < A.P; p++) A.u_frac[(uint64_t)u * A.P + p] = A.frac[c * A.P + p];
+    if (lane == 0) {
+      const uint32_t pc = A.parent[c];
+      A.u_parent[u] = pc == NONE ? NONE : A.uid[pc];
+      A.u_site[u] = A.site[c];
+      A.u_node[u] = A.node[c];
+      A.u_kind[u] = A.kind[c];
+    }
+    for (uint32_t p = lane; p < A.P; p += 32) A.u_frac[(uint64_t)u * A.P + p] = A.frac[c * A.P + p];
     // present children are a contiguous run of unified ids: the first present child of c
     const uint32_t d0 = A.first_child[c], nc = A.n_children[c];
     uint32_t cnt = 0, first = NONE;
     for (uint32_t d = d0; d < d0 + nc; d++) {
-      bool dp = false;
-      for (uint32_t p = 0; p < A.P && !dp; p++) dp = A.pres[(uint64_t)d * A.P + p];
-      if (dp) {
+      if (warp_any_present(A.pres, d, A.P)) {
         if (first == NONE) first = A.uid[d];
         cnt++;
       }
     }
-    A.u_first_child[u] = first == NONE ? 0u : first;
-    A.u_n_children[u] = cnt;
+    if (lane == 0) {
+      A.u_first_child[u] = first == NONE ? 0u : first;
+      A.u_n_children[u] = cnt;
+    }
   }
 }
 
@@ -224,7 +236,8 @@ cudaError_t launch_union_inputs(const gpa_structure_s *s, uint32_t P, const uint
   const uint32_t n_func = s->info.n_func, n_call = s->info.n_call;
   const uint32_t m = n_func > n_call ? n_func : n_call;
   if (m == 0) return cudaSuccess;
-  k_union_inputs<<<(m + 255) / 256, 256, 0, st>>>(P, n_func, n_call, fs, ds, s->d_scc_of, fact, dact, w, S_u, w_u);
+  k_union_inputs<<<(unsigned)(((uint64_t)m * 32 + 255) / 256), 256, 0, st>>>(P, n_func, n_call, fs, ds, s->d_scc_of, fact,
+                                                                           dact, w, S_u, w_u);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -241,7 +254,7 @@ cudaError_t launch_multi_tree(const gpa_structure_s *s, const gpa_cct_s *sup, ui
       count_launches(1);
     }
   }
-  k_multi_any<<<grid_of(sup->n), 256, 0, st>>>(pres, sup->n, P, flag);
+  k_multi_any<<<grid_of(sup->n * 32), 256, 0, st>>>(pres, sup->n, P, flag);
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -252,7 +265,7 @@ cudaError_t launch_multi_compact(const gpa_cct_s *sup, uint32_t P, const uint8_t
                                  const double *frac, gpa_cct_multi_s *m, cudaStream_t st) {
   CompactArgs A{sup->n, P, sup->parent, sup->site, sup->node, sup->first_child, sup->n_children, sup->kind, pres, uid,
                 frac, m->parent, m->site, m->node, m->first_child, m->n_children, m->kind, m->frac};
-  k_multi_compact<<<grid_of(sup->n), 256, 0, st>>>(A);
+  k_multi_compact<<<grid_of(sup->n * 32), 256, 0, st>>>(A);
   count_launches(1);
   return cudaGetLastError();
 }
