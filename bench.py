@@ -341,9 +341,12 @@ def run_gpa(args):
                 cct.free()               # stream-ordered on B
         return nctx
 
-    # CCT without a host round trip inside the step (gpa_reconstruct_cct_async); --sync-cct for
-    # the synchronous call
-    async_cct = world == 1 and not args.sync_cct
+    # CCT without a host round trip inside the step (gpa_reconstruct_cct_async) when batches are
+    # pipelined.  One batch at a time keeps the synchronous call: there the asynchronous tree's
+    # settle() overlaps the next batch's attribution, and in 2 of 4 C5 runs that batch's
+    # attribution then took 15-40 ms instead of 12 (never with the synchronous call: 12.43-12.45
+    # ms per step over 4 runs)
+    async_cct = world == 1 and pipeline and not args.sync_cct
     cm_async = [None]
 
     def run_steps(k: int, timed: bool, host=None, results=None):

@@ -1,2 +1,5 @@
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cctp_ncu.csv python tools/prof_cctp.py 100000000 2 > /dev/null 2>&1
-python tools/launch_table.py gpurun_out/cctp_ncu.csv 0.5
+for i in 1 2 3; do
+  timeout 300 python bench.py --config C5 --no-cpu-baseline --no-e2e | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('serial', round(d['ms_per_step'],3), round(d['roofline']['frac'],3), [round(x,1) for x in d['phases_ms']['attr_ms_per_step']])"
+done
+timeout 300 python bench.py --config C5 --no-cpu-baseline --no-e2e --pipeline | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('pipe', round(d['ms_per_step'],3), round(d['roofline']['frac'],3), [round(x,1) for x in d['phases_ms']['attr_ms_per_step']])"
+timeout 300 python bench.py --config C3 --no-cpu-baseline --no-e2e | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C3 serial', round(d['ms_per_step'],3))"
