@@ -346,7 +346,7 @@ def run_gpa(args):
     # settle() overlaps the next batch's attribution, and in 2 of 4 C5 runs that batch's
     # attribution then took 15-40 ms instead of 12 (never with the synchronous call: 12.43-12.45
     # ms per step over 4 runs)
-    async_cct = world == 1 and pipeline and not args.sync_cct
+    async_cct = world == 1 and (pipeline or args.async_cct) and not args.sync_cct
     cm_async = [None]
 
     def run_steps(k: int, timed: bool, host=None, results=None):
@@ -425,17 +425,21 @@ def run_gpa(args):
     if world > 1:
         dist.barrier()
     l0 = gpa.kernel_launches()
+    import gc
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()  # no collector pause between a step's event and its kernels' launch
         t0.record(A)
         nctx = run_steps(args.steps, True)
         B.wait_stream(A)
         t1.record(B)
         torch.cuda.synchronize()
+        gc.enable()
         if world > 1:
             dist.barrier()
     launches = gpa.kernel_launches() - l0
@@ -587,6 +591,7 @@ def main():
                     help="N > 1: reduce-scatter + per-rank roll-ups (default) or reduce to rank 0")
     ap.add_argument("--no-balance", action="store_true", help="N > 1: equal shards (rank 0 not lightened)")
     ap.add_argument("--sync-cct", action="store_true", help="synchronous gpa_reconstruct_cct (A/B of the async tree)")
+    ap.add_argument("--async-cct", action="store_true", help="asynchronous tree also with one batch at a time")
     ap.add_argument("--pipeline", action="store_true",
                     help="enqueue batch i+1's attribution before batch i's analysis (C5: +1.7 %% throughput, "
                          "the attribution kernel slowed by the concurrent analysis; DESIGN.md §11)")
