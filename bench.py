@@ -376,13 +376,20 @@ def run_gpa(args):
                 return 0
             return r
 
+        dbg = timed and os.environ.get("GPA_BENCH_HOSTTIME")
         for i in range(k):
+            h0 = time.perf_counter()
             enqueue_attr(i, timed, host)
+            h1 = time.perf_counter()
             nctx = settle() or nctx
+            h2 = time.perf_counter()
             if not pipeline:
                 nctx = keep(analyse(i, timed, results))
             elif i > 0:
                 nctx = keep(analyse(i - 1, timed, results))
+            if dbg:
+                print(f"step {i}: enqueue {1e3 * (h1 - h0):.3f} ms, settle {1e3 * (h2 - h1):.3f} ms, analyse "
+                      f"{1e3 * (time.perf_counter() - h2):.3f} ms", file=sys.stderr)
         if pipeline and k > 0:
             nctx = settle() or nctx
             nctx = keep(analyse(k - 1, timed, results))

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include "gpa.h"
@@ -40,6 +41,8 @@ static uint64_t pool_keep() {
 
 // return reserved pool memory above the release threshold to the driver (after large frees)
 static void pool_trim(int dev) {
+  static const bool off = getenv("GPA_POOL_NO_TRIM") != nullptr;  // (diagnostics)
+  if (off) return;
   std::lock_guard<std::mutex> lock(g_pool_mu);
   if (dev >= 0 && dev < 64 && g_pools[dev]) cudaMemPoolTrimTo(g_pools[dev], pool_keep());
 }
@@ -72,7 +75,13 @@ cudaError_t gpa::pool_alloc(void **p, size_t bytes, cudaStream_t st) {
       cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
-  return cudaMallocFromPoolAsync(p, bytes, pools[dev], st);
+  static const bool dbg = getenv("GPA_DEBUG_POOL") != nullptr;  // (diagnostics) slow pool calls
+  if (!dbg) return cudaMallocFromPoolAsync(p, bytes, pools[dev], st);
+  const auto t0 = std::chrono::steady_clock::now();
+  e = cudaMallocFromPoolAsync(p, bytes, pools[dev], st);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (ms > 0.5) fprintf(stderr, "gpa pool_alloc %zu bytes: %.3f ms\n", bytes, ms);
+  return e;
 }
 
 static gpa_status fail(gpa_status st, const char *fmt, ...) {
