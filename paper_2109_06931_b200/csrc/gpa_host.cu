@@ -297,9 +297,11 @@ gpa_status upload(gpa_structure_s *s, T **dptr, const T *h, size_t n) {
 void free_structure(gpa_structure_s *s) {
   if (!s) return;
   DeviceGuard g(s->device);
+  scratch_release(&s->scratch);
   for (void *p : s->allocs) cudaFree(p);
   delete s;
 }
+
 
 gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s *s) {
   const uint32_t ni = d->n_inst, ns = d->n_scope, nf = d->n_func, nc = d->n_call;
@@ -321,6 +323,7 @@ gpa_status build(const gpa_structure_desc *d, const Derived &dv, gpa_structure_s
   UP(s->d_inst_len, len);
   UP(s->d_inst_class, cls);
   AttrTables &T = s->attr;
+  T.cache = &s->scratch;
   T.n_inst = ni;
   T.inst_addr = s->d_inst_addr;
   T.inst_len = s->d_inst_len;
@@ -692,6 +695,62 @@ static cudaError_t calloc_dev(gpa_cct_s *c, T **p, size_t n) {
   if (e == cudaSuccess) c->allocs.push_back(*p);
   return e;
 }
+
+namespace gpa {
+cudaError_t scratch_get(ScratchCache *c, size_t bytes, cudaStream_t st, void **out, bool *cached) {
+  *cached = false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) c = nullptr;  // graphs: pool
+  if (c) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (!c->busy) {
+      cudaError_t e = cudaSuccess;
+      if (!c->done) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
+      if (e == cudaSuccess && c->bytes < bytes) {  // grow: the old block is released after its last use
+        if (c->mem) {
+          if (c->last && c->last != st) cudaStreamWaitEvent(st, c->done, 0);
+          cudaFreeAsync(c->mem, st);
+          c->mem = nullptr;
+          c->bytes = 0;
+          c->last = st;
+        }
+        e = pool_alloc(&c->mem, bytes, st);
+        if (e == cudaSuccess) c->bytes = bytes;
+      }
+      if (e == cudaSuccess && c->mem) {
+        if (c->last && c->last != st) e = cudaStreamWaitEvent(st, c->done, 0);
+        c->busy = true;
+        *out = c->mem;
+        *cached = true;
+        return e;
+      }
+      cudaGetLastError();
+    }
+  }
+  return pool_alloc(out, bytes, st);
+}
+
+cudaError_t scratch_put(ScratchCache *c, void *p, bool cached, cudaStream_t st) {
+  if (!cached) return cudaFreeAsync(p, st);
+  std::lock_guard<std::mutex> lock(c->mu);
+  cudaError_t e = cudaEventRecord(c->done, st);
+  c->last = st;
+  c->busy = false;
+  return e;
+}
+
+void scratch_release(ScratchCache *c) {
+  std::lock_guard<std::mutex> lock(c->mu);
+  if (c->mem) {
+    if (c->done) cudaEventSynchronize(c->done);
+    cudaFree(c->mem);
+  }
+  if (c->done) cudaEventDestroy(c->done);
+  c->mem = nullptr;
+  c->done = nullptr;
+  c->bytes = 0;
+}
+}  // namespace gpa
 
 extern "C" {
 

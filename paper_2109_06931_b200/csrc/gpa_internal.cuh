@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -19,6 +20,22 @@ constexpr int NCOLS = GPA_NUM_DERIVED;
 enum { ROLL_LINE = 0, ROLL_LOOP = 1, ROLL_INLINE = 2, ROLL_FUNC = 3, ROLL_KINDS = 4 };
 
 // Tables the attribution kernel reads (passed by value as a kernel parameter).
+// One device block reused by consecutive attribution calls on a structure (the per-call scratch:
+// plan, accumulators, CTA slabs), so a call makes no pool allocation: a call on another stream
+// than the previous one first waits for that call's event.  A call that finds it busy (another
+// host thread) or too small allocates from the pool as before.
+struct ScratchCache {
+  std::mutex mu;
+  void *mem = nullptr;
+  size_t bytes = 0;
+  bool busy = false;
+  cudaStream_t last = nullptr;
+  cudaEvent_t done = nullptr;
+};
+cudaError_t scratch_get(ScratchCache *c, size_t bytes, cudaStream_t st, void **out, bool *cached);
+cudaError_t scratch_put(ScratchCache *c, void *p, bool cached, cudaStream_t st);
+void scratch_release(ScratchCache *c);
+
 struct AttrTables {
   uint64_t base;          // first instruction start
   uint64_t end;           // last instruction end (exclusive)
@@ -29,6 +46,7 @@ struct AttrTables {
   const uint64_t *inst_addr;
   const uint16_t *inst_len;
   uint32_t n_inst;
+  ScratchCache *cache;    // host side: the structure's reusable call scratch (never read by kernels)
 };
 
 constexpr uint32_t kRollChunk = 32;  // instructions per roll-up work item
@@ -66,6 +84,7 @@ struct gpa_structure_s {
   int device = 0;
   gpa_structure_info info{};
   gpa::AttrTables attr{};
+  gpa::ScratchCache scratch;  // attr.cache
   // device tables
   uint64_t *d_inst_addr = nullptr;
   uint16_t *d_inst_len = nullptr;

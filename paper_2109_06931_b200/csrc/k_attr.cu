@@ -1638,7 +1638,8 @@ cudaError_t launch_planned(const AttrTables &T, int variant, const uint4 *rec, u
   p.n_gran = T.n_gran;
   const size_t b0 = al256(plan_bytes(T, variant)), b1 = build_bytes(T, variant), b2 = acc_bytes(p, sm_count);
   uint8_t *mem = nullptr;
-  cudaError_t e = pool_alloc((void **)&mem, b0 + b1 + b2, st);
+  bool cached = false;  // the structure's reusable scratch (no pool call), else a pool block
+  cudaError_t e = scratch_get(T.cache, b0 + b1 + b2, st, (void **)&mem, &cached);
   if (e != cudaSuccess) return e;
   plan_ptrs(T, variant, mem, &p);
   AttrAcc a;
@@ -1650,7 +1651,7 @@ cudaError_t launch_planned(const AttrTables &T, int variant, const uint4 *rec, u
   if (e == cudaSuccess) e = build_kernels(T, p, rec, n, mem + b0, sm_count, st);
   if (e == cudaSuccess) e = plan_launch(T, p, a, rec, n, ri, sm_count, st, false);
   if (e == cudaSuccess) e = plan_fold_final(T, p, a, (p.variant != 8 || GPA_CODE_PACK) ? sm_count : 0, H, U, sm_count, st);
-  cudaError_t e2 = cudaFreeAsync(mem, st);
+  cudaError_t e2 = scratch_put(T.cache, mem, cached, st);
   return e != cudaSuccess ? e : e2;
 }
 
