@@ -556,3 +556,46 @@ def test_ring_stress_exact(gpa, attr_kernel, kernel, stress):
     Ho, Uo, rio = oracle.attribute(w.structure, w.records_host(), rec_inst=True)
     assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
     assert np.array_equal(ri.cpu().numpy().view(np.uint32), rio)
+
+
+def test_scratch_reuse_across_streams(gpa):
+    """Consecutive attribution calls on one structure reuse its scratch block (ScratchCache); calls
+    alternating between two streams (the second waits on the first's event) and a call from a
+    second host thread while one is being enqueued stay bit-exact."""
+    import threading
+    w = gen.workload("C2", records=3_000_000)
+    s = gpa.load_structure(w.structure, 0)
+    rec = _device_records(w)
+    Ho, Uo, _ = oracle.attribute(w.structure, w.records_host())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i in range(6):
+        H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device=DEV)
+        U = torch.zeros(16, dtype=torch.int64, device=DEV)
+        st = streams[i % 2]
+        st.wait_stream(torch.cuda.current_stream())
+        gpa.attribute_samples(s, rec, H, U, stream=st)
+        outs.append((H, U))
+    errs = []
+
+    def worker():
+        try:
+            H = torch.zeros((s.info["n_inst"], 16), dtype=torch.int64, device=DEV)
+            U = torch.zeros(16, dtype=torch.int64, device=DEV)
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            gpa.attribute_samples(s, rec, H, U, stream=st)
+            st.synchronize()
+            outs.append((H, U))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker) for _ in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs
+    for H, U in outs:
+        assert np.array_equal(u64(H), Ho) and np.array_equal(u64(U), Uo)
