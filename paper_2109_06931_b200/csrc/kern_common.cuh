@@ -291,7 +291,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t *v, uint64_
 // next tile by ticket, publishes its aggregate, then warp 0 walks back over the predecessors'
 // published (aggregate | inclusive) words 32 at a time until it meets an inclusive prefix, and
 // publishes its own inclusive prefix.  One read and one write per element.
-constexpr int kLbThreads = 512, kLbItems = 8, kLbTile = kLbThreads * kLbItems;
+#ifndef GPA_SCAN_ITEMS
+#define GPA_SCAN_ITEMS 24  // 8: f4 on B3 2.36 ms, 16: 2.30, 24: 2.27 (fewer tiles in the look-back chain)
+#endif
+constexpr int kLbThreads = 512, kLbItems = GPA_SCAN_ITEMS, kLbTile = kLbThreads * kLbItems;
+static_assert(kLbItems % 4 == 0, "scan items per thread: whole 16-B vectors");
 
 __global__ void __launch_bounds__(kLbThreads) k_scan_lb(uint32_t *__restrict__ v, uint64_t m,
                                                        unsigned long long *state, uint32_t *ctr,
@@ -304,8 +308,11 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lb(uint32_t *__restrict__ v
   const uint64_t i0 = (uint64_t)tile * kLbTile + (uint64_t)threadIdx.x * kLbItems;
   uint32_t x[kLbItems], sum = 0;
   if (i0 + kLbItems <= m) {
-    const uint4 a = *reinterpret_cast<const uint4 *>(v + i0), b = *reinterpret_cast<const uint4 *>(v + i0 + 4);
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+#pragma unroll
+    for (int k4 = 0; k4 < kLbItems / 4; k4++) {
+      const uint4 a = *reinterpret_cast<const uint4 *>(v + i0 + 4 * k4);
+      x[4 * k4] = a.x; x[4 * k4 + 1] = a.y; x[4 * k4 + 2] = a.z; x[4 * k4 + 3] = a.w;
+    }
   } else {
 #pragma unroll
     for (int q = 0; q < kLbItems; q++) x[q] = i0 + q < m ? v[i0 + q] : 0;
@@ -348,8 +355,9 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lb(uint32_t *__restrict__ v
       y[q] = run;
       run += x[q];
     }
-    *reinterpret_cast<uint4 *>(v + i0) = make_uint4(y[0], y[1], y[2], y[3]);
-    *reinterpret_cast<uint4 *>(v + i0 + 4) = make_uint4(y[4], y[5], y[6], y[7]);
+#pragma unroll
+    for (int k4 = 0; k4 < kLbItems / 4; k4++)
+      *reinterpret_cast<uint4 *>(v + i0 + 4 * k4) = make_uint4(y[4 * k4], y[4 * k4 + 1], y[4 * k4 + 2], y[4 * k4 + 3]);
   } else {
 #pragma unroll
     for (int q = 0; q < kLbItems; q++)
